@@ -1,0 +1,238 @@
+/*
+ * sqz.h -- C ABI of libsqz.so, the B200-native (sm_100a) hot path of
+ * Squeezed Attention (Hooper et al., arXiv 2411.09688).
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX source; readings R<k> are
+ * listed in DESIGN.md.  The online path is two steps:
+ *   1. sqz_centroid_lookup  -- Eq. 1-3 centroid scoring + global threshold
+ *       -> per-(b,h) selected clusters and the "tensor
+ *      of key indices that need to be selectively loaded";
+ *   2. sqz_sparse_attention -- exact attention over the selected fixed-context
+ *      keys plus the dense user KV, split-KV with a merge.
+ * sqz_cluster_keys is the offline step.
+ *
+ * Conventions (all entry points)
+ *   - Every tensor argument is CALLER-OWNED DEVICE memory (cudaMalloc /
+ *     torch), row-major with the last dimension contiguous; strides are
+ *     implied by the shapes given.  The library never allocates device memory
+ *     and never copies to the host on the online path.
+ *   - Per-head tables are laid out [H, ...]; queries and user KV [B, H, ...].
+ *   - "stream" is a cudaStream_t passed as void*; every online call only
+ *     enqueues work on it (no host synchronisation).
+ *   - Scratch: every call that needs scratch takes (ws, ws_bytes); the size is
+ *     given by the matching *_workspace() query.  Workspaces must be zeroed
+ *     ONCE before first use (sqz_workspace_init); the library leaves its
+ *     counters zeroed again when each call completes, so a workspace can be
+ *     reused by consecutive calls on the same stream (not concurrently).
+ *   - Return codes: SQZ_OK, or an error code; sqz_last_error() returns a
+ *     thread-local message naming the offending argument.  Argument errors
+ *     are detected on the host before anything is enqueued.
+ */
+#ifndef SQZ_H
+#define SQZ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SQZ_ABI_VERSION 1
+
+enum {
+    SQZ_OK = 0,
+    SQZ_ERR_INVALID_ARG = 2, /* shape / dtype / nullptr / T < 0 or NaN / c > L          */
+    SQZ_ERR_FORMAT = 3,      /* malformed index tables                                   */
+    SQZ_ERR_INVARIANT = 4,   /* tables violate sum N = L, perm not a permutation, ...    */
+    SQZ_ERR_CUDA = 5,        /* a CUDA runtime call failed (message has the CUDA error)  */
+    SQZ_ERR_EMPTY = 7,       /* a final (non-partial) output row attended no key         */
+    SQZ_ERR_UNSUPPORTED = 8  /* valid but not supported by this build (e.g. d not 64/128) */
+};
+
+typedef enum { SQZ_F32 = 0, SQZ_BF16 = 1 } sqz_dtype;
+
+/* ---------------------------------------------------------------------- */
+/* Index: per-head centroid tables and the cluster-major key layout (D1-D4) */
+/* ---------------------------------------------------------------------- */
+/* The fixed-context K/V are stored permuted into cluster-major order: the
+ * keys of Level-2 cluster i occupy positions [key_off[h][i], key_off[h][i+1])
+ * of Kp[h] / Vp[h], and perm[h][pos] is the original key index of position
+ * pos.  This is legal because fixed-context keys are all visible to every
+ * query (no causal mask within the fixed context), so attention is
+ * permutation-invariant over them.  With two levels, Level-2 clusters are
+ * numbered grouped by their Level-1 parent: the children of Level-1 cluster p
+ * are Level-2 ids [child_off[h][p], child_off[h][p+1]).
+ *
+ *   field      shape        type              meaning
+ *   C2         [H, c2, d]   dtype             Level-2 (finest) centroids C_i (R2)
+ *   N2         [H, c2]      int32             keys per Level-2 cluster, N_i (Eq. 1)
+ *   key_off    [H, c2 + 1]  int32             cluster-major key ranges
+ *   perm       [H, L]       int32             position -> original key index
+ *   C1         [H, c1, d]   dtype             Level-1 centroids (levels == 2)
+ *   N1         [H, c1]      int32             descendant keys of each Level-1 cluster (R4)
+ *   child_off  [H, c1 + 1]  int32             Level-2 children ranges (levels == 2)
+ * Single level: levels = 1, c1 = 0, C1/N1/child_off = NULL. */
+typedef struct {
+    int32_t H;       /* heads                                  */
+    int32_t d;       /* head dimension: 64 or 128              */
+    int64_t L;       /* fixed-context keys per head            */
+    int32_t levels;  /* 1 or 2                                 */
+    int32_t c1;      /* Level-1 clusters (0 when levels == 1)  */
+    int32_t c2;      /* Level-2 / single-level clusters        */
+    int32_t dtype;   /* sqz_dtype of C1, C2 (and of K, V, Q)   */
+    void *C1;
+    int32_t *N1;
+    int32_t *child_off;
+    void *C2;
+    int32_t *N2;
+    int32_t *key_off;
+    int32_t *perm;
+} sqz_index;
+
+/* ---------------------------------------------------------------------- */
+/* Offline: K-means key clustering (section 3.1; section 3.3       */
+/* P:244-247; Fig. 2)                                            */
+/* ---------------------------------------------------------------------- */
+typedef struct {
+    int32_t max_iters; /* Lloyd iterations per level (e.g. 50)                       */
+    float tol;         /* stop when the max centroid shift < tol (e.g. 1e-4)         */
+} sqz_kmeans_params;
+
+/* Workspace bytes for sqz_cluster_keys with the index geometry in *idx. */
+int sqz_cluster_keys_workspace(const sqz_index *idx, size_t *ws_bytes);
+
+/* Clusters the keys of every head and writes the index tables and the
+ * cluster-major copies of K and V.
+ *   K, V   [H, L, d] dtype, ORIGINAL key order (read only)
+ *   init2  [H, c2] int64 device: seeded initial subset for Level 2 (R3)
+ *   init1  [H, c1] int64 device: initial subset of the Level-2 centroids for
+ *          Level 1 (levels == 2), else NULL
+ *   idx    geometry fields (H, d, L, levels, c1, c2, dtype) set by the caller;
+ *          every table pointer must point to caller-allocated device memory of
+ *          the shape above; all tables are written.
+ *   Kp, Vp [H, L, d] dtype outputs (cluster-major copies)
+ *   iters_out optional HOST int32[2]: max Lloyd iterations over heads used by
+ *          Level 2 and Level 1.
+ * Algorithm: Lloyd on unit-normalised keys (assignment argmin ||x^ - mu||^2,
+ * ties to the lowest id; farthest-point repair of empty clusters; update =
+ * mean of member x^), then C_i = mean of the RAW member keys rounded once to
+ * dtype; Level 1 clusters the stored C2 rows, C1 = unweighted mean of child
+ * rows, N1 = descendant keys.  This is the only call that synchronises the
+ * stream (once per Lloyd iteration, to test convergence). */
+int sqz_cluster_keys(const void *K, const void *V, const int64_t *init2, const int64_t *init1,
+                     sqz_index *idx, void *Kp, void *Vp, const sqz_kmeans_params *p, void *ws,
+                     size_t ws_bytes, int32_t *iters_out, void *stream);
+
+/* Checks the index invariants on the device (sum N2 = L, key_off consistent
+ * with N2, perm a permutation of [0, L), child_off a partition of [0, c2),
+ * N1 = descendant keys).  Synchronises the stream.  SQZ_ERR_INVARIANT on
+ * failure.  ws: sqz_index_validate_workspace() bytes. */
+int sqz_index_validate_workspace(const sqz_index *idx, size_t *ws_bytes);
+int sqz_index_validate(const sqz_index *idx, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Online step 1: centroid lookup (Eq. 1-3; section 4.1)          */
+/* ---------------------------------------------------------------------- */
+typedef struct {
+    float scale; /* logit scale s_i = scale * q.C_i; 1/sqrt(d) default (R1)          */
+    float T;     /* global threshold (finest level), T >= 0; T == 0 selects all (R6)  */
+    float T1;    /* Level-1 threshold (levels == 2), T1 >= 0                         */
+} sqz_lookup_params;
+
+/* Outputs of the lookup, caller-allocated device memory.
+ *   clusters   [B, H, c2] int32: ascending selected finest-level cluster ids;
+ *              the first n_clusters[b,h] entries are valid
+ *   n_clusters [B, H] int32
+ *   n_keys     [B, H] int32: k = sum of N_i over the selected clusters
+ *   key_idx    [B, H, L] int32: cluster-major positions (into Kp/Vp) of the
+ *              selected keys, ascending; the first n_keys[b,h] are valid.
+ *              This is the paper's key-index tensor.
+ *   l1_surv    optional [B, H, c1] uint8: Level-1 survivors (levels == 2)
+ *   dbg_S      optional [B, H, c2] fp32: finest-level S_i (decode) or S-bar_i
+ *              (prefill) as the kernel evaluated it, NaN for rows not scanned
+ *   dbg_S1     optional [B, H, c1] fp32: Level-1 S^(1) / S-bar^(1)
+ *   dbg_lse    optional [B, H, n_q] fp32: finest-level log denominator per query
+ *              (log sum_j N_j exp(s_j) over the scanned rows; -inf if none) */
+typedef struct {
+    int32_t *clusters;
+    int32_t *n_clusters;
+    int32_t *n_keys;
+    int32_t *key_idx;
+    uint8_t *l1_surv;
+    float *dbg_S;
+    float *dbg_S1;
+    float *dbg_lse;
+} sqz_selection;
+
+int sqz_lookup_workspace(const sqz_index *idx, int32_t B, int32_t n_q, size_t *ws_bytes);
+
+/* Q [B, H, n_q, d] dtype.  n_q == 1 is the generation stage: per
+ * (b,h) the cluster i is selected iff S_i > T, evaluated as
+ * (s_i - m) > log D + log T with m = max_j s_j, D = sum_j N_j exp(s_j - m)
+ * (the paper's single-pass form with the max folded into the threshold,
+ * P:775-776).  n_q > 1 is the prefill stage: S-bar_i =
+ * (1/n_q) sum_t S_{t,i}, selected iff S-bar_i > T, one selection per (b,h)
+ * shared by its n_q queries (R7).  levels == 2: Level-1 scores with N1 against
+ * T1, survivors expanded to their children, Level-2 scores with the
+ * denominator restricted to those children (Eq. 3), against T. */
+int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t n_q,
+                        const sqz_lookup_params *p, const sqz_selection *out, void *ws,
+                        size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Online step 2: sparse attention (section 4.2)                  */
+/* ---------------------------------------------------------------------- */
+typedef struct {
+    float scale;       /* z = scale * q.k (1/sqrt(d))                                      */
+    int32_t causal;    /* 1: user key u visible to query t iff u <= t + n_u - n_q (R8)       */
+    int32_t partial;   /* 1: rows with no attended key give O = 0, LSE = -inf (identity     */
+                       /*    partial for a later merge); 0: such rows are an error,          */
+                       /*    reported by sqz_attention_status()                              */
+    int32_t out_dtype; /* sqz_dtype of O                                                     */
+} sqz_attn_params;
+
+int sqz_attention_workspace(const sqz_index *idx, int32_t B, int32_t n_q, int32_t n_u,
+                            size_t *ws_bytes);
+
+/* Q [B,H,n_q,d] dtype; Kp, Vp [H,L,d] dtype (cluster-major); sel: output of
+ * sqz_centroid_lookup (n_keys and key_idx are read); Ku, Vu [B,H,n_u,d] dtype
+ * (may be NULL when n_u == 0).  Outputs: O [B,H,n_q,d] out_dtype and
+ * LSE [B,H,n_q] fp32 = natural-log sum of exp(z) over the attended keys.
+ * For each query row the attended set is the selected fixed keys of its (b,h)
+ * plus the visible user keys; O is the exact softmax-weighted sum of their
+ * values.  Work is split into fixed-size key chunks ("a fixed number of ...
+ * keys ... for a single SM") whose partials are merged. */
+int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, const void *Vp,
+                         const sqz_index *idx, const sqz_selection *sel, const void *Ku,
+                         const void *Vu, int32_t n_u, const sqz_attn_params *p, void *O,
+                         float *LSE, void *ws, size_t ws_bytes, void *stream);
+
+/* Synchronises the stream and returns SQZ_ERR_EMPTY if the last non-partial
+ * sqz_sparse_attention on this workspace produced a row with no attended key
+ * (and clears the flag), else SQZ_OK. */
+int sqz_attention_status(void *ws, size_t ws_bytes, void *stream);
+
+/* Merge of P partial results:
+ *   O_parts [P, rows, d] fp32, LSE_parts [P, rows] fp32 (natural log; -inf =
+ *   identity partial)  ->  O [rows, d] out_dtype, LSE [rows] fp32 with
+ *   LSE = log sum_p exp(LSE_p), O = sum_p exp(LSE_p - LSE) O_p. */
+int sqz_merge_partials(int32_t P, const float *O_parts, const float *LSE_parts, int64_t rows,
+                       int32_t d, void *O, float *LSE, int32_t out_dtype, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Misc                                                                      */
+/* ---------------------------------------------------------------------- */
+/* Zero a workspace (cudaMemsetAsync) before its first use. */
+int sqz_workspace_init(void *ws, size_t ws_bytes, void *stream);
+/* Thread-local message describing the last error returned on this thread. */
+const char *sqz_last_error(void);
+/* SQZ_ABI_VERSION of the loaded library. */
+int sqz_abi_version(void);
+/* SQZ_OK iff the current device is an sm_100 part the library was built for. */
+int sqz_device_check(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SQZ_H */

@@ -1,0 +1,39 @@
+"""Global-threshold calibration (harness; App. C).
+
+The paper picks ONE threshold T "to achieve the desired sparsity level" and keeps
+it for prefill and generation; calibration uses 100 tokens at the end of
+the fixed context, here 100 extra queries from the same generator (R17).
+T is the N-weighted quantile of the calibration scores S_i (or S-bar_i): the
+value at which the expected retained key fraction equals `retention`, placed at
+the midpoint between the two adjacent distinct scores.  The Level-1
+threshold T1 is the same quantile on S^(1) with N^(1) weights at retention 0.5
+("50% of the keys would be ruled out").
+
+Host-side logic over scores the CUDA lookup produced (sqz_selection.dbg_S).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def weighted_threshold(S, N, retention: float) -> float:
+    """S: [..., c] scores (NaN = not scanned, ignored), N: broadcastable [..., c]
+    key counts.  Returns T with sum_{S > T} N / sum N ~= retention."""
+    S = np.asarray(S, dtype=np.float64)
+    W = np.broadcast_to(np.asarray(N, dtype=np.float64), S.shape)
+    m = ~np.isnan(S)
+    s, w = S[m], W[m]
+    if retention >= 1.0:
+        return 0.0
+    if retention <= 0.0:
+        return float(s.max()) * 2.0
+    order = np.argsort(-s, kind="stable")
+    s, w = s[order], w[order]
+    cum = np.cumsum(w) / w.sum()
+    k = int(np.searchsorted(cum, retention))  # first index reaching the target
+    k = min(k, len(s) - 1)
+    hi = s[k]
+    lower = s[k + 1:]
+    lower = lower[lower < hi]
+    lo = lower[0] if len(lower) else 0.0
+    return float(0.5 * (hi + lo))

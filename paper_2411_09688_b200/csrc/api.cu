@@ -1,0 +1,351 @@
+// api.cu -- the C ABI of libsqz.so (include/sqz.h): argument validation,
+// workspace carving and kernel launches.  No device allocation, no host
+// synchronisation on the online path.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/sqz.h"
+#include "internal.h"
+
+using namespace sqz;
+
+namespace {
+thread_local char g_err[512] = "";
+
+int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+int cuda_fail(cudaError_t e, const char *what) {
+    return fail(SQZ_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+struct Carve {
+    char *p;
+    size_t used = 0;
+    template <typename X> X *take(size_t n) {
+        used = (used + 255) & ~(size_t)255;
+        X *r = reinterpret_cast<X *>(p ? p + used : nullptr);
+        used += n * sizeof(X);
+        return r;
+    }
+};
+
+int check_index(const sqz_index *idx, bool need_tables) {
+    if (!idx) return fail(SQZ_ERR_INVALID_ARG, "idx is NULL");
+    if (idx->H < 1) return fail(SQZ_ERR_INVALID_ARG, "idx->H = %d must be >= 1", idx->H);
+    if (idx->d != 64 && idx->d != 128)
+        return fail(SQZ_ERR_UNSUPPORTED, "idx->d = %d: head dimension must be 64 or 128", idx->d);
+    if (idx->L < 1 || idx->L > 0x7fffffffLL)
+        return fail(SQZ_ERR_INVALID_ARG, "idx->L = %lld out of range [1, 2^31)", (long long)idx->L);
+    if (idx->levels != 1 && idx->levels != 2)
+        return fail(SQZ_ERR_INVALID_ARG, "idx->levels = %d must be 1 or 2", idx->levels);
+    if (idx->dtype != SQZ_F32 && idx->dtype != SQZ_BF16)
+        return fail(SQZ_ERR_INVALID_ARG, "idx->dtype = %d is not a sqz_dtype", idx->dtype);
+    if (idx->c2 < 1 || (int64_t)idx->c2 > idx->L)
+        return fail(SQZ_ERR_INVALID_ARG, "idx->c2 = %d must be in [1, L=%lld]", idx->c2,
+                    (long long)idx->L);
+    if (idx->levels == 2 && (idx->c1 < 1 || idx->c1 > idx->c2))
+        return fail(SQZ_ERR_INVALID_ARG, "idx->c1 = %d must be in [1, c2=%d]", idx->c1, idx->c2);
+    if (need_tables) {
+        if (!idx->C2 || !idx->N2 || !idx->key_off)
+            return fail(SQZ_ERR_INVALID_ARG, "idx->C2 / N2 / key_off must be non-NULL");
+        if (!aligned16(idx->C2)) return fail(SQZ_ERR_INVALID_ARG, "idx->C2 must be 16-byte aligned");
+        if (idx->levels == 2) {
+            if (!idx->C1 || !idx->N1 || !idx->child_off)
+                return fail(SQZ_ERR_INVALID_ARG, "idx->C1 / N1 / child_off must be non-NULL (levels=2)");
+            if (!aligned16(idx->C1)) return fail(SQZ_ERR_INVALID_ARG, "idx->C1 must be 16-byte aligned");
+        }
+    }
+    return SQZ_OK;
+}
+
+// ---------------- lookup workspace ----------------
+struct LookupWs {
+    LevelArgs l1, l2;
+    size_t bytes;
+};
+
+LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base) {
+    Carve cv{base};
+    const int64_t BH = (int64_t)B * idx->H;
+    const int CHR = lookup_chunk_rows();
+    const int nqt = (n_q + lookup_qtile() - 1) / lookup_qtile();
+    const bool prefill = n_q > 1;
+    LookupWs w;
+    std::memset(&w.l1, 0, sizeof(w.l1));
+    std::memset(&w.l2, 0, sizeof(w.l2));
+    auto level = [&](LevelArgs &lv, int c) {
+        const int nch = (c + CHR - 1) / CHR;
+        lv.tick = cv.take<int32_t>(BH);
+        lv.sel_pref = cv.take<int32_t>(BH * c);
+        if (prefill) {
+            lv.rowlse = cv.take<float>(BH * n_q);
+            lv.colpart = cv.take<float>((size_t)nqt * BH * c);
+        } else {
+            lv.logits = cv.take<float>(BH * c);
+            lv.part = cv.take<float2>(BH * nch);
+        }
+    };
+    level(w.l2, idx->c2);
+    if (idx->levels == 2) {
+        level(w.l1, idx->c1);
+        w.l1.list = cv.take<int32_t>(BH * idx->c1);
+        w.l1.n_list = cv.take<int32_t>(BH);
+        w.l1.exp_list = cv.take<int32_t>(BH * idx->c2);
+        w.l1.n_exp = cv.take<int32_t>(BH);
+    }
+    w.bytes = cv.used + 256;
+    return w;
+}
+
+// ---------------- attention workspace ----------------
+struct AttnWs {
+    float *part_o, *part_lse;
+    int32_t *status;
+    int32_t kch, max_chunks;
+    size_t bytes;
+};
+AttnWs attn_carve(const sqz_index *idx, int B, int n_q, int n_u, char *base) {
+    Carve cv{base};
+    AttnWs w;
+    w.kch = attention_kch(n_q);
+    w.max_chunks = (int)((idx->L + w.kch - 1) / w.kch + (n_u + w.kch - 1) / w.kch);
+    const size_t rows = (size_t)B * idx->H * n_q;
+    w.status = cv.take<int32_t>(64);
+    w.part_lse = cv.take<float>(rows * w.max_chunks);
+    w.part_o = cv.take<float>(rows * w.max_chunks * idx->d);
+    w.bytes = cv.used + 256;
+    return w;
+}
+char *align_ws(void *ws) { return reinterpret_cast<char *>(((uintptr_t)ws + 255) & ~(uintptr_t)255); }
+}  // namespace
+
+extern "C" {
+
+const char *sqz_last_error(void) { return g_err; }
+int sqz_abi_version(void) { return SQZ_ABI_VERSION; }
+
+int sqz_device_check(void) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    cudaDeviceProp p;
+    e = cudaGetDeviceProperties(&p, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+    if (p.major != 10 || p.minor != 0)
+        return fail(SQZ_ERR_UNSUPPORTED, "device %s is sm_%d%d; libsqz is built for sm_100a", p.name,
+                    p.major, p.minor);
+    return SQZ_OK;
+}
+
+int sqz_workspace_init(void *ws, size_t ws_bytes, void *stream) {
+    if (!ws && ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws is NULL");
+    cudaError_t e = cudaMemsetAsync(ws, 0, ws_bytes, (cudaStream_t)stream);
+    return e == cudaSuccess ? SQZ_OK : cuda_fail(e, "cudaMemsetAsync(ws)");
+}
+
+// ------------------------------------------------------------------ offline
+int sqz_cluster_keys_workspace(const sqz_index *idx, size_t *ws_bytes) {
+    int rc = check_index(idx, false);
+    if (rc) return rc;
+    if (!ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes is NULL");
+    *ws_bytes = kmeans_workspace_bytes(*idx) + 256;
+    return SQZ_OK;
+}
+
+int sqz_cluster_keys(const void *K, const void *V, const int64_t *init2, const int64_t *init1,
+                     sqz_index *idx, void *Kp, void *Vp, const sqz_kmeans_params *p, void *ws,
+                     size_t ws_bytes, int32_t *iters_out, void *stream) {
+    int rc = check_index(idx, true);
+    if (rc) return rc;
+    if (!K || !V || !Kp || !Vp) return fail(SQZ_ERR_INVALID_ARG, "K, V, Kp, Vp must be non-NULL");
+    if (!aligned16(K) || !aligned16(V) || !aligned16(Kp) || !aligned16(Vp))
+        return fail(SQZ_ERR_INVALID_ARG, "K, V, Kp, Vp must be 16-byte aligned");
+    if (!init2) return fail(SQZ_ERR_INVALID_ARG, "init2 is NULL");
+    if (idx->levels == 2 && !init1) return fail(SQZ_ERR_INVALID_ARG, "init1 is NULL (levels=2)");
+    if (!idx->perm) return fail(SQZ_ERR_INVALID_ARG, "idx->perm is NULL");
+    if (!p || p->max_iters < 1 || !(p->tol >= 0.f))
+        return fail(SQZ_ERR_INVALID_ARG, "kmeans params: max_iters >= 1 and tol >= 0 required");
+    if (!ws) return fail(SQZ_ERR_INVALID_ARG, "ws is NULL");
+    char err[400] = "";
+    rc = cluster_keys(K, V, init2, init1, idx, Kp, Vp, *p, ws, ws_bytes, iters_out,
+                      (cudaStream_t)stream, err, sizeof(err));
+    if (rc) return fail(rc, "sqz_cluster_keys: %s", err);
+    return SQZ_OK;
+}
+
+int sqz_index_validate_workspace(const sqz_index *idx, size_t *ws_bytes) {
+    int rc = check_index(idx, false);
+    if (rc) return rc;
+    if (!ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes is NULL");
+    *ws_bytes = validate_workspace_bytes(*idx);
+    return SQZ_OK;
+}
+
+int sqz_index_validate(const sqz_index *idx, void *ws, size_t ws_bytes, void *stream) {
+    int rc = check_index(idx, true);
+    if (rc) return rc;
+    if (!idx->perm) return fail(SQZ_ERR_INVALID_ARG, "idx->perm is NULL");
+    char err[400] = "";
+    rc = index_validate(*idx, ws, ws_bytes, (cudaStream_t)stream, err, sizeof(err));
+    if (rc) return fail(rc, "%s", err);
+    return SQZ_OK;
+}
+
+// ------------------------------------------------------------------ lookup
+int sqz_lookup_workspace(const sqz_index *idx, int32_t B, int32_t n_q, size_t *ws_bytes) {
+    int rc = check_index(idx, false);
+    if (rc) return rc;
+    if (B < 1 || n_q < 1) return fail(SQZ_ERR_INVALID_ARG, "B = %d and n_q = %d must be >= 1", B, n_q);
+    if (!ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes is NULL");
+    *ws_bytes = lookup_carve(idx, B, n_q, nullptr).bytes + 256;
+    return SQZ_OK;
+}
+
+int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t n_q,
+                        const sqz_lookup_params *p, const sqz_selection *out, void *ws,
+                        size_t ws_bytes, void *stream) {
+    int rc = check_index(idx, true);
+    if (rc) return rc;
+    if (!Q) return fail(SQZ_ERR_INVALID_ARG, "Q is NULL");
+    if (!aligned16(Q)) return fail(SQZ_ERR_INVALID_ARG, "Q must be 16-byte aligned");
+    if (B < 1 || n_q < 1) return fail(SQZ_ERR_INVALID_ARG, "B = %d and n_q = %d must be >= 1", B, n_q);
+    if (!p) return fail(SQZ_ERR_INVALID_ARG, "params is NULL");
+    if (!(p->T >= 0.f) || std::isinf(p->T))
+        return fail(SQZ_ERR_INVALID_ARG, "T = %g must be finite and >= 0", (double)p->T);
+    if (idx->levels == 2 && (!(p->T1 >= 0.f) || std::isinf(p->T1)))
+        return fail(SQZ_ERR_INVALID_ARG, "T1 = %g must be finite and >= 0", (double)p->T1);
+    if (!std::isfinite(p->scale)) return fail(SQZ_ERR_INVALID_ARG, "scale must be finite");
+    if (!out || !out->clusters || !out->n_clusters || !out->n_keys || !out->key_idx)
+        return fail(SQZ_ERR_INVALID_ARG, "selection outputs clusters/n_clusters/n_keys/key_idx required");
+    if (!ws) return fail(SQZ_ERR_INVALID_ARG, "ws is NULL");
+    LookupWs w = lookup_carve(idx, B, n_q, align_ws(ws));
+    if (ws_bytes < w.bytes + 256)
+        return fail(SQZ_ERR_INVALID_ARG, "ws_bytes = %zu < required %zu", ws_bytes, w.bytes + 256);
+
+    LookupShape s{B, idx->H, n_q, idx->d, idx->dtype, p->scale};
+    cudaStream_t st = (cudaStream_t)stream;
+    LevelArgs &l2 = w.l2;
+    l2.C = idx->C2;
+    l2.N = idx->N2;
+    l2.off = idx->key_off;
+    l2.c = idx->c2;
+    l2.T = p->T;
+    l2.list = out->clusters;
+    l2.n_list = out->n_clusters;
+    l2.exp_list = out->key_idx;
+    l2.n_exp = out->n_keys;
+    l2.exp_stride = idx->L;
+    l2.dbg_S = out->dbg_S;
+    l2.dbg_lse = out->dbg_lse;
+    if (idx->levels == 2) {
+        LevelArgs &l1 = w.l1;
+        l1.C = idx->C1;
+        l1.N = idx->N1;
+        l1.off = idx->child_off;
+        l1.c = idx->c1;
+        l1.T = p->T1;
+        l1.exp_stride = idx->c2;
+        l1.bitmap = out->l1_surv;
+        l1.dbg_S = out->dbg_S1;
+        cudaError_t e = launch_lookup_level(s, Q, l1, st);
+        if (e != cudaSuccess) return cuda_fail(e, "lookup level 1");
+        l2.rows = l1.exp_list;
+        l2.n_rows = l1.n_exp;
+        l2.row_stride = idx->c2;
+    }
+    cudaError_t e = launch_lookup_level(s, Q, l2, st);
+    if (e != cudaSuccess) return cuda_fail(e, "lookup level 2");
+    return SQZ_OK;
+}
+
+// ------------------------------------------------------------------ attention
+int sqz_attention_workspace(const sqz_index *idx, int32_t B, int32_t n_q, int32_t n_u,
+                            size_t *ws_bytes) {
+    int rc = check_index(idx, false);
+    if (rc) return rc;
+    if (B < 1 || n_q < 1 || n_u < 0)
+        return fail(SQZ_ERR_INVALID_ARG, "B=%d, n_q=%d must be >= 1 and n_u=%d >= 0", B, n_q, n_u);
+    if (!ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes is NULL");
+    *ws_bytes = attn_carve(idx, B, n_q, n_u, nullptr).bytes + 256;
+    return SQZ_OK;
+}
+
+int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, const void *Vp,
+                         const sqz_index *idx, const sqz_selection *sel, const void *Ku,
+                         const void *Vu, int32_t n_u, const sqz_attn_params *p, void *O,
+                         float *LSE, void *ws, size_t ws_bytes, void *stream) {
+    int rc = check_index(idx, false);
+    if (rc) return rc;
+    if (!Q || !Kp || !Vp) return fail(SQZ_ERR_INVALID_ARG, "Q, Kp, Vp must be non-NULL");
+    if (!aligned16(Q) || !aligned16(Kp) || !aligned16(Vp))
+        return fail(SQZ_ERR_INVALID_ARG, "Q, Kp, Vp must be 16-byte aligned");
+    if (B < 1 || n_q < 1 || n_u < 0)
+        return fail(SQZ_ERR_INVALID_ARG, "B=%d, n_q=%d must be >= 1 and n_u=%d >= 0", B, n_q, n_u);
+    if (n_u > 0 && (!Ku || !Vu)) return fail(SQZ_ERR_INVALID_ARG, "Ku, Vu required when n_u > 0");
+    if (n_u > 0 && (!aligned16(Ku) || !aligned16(Vu)))
+        return fail(SQZ_ERR_INVALID_ARG, "Ku, Vu must be 16-byte aligned");
+    if (!sel || !sel->n_keys || !sel->key_idx)
+        return fail(SQZ_ERR_INVALID_ARG, "sel->n_keys and sel->key_idx are required");
+    if (!p) return fail(SQZ_ERR_INVALID_ARG, "params is NULL");
+    if (p->out_dtype != SQZ_F32 && p->out_dtype != SQZ_BF16)
+        return fail(SQZ_ERR_INVALID_ARG, "out_dtype = %d is not a sqz_dtype", p->out_dtype);
+    if (!std::isfinite(p->scale)) return fail(SQZ_ERR_INVALID_ARG, "scale must be finite");
+    if (!O || !LSE) return fail(SQZ_ERR_INVALID_ARG, "O and LSE must be non-NULL");
+    if (!ws) return fail(SQZ_ERR_INVALID_ARG, "ws is NULL");
+    AttnWs w = attn_carve(idx, B, n_q, n_u, align_ws(ws));
+    if (ws_bytes < w.bytes + 256)
+        return fail(SQZ_ERR_INVALID_ARG, "ws_bytes = %zu < required %zu", ws_bytes, w.bytes + 256);
+    AttnArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.Q = Q; a.Kp = Kp; a.Vp = Vp; a.Ku = Ku; a.Vu = Vu;
+    a.n_keys = sel->n_keys; a.key_idx = sel->key_idx;
+    a.B = B; a.H = idx->H; a.n_q = n_q; a.n_u = n_u; a.d = idx->d; a.dtype = idx->dtype;
+    a.causal = p->causal ? 1 : 0; a.partial = p->partial ? 1 : 0; a.out_dtype = p->out_dtype;
+    a.L = idx->L; a.scale = p->scale;
+    a.kch = w.kch; a.max_chunks = w.max_chunks;
+    a.part_o = w.part_o; a.part_lse = w.part_lse; a.status = w.status;
+    a.O = O; a.LSE = LSE;
+    cudaError_t e = launch_attention(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "sparse attention launch");
+    return SQZ_OK;
+}
+
+int sqz_attention_status(void *ws, size_t ws_bytes, void *stream) {
+    if (!ws || ws_bytes < 512) return fail(SQZ_ERR_INVALID_ARG, "ws too small");
+    int32_t *status = reinterpret_cast<int32_t *>(align_ws(ws));
+    int32_t h = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(&h, status, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, sizeof(h), st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "attention status");
+    if (h) return fail(SQZ_ERR_EMPTY, "a final output row attended no key (S:351-353)");
+    return SQZ_OK;
+}
+
+int sqz_merge_partials(int32_t P, const float *O_parts, const float *LSE_parts, int64_t rows,
+                       int32_t d, void *O, float *LSE, int32_t out_dtype, void *stream) {
+    if (P < 1 || rows < 0 || d < 1)
+        return fail(SQZ_ERR_INVALID_ARG, "P=%d >= 1, rows=%lld >= 0, d=%d >= 1 required", P,
+                    (long long)rows, d);
+    if (!O_parts || !LSE_parts || !O || !LSE)
+        return fail(SQZ_ERR_INVALID_ARG, "O_parts, LSE_parts, O, LSE must be non-NULL");
+    if (out_dtype != SQZ_F32 && out_dtype != SQZ_BF16)
+        return fail(SQZ_ERR_INVALID_ARG, "out_dtype = %d is not a sqz_dtype", out_dtype);
+    if (rows > 0x7fffffffLL) return fail(SQZ_ERR_UNSUPPORTED, "rows must be < 2^31");
+    cudaError_t e = launch_merge(P, O_parts, LSE_parts, rows, d, O, LSE, out_dtype, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "merge launch");
+    return SQZ_OK;
+}
+
+}  // extern "C"

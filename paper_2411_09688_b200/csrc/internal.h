@@ -1,0 +1,80 @@
+// internal.h -- launcher interfaces between the C-ABI layer (api.cu) and the
+// kernel translation units.  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sqz.h"
+
+namespace sqz {
+
+// One lookup level (Eq. 1 single level, or Eq. 2 / Eq. 3 of the hierarchy).
+struct LevelArgs {
+    const void *C;        // [H, c, d] centroid table of this level
+    const int32_t *N;     // [H, c] Eq.1 weights N_i (descendant keys for Level 1, R4)
+    const int32_t *off;   // [H, c+1] expansion ranges (key_off or child_off)
+    int32_t c;            // rows in this level's table
+    float T;              // threshold for this level
+    // row space: all c rows, or the per-(b,h) candidate list rows[b,h,0..n_rows)
+    const int32_t *rows;  // [B,H,row_stride] or null
+    const int32_t *n_rows;
+    int32_t row_stride;
+    // scratch
+    float *logits;        // [B,H,c]           (decode)
+    float2 *part;         // [B,H,nch] (m, D)  (decode)
+    int32_t *tick;        // [B*H] self-cleaning tickets
+    int32_t *sel_pref;    // [B,H,c] prefix of expanded counts over the selected list
+    float *rowlse;        // [B,H,n_q]         (prefill)
+    float *colpart;       // [nqt,B,H,c]       (prefill)
+    // outputs
+    int32_t *list;        // [B,H,c] ascending selected row ids
+    int32_t *n_list;      // [B,H]
+    int32_t *exp_list;    // [B,H,exp_stride] expanded positions (keys or Level-2 rows)
+    int32_t *n_exp;       // [B,H]
+    int64_t exp_stride;
+    uint8_t *bitmap;      // optional [B,H,c]
+    float *dbg_S;         // optional [B,H,c]
+    float *dbg_lse;       // optional [B,H,n_q]
+};
+
+struct LookupShape {
+    int32_t B, H, n_q, d, dtype;
+    float scale;
+};
+
+// lookup.cu
+cudaError_t launch_lookup_level(const LookupShape &s, const void *Q, const LevelArgs &lv,
+                                cudaStream_t st);
+int lookup_chunk_rows();
+int lookup_qtile();
+
+// attention.cu
+struct AttnArgs {
+    const void *Q, *Kp, *Vp, *Ku, *Vu;
+    const int32_t *n_keys, *key_idx;
+    int32_t B, H, n_q, n_u, d, dtype, causal, partial, out_dtype;
+    int64_t L;
+    float scale;
+    int32_t kch, max_chunks;
+    float *part_o;    // [rows, max_chunks, d]
+    float *part_lse;  // [rows, max_chunks]
+    int32_t *status;  // [1]
+    void *O;
+    float *LSE;
+};
+cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st);
+int attention_kch(int n_q);
+cudaError_t launch_merge(int P, const float *O_parts, const float *LSE_parts, int64_t rows, int d,
+                         void *O, float *LSE, int out_dtype, cudaStream_t st);
+
+// kmeans.cu
+struct KmeansWs;
+size_t kmeans_workspace_bytes(const sqz_index &idx);
+int cluster_keys(const void *K, const void *V, const int64_t *init2, const int64_t *init1,
+                 sqz_index *idx, void *Kp, void *Vp, const sqz_kmeans_params &p, void *ws,
+                 size_t ws_bytes, int32_t *iters_out, cudaStream_t st, char *err, size_t errlen);
+size_t validate_workspace_bytes(const sqz_index &idx);
+int index_validate(const sqz_index &idx, void *ws, size_t ws_bytes, cudaStream_t st, char *err,
+                   size_t errlen);
+
+}  // namespace sqz

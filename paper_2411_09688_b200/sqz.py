@@ -1,0 +1,343 @@
+"""Thin ctypes binding of libsqz.so (include/sqz.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  PyTorch supplies device memory and the current stream.  There is
+no CPU fallback -- if libsqz.so is missing or the device is not sm_100, calls
+raise.
+
+The raw entry points keep the C names (``sqz_centroid_lookup`` ...); the
+snake-case helpers below (``cluster_keys``, ``centroid_lookup``,
+``sparse_attention``, ``merge_partials``) allocate outputs / workspaces as
+torch tensors and call them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libsqz.so")
+
+SQZ_F32, SQZ_BF16 = 0, 1
+SQZ_OK, SQZ_ERR_INVALID_ARG, SQZ_ERR_FORMAT, SQZ_ERR_INVARIANT = 0, 2, 3, 4
+SQZ_ERR_CUDA, SQZ_ERR_EMPTY, SQZ_ERR_UNSUPPORTED = 5, 7, 8
+
+EXPORTS = [
+    "sqz_cluster_keys_workspace", "sqz_cluster_keys", "sqz_index_validate_workspace",
+    "sqz_index_validate", "sqz_lookup_workspace", "sqz_centroid_lookup",
+    "sqz_attention_workspace", "sqz_sparse_attention", "sqz_attention_status",
+    "sqz_merge_partials", "sqz_workspace_init", "sqz_last_error", "sqz_abi_version",
+    "sqz_device_check",
+]
+
+
+class sqz_index(ctypes.Structure):
+    _fields_ = [("H", ctypes.c_int32), ("d", ctypes.c_int32), ("L", ctypes.c_int64),
+                ("levels", ctypes.c_int32), ("c1", ctypes.c_int32), ("c2", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("C1", ctypes.c_void_p), ("N1", ctypes.c_void_p),
+                ("child_off", ctypes.c_void_p), ("C2", ctypes.c_void_p), ("N2", ctypes.c_void_p),
+                ("key_off", ctypes.c_void_p), ("perm", ctypes.c_void_p)]
+
+
+class sqz_kmeans_params(ctypes.Structure):
+    _fields_ = [("max_iters", ctypes.c_int32), ("tol", ctypes.c_float)]
+
+
+class sqz_lookup_params(ctypes.Structure):
+    _fields_ = [("scale", ctypes.c_float), ("T", ctypes.c_float), ("T1", ctypes.c_float)]
+
+
+class sqz_selection(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("clusters", "n_clusters", "n_keys", "key_idx", "l1_surv", "dbg_S", "dbg_S1",
+                 "dbg_lse")]
+
+
+class sqz_attn_params(ctypes.Structure):
+    _fields_ = [("scale", ctypes.c_float), ("causal", ctypes.c_int32), ("partial", ctypes.c_int32),
+                ("out_dtype", ctypes.c_int32)]
+
+
+class SqzError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libsqz error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libsqz.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO):
+            raise RuntimeError(f"{SO} is missing: build it with __graft_entry__.build(); "
+                               "there is no CPU fallback")
+        L = ctypes.CDLL(SO)
+        vp, sz, szp = ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)
+        i32, i64 = ctypes.c_int32, ctypes.c_int64
+        ip = ctypes.POINTER(sqz_index)
+        L.sqz_last_error.restype = ctypes.c_char_p
+        L.sqz_cluster_keys_workspace.argtypes = [ip, szp]
+        L.sqz_cluster_keys.argtypes = [vp, vp, vp, vp, ip, vp, vp,
+                                       ctypes.POINTER(sqz_kmeans_params), vp, sz,
+                                       ctypes.POINTER(ctypes.c_int32), vp]
+        L.sqz_index_validate_workspace.argtypes = [ip, szp]
+        L.sqz_index_validate.argtypes = [ip, vp, sz, vp]
+        L.sqz_lookup_workspace.argtypes = [ip, i32, i32, szp]
+        L.sqz_centroid_lookup.argtypes = [ip, vp, i32, i32, ctypes.POINTER(sqz_lookup_params),
+                                          ctypes.POINTER(sqz_selection), vp, sz, vp]
+        L.sqz_attention_workspace.argtypes = [ip, i32, i32, i32, szp]
+        L.sqz_sparse_attention.argtypes = [vp, i32, i32, vp, vp, ip,
+                                           ctypes.POINTER(sqz_selection), vp, vp, i32,
+                                           ctypes.POINTER(sqz_attn_params), vp, vp, vp, sz, vp]
+        L.sqz_attention_status.argtypes = [vp, sz, vp]
+        L.sqz_merge_partials.argtypes = [i32, vp, vp, i64, i32, vp, vp, i32, vp]
+        L.sqz_workspace_init.argtypes = [vp, sz, vp]
+        for n in EXPORTS:
+            getattr(L, n).restype = ctypes.c_char_p if n == "sqz_last_error" else ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != SQZ_OK:
+        raise SqzError(rc, lib().sqz_last_error().decode())
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def torch_dtype(dt):
+    return torch.bfloat16 if dt == SQZ_BF16 else torch.float32
+
+
+def sqz_dtype(t: torch.Tensor):
+    if t.dtype == torch.bfloat16:
+        return SQZ_BF16
+    if t.dtype == torch.float32:
+        return SQZ_F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def to_device(stored: np.ndarray, device="cuda") -> torch.Tensor:
+    """Storage-convention numpy array (bf16 bits as uint16, or fp32) -> device tensor."""
+    a = np.ascontiguousarray(stored)
+    if a.dtype == np.uint16:
+        return torch.from_numpy(a.view(np.int16)).view(torch.bfloat16).to(device)
+    return torch.from_numpy(a).to(device)
+
+
+def workspace(nbytes: int, device="cuda") -> torch.Tensor:
+    ws = torch.zeros(max(int(nbytes), 512), dtype=torch.uint8, device=device)
+    return ws
+
+
+# --------------------------------------------------------------------------
+@dataclass
+class Index:
+    """Device-resident index tables (include/sqz.h, sqz_index)."""
+    H: int
+    d: int
+    L: int
+    c2: int
+    dtype: int
+    C2: torch.Tensor
+    N2: torch.Tensor
+    key_off: torch.Tensor
+    perm: torch.Tensor
+    c1: int = 0
+    C1: torch.Tensor = None
+    N1: torch.Tensor = None
+    child_off: torch.Tensor = None
+
+    @property
+    def levels(self):
+        return 2 if self.c1 > 0 else 1
+
+    def struct(self) -> sqz_index:
+        s = sqz_index()
+        s.H, s.d, s.L, s.levels, s.c1, s.c2, s.dtype = (self.H, self.d, self.L, self.levels,
+                                                        self.c1, self.c2, self.dtype)
+        for f in ("C1", "N1", "child_off", "C2", "N2", "key_off", "perm"):
+            t = getattr(self, f)
+            setattr(s, f, None if t is None else t.data_ptr())
+        return s
+
+    @staticmethod
+    def empty(H, d, L, c2, c1=0, dtype=SQZ_BF16, device="cuda"):
+        td = torch_dtype(dtype)
+        i32 = dict(dtype=torch.int32, device=device)
+        return Index(H=H, d=d, L=L, c2=c2, dtype=dtype,
+                     C2=torch.empty(H, c2, d, dtype=td, device=device),
+                     N2=torch.empty(H, c2, **i32), key_off=torch.empty(H, c2 + 1, **i32),
+                     perm=torch.empty(H, L, **i32), c1=c1,
+                     C1=torch.empty(H, c1, d, dtype=td, device=device) if c1 else None,
+                     N1=torch.empty(H, c1, **i32) if c1 else None,
+                     child_off=torch.empty(H, c1 + 1, **i32) if c1 else None)
+
+
+def cluster_keys(K: torch.Tensor, V: torch.Tensor, c2: int, init2: torch.Tensor, c1: int = 0,
+                 init1: torch.Tensor = None, max_iters: int = 50, tol: float = 1e-4):
+    """sqz_cluster_keys: returns (Index, Kp, Vp, (iters_level2, iters_level1))."""
+    H, L, d = K.shape
+    idx = Index.empty(H, d, L, c2, c1, sqz_dtype(K), K.device)
+    s = idx.struct()
+    nb = ctypes.c_size_t(0)
+    _check(lib().sqz_cluster_keys_workspace(ctypes.byref(s), ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=K.device)
+    Kp = torch.empty_like(K)
+    Vp = torch.empty_like(V)
+    it = (ctypes.c_int32 * 2)()
+    p = sqz_kmeans_params(max_iters, tol)
+    i2 = init2.to(device=K.device, dtype=torch.int64).contiguous()
+    i1 = None if init1 is None else init1.to(device=K.device, dtype=torch.int64).contiguous()
+    _check(lib().sqz_cluster_keys(_p(K), _p(V), _p(i2), _p(i1), ctypes.byref(s), _p(Kp), _p(Vp),
+                                  ctypes.byref(p), _p(ws), nb.value, it, _stream()))
+    return idx, Kp, Vp, (it[0], it[1])
+
+
+def index_validate(idx: Index):
+    s = idx.struct()
+    nb = ctypes.c_size_t(0)
+    _check(lib().sqz_index_validate_workspace(ctypes.byref(s), ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=idx.C2.device)
+    _check(lib().sqz_index_validate(ctypes.byref(s), _p(ws), nb.value, _stream()))
+
+
+@dataclass
+class Selection:
+    clusters: torch.Tensor
+    n_clusters: torch.Tensor
+    n_keys: torch.Tensor
+    key_idx: torch.Tensor
+    l1_surv: torch.Tensor = None
+    dbg_S: torch.Tensor = None
+    dbg_S1: torch.Tensor = None
+    dbg_lse: torch.Tensor = None
+
+    @staticmethod
+    def empty(idx: Index, B, n_q, debug=False, device="cuda"):
+        i32 = dict(dtype=torch.int32, device=device)
+        f32 = dict(dtype=torch.float32, device=device)
+        H = idx.H
+        return Selection(
+            clusters=torch.empty(B, H, idx.c2, **i32), n_clusters=torch.empty(B, H, **i32),
+            n_keys=torch.empty(B, H, **i32), key_idx=torch.empty(B, H, idx.L, **i32),
+            l1_surv=torch.empty(B, H, idx.c1, dtype=torch.uint8, device=device)
+            if (debug and idx.c1) else None,
+            dbg_S=torch.empty(B, H, idx.c2, **f32) if debug else None,
+            dbg_S1=torch.empty(B, H, idx.c1, **f32) if (debug and idx.c1) else None,
+            dbg_lse=torch.empty(B, H, n_q, **f32) if debug else None)
+
+    def struct(self) -> sqz_selection:
+        s = sqz_selection()
+        for f, _ in sqz_selection._fields_:
+            t = getattr(self, f)
+            setattr(s, f, None if t is None else t.data_ptr())
+        return s
+
+
+class Workspaces:
+    """Cached zero-initialised workspaces (the library keeps them re-usable)."""
+
+    def __init__(self):
+        self._ws = {}
+
+    def get(self, key, nbytes, device):
+        t = self._ws.get(key)
+        if t is None or t.numel() < nbytes:
+            t = workspace(nbytes, device)
+            self._ws[key] = t
+        return t
+
+
+_WS = Workspaces()
+
+
+def lookup_workspace_bytes(idx: Index, B, n_q):
+    s = idx.struct()
+    nb = ctypes.c_size_t(0)
+    _check(lib().sqz_lookup_workspace(ctypes.byref(s), B, n_q, ctypes.byref(nb)))
+    return nb.value
+
+
+def attention_workspace_bytes(idx: Index, B, n_q, n_u):
+    s = idx.struct()
+    nb = ctypes.c_size_t(0)
+    _check(lib().sqz_attention_workspace(ctypes.byref(s), B, n_q, n_u, ctypes.byref(nb)))
+    return nb.value
+
+
+def centroid_lookup(idx: Index, Q: torch.Tensor, scale: float, T: float, T1: float = 0.0,
+                    sel: Selection = None, ws: torch.Tensor = None, debug=False) -> Selection:
+    """sqz_centroid_lookup on Q[B,H,n_q,d]."""
+    B, H, n_q, d = Q.shape
+    if sel is None:
+        sel = Selection.empty(idx, B, n_q, debug, Q.device)
+    s = idx.struct()
+    if ws is None:
+        ws = _WS.get(("lookup", Q.device), lookup_workspace_bytes(idx, B, n_q), Q.device)
+    p = sqz_lookup_params(scale, T, T1)
+    ss = sel.struct()
+    _check(lib().sqz_centroid_lookup(ctypes.byref(s), _p(Q), B, n_q, ctypes.byref(p),
+                                     ctypes.byref(ss), _p(ws), ws.numel(), _stream()))
+    return sel
+
+
+def sparse_attention(Q, Kp, Vp, idx: Index, sel: Selection, Ku=None, Vu=None, scale=None,
+                     causal=False, partial=False, out_dtype=None, O=None, LSE=None, ws=None):
+    """sqz_sparse_attention: returns (O[B,H,n_q,d], LSE[B,H,n_q])."""
+    B, H, n_q, d = Q.shape
+    n_u = 0 if Ku is None else Ku.shape[2]
+    if scale is None:
+        scale = 1.0 / float(np.sqrt(d))
+    if out_dtype is None:
+        out_dtype = idx.dtype
+    if O is None:
+        O = torch.empty(B, H, n_q, d, dtype=torch_dtype(out_dtype), device=Q.device)
+    if LSE is None:
+        LSE = torch.empty(B, H, n_q, dtype=torch.float32, device=Q.device)
+    s = idx.struct()
+    if ws is None:
+        ws = _WS.get(("attn", Q.device), attention_workspace_bytes(idx, B, n_q, n_u), Q.device)
+    p = sqz_attn_params(scale, int(causal), int(partial), out_dtype)
+    ss = sel.struct()
+    _check(lib().sqz_sparse_attention(_p(Q), B, n_q, _p(Kp), _p(Vp), ctypes.byref(s),
+                                      ctypes.byref(ss), _p(Ku), _p(Vu), n_u, ctypes.byref(p),
+                                      _p(O), _p(LSE), _p(ws), ws.numel(), _stream()))
+    return O, LSE
+
+
+def attention_status(ws: torch.Tensor = None, device="cuda"):
+    if ws is None:
+        ws = _WS._ws.get(("attn", torch.device(device) if isinstance(device, str) else device))
+        if ws is None:
+            for k, v in _WS._ws.items():
+                if k[0] == "attn":
+                    ws = v
+    _check(lib().sqz_attention_status(_p(ws), ws.numel(), _stream()))
+
+
+def merge_partials(O_parts: torch.Tensor, LSE_parts: torch.Tensor, out_dtype=SQZ_F32):
+    """sqz_merge_partials: O_parts[P,rows,d] fp32, LSE_parts[P,rows] fp32."""
+    P, rows, d = O_parts.shape
+    O = torch.empty(rows, d, dtype=torch_dtype(out_dtype), device=O_parts.device)
+    LSE = torch.empty(rows, dtype=torch.float32, device=O_parts.device)
+    _check(lib().sqz_merge_partials(P, _p(O_parts.contiguous()), _p(LSE_parts.contiguous()), rows,
+                                    d, _p(O), _p(LSE), out_dtype, _stream()))
+    return O, LSE
+
+
+def device_check():
+    _check(lib().sqz_device_check())

@@ -1,0 +1,91 @@
+"""GPU offline clustering (sqz_cluster_keys) vs the oracle (section 3.1, 3.3).
+
+K-means has many correct results, so general data is checked by invariants; on a
+well-separated mixture started from the same seeded subset the partitions must be
+identical (K-means pins)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2411_09688_b200 import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _build(fc, c2, init2, c1=0, init1=None, iters=50):
+    from paper_2411_09688_b200 import sqz
+
+    K = sqz.to_device(fc.K)
+    V = sqz.to_device(fc.V)
+    i2 = torch.from_numpy(init2).cuda()
+    i1 = None if init1 is None else torch.from_numpy(init1).cuda()
+    idx, Kp, Vp, its = sqz.cluster_keys(K, V, c2, i2, c1, i1, max_iters=iters)
+    torch.cuda.synchronize()
+    sqz.index_validate(idx)
+    return idx, Kp, Vp, its
+
+
+def _np(t):
+    if t.dtype == torch.bfloat16:
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+@pytest.mark.parametrize("levels", [1, 2])
+@pytest.mark.parametrize("dtype", [synth.BF16, synth.F32])
+def test_separated_mixture_identical_to_oracle(levels, dtype):
+    H, L, d, G = 2, 3000, 128, 16
+    c1 = 4 if levels == 2 else 0
+    fc = synth.fixed_context(H, L, d, G, dtype=dtype, seed=41, sep=True, G1=c1)
+    # one initial point per generating component, same subset for GPU and oracle
+    init2 = np.stack([[np.nonzero(fc.labels[h] == g)[0][0] for g in range(G)] for h in range(H)])
+    init1 = np.stack([np.arange(c1) for _ in range(H)]) if c1 else None
+    g, Kp, Vp, _ = _build(fc, G, init2.astype(np.int64), c1,
+                          None if init1 is None else init1.astype(np.int64))
+    r = oracle.build_index(fc.K, G, init2, c1, init1)
+    assert np.array_equal(_np(g.N2), r.N2)
+    assert np.array_equal(_np(g.key_off), r.key_off)
+    assert np.array_equal(_np(g.perm), r.perm)
+    assert np.array_equal(_np(g.C2), oracle.encode(r.C2, dtype))
+    if levels == 2:
+        assert np.array_equal(_np(g.child_off), r.child_off)
+        assert np.array_equal(_np(g.N1), r.N1)
+        assert np.array_equal(_np(g.C1), oracle.encode(r.C1, dtype))
+    assert np.array_equal(_np(Kp), oracle.permute_kv(fc.K, r))
+    assert np.array_equal(_np(Vp), oracle.permute_kv(fc.V, r))
+
+
+@pytest.mark.parametrize("levels", [1, 2])
+def test_generic_data_invariants_and_determinism(levels):
+    H, L, d = 3, 5000, 128
+    c2, c1 = 250, (50 if levels == 2 else 0)
+    fc = synth.fixed_context(H, L, d, c2, dtype=synth.BF16, seed=42, G1=c1)
+    init2 = synth.kmeans_init(H, L, c2, seed=43)
+    init1 = synth.kmeans_init(H, c2, c1, seed=44) if c1 else None
+    g, Kp, Vp, its = _build(fc, c2, init2, c1, init1, iters=20)
+    g2, _, _, _ = _build(fc, c2, init2, c1, init1, iters=20)
+    for f in ("C2", "N2", "key_off", "perm"):
+        assert torch.equal(getattr(g, f), getattr(g2, f)), f  # bit-reproducible
+    K = oracle.to_f64(fc.K)
+    perm, ko, N2, C2 = _np(g.perm), _np(g.key_off), _np(g.N2), oracle.to_f64(_np(g.C2))
+    for h in range(H):
+        assert N2[h].min() >= 1 and N2[h].sum() == L
+        for i in range(0, c2, 7):
+            mem = perm[h, ko[h, i]:ko[h, i + 1]]
+            assert np.all(np.diff(mem) > 0)
+            mean = oracle.round_to(K[h][mem].mean(0), synth.BF16)
+            # raw-mean centroid (R2), rounded once; allow 1 bf16 ulp for the tie cases
+            assert np.all(np.abs(C2[h, i] - mean) <= np.abs(mean) * 2 ** -7 + 1e-30)
+    assert np.array_equal(_np(Kp), np.stack([fc.K[h][perm[h]] for h in range(H)]))
+    if levels == 2:
+        co, N1 = _np(g.child_off), _np(g.N1)
+        for h in range(H):
+            for p in range(c1):
+                assert N1[h, p] == N2[h, co[h, p]:co[h, p + 1]].sum()

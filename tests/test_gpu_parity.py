@@ -1,0 +1,235 @@
+"""GPU parity: libsqz (through the C ABI) vs the fp64 CPU oracle on the same seeded inputs.
+
+Selection: identical finest-level cluster sets except clusters whose oracle score lies
+within 1e-5 relative of the threshold; hierarchical Level 2 is compared conditioned on
+the GPU's Level-1 survivors (parity rules).  Attention: evaluated by the
+oracle on the GPU's selected key set ("given the same mask"); bf16 O max-abs <= 2e-2 and
+rel-L2 <= 5e-3, fp32 O max-abs <= 1e-4, LSE within 1e-3 (north star)."""
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2411_09688_b200 import calib, synth
+
+from helpers import (assert_selection_parity, gpu_index, gpu_sets, key_mask_from_gpu,
+                     oracle_problem, rel_l2)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2411_09688_b200 import sqz
+
+    sqz.device_check()
+
+
+def _sqz():
+    from paper_2411_09688_b200 import sqz
+
+    return sqz
+
+
+def _calibrate(P, scale, retention, prefill=False, n_cal=24, ret1=0.5):
+    """T (and T1) from oracle scores of separate calibration queries (R17)."""
+    idx = P["idx"]
+    mix = P["fc"].mix
+    if prefill:
+        Qc = synth.prefill_queries(mix, 4, 64, seed=777, dtype=P["dtype"])
+    else:
+        Qc = synth.decode_queries(mix, n_cal, seed=777, dtype=P["dtype"])
+    Qc = oracle.to_f64(Qc)
+    T1 = 0.0
+    if idx.levels == 2:
+        r = oracle.lookup(Qc, idx, scale, 0.0, 0.0)
+        T1 = calib.weighted_threshold(r["Sbar1"], idx.N1[None], ret1)
+    r = oracle.lookup(Qc, idx, scale, 0.0, T1)
+    T = calib.weighted_threshold(r["Sbar2"], idx.N2[None], retention)
+    return T, T1
+
+
+def _check_lookup(P, sel, scale, T, T1, B):
+    idx = P["idx"]
+    Q64 = oracle.to_f64(P["Q"])
+    H = idx.H
+    forced = None
+    if idx.levels == 2:
+        ref1 = oracle.lookup(Q64, idx, scale, T, T1)
+        g1 = sel.l1_surv.cpu().numpy().astype(bool)
+        assert_selection_parity(g1, ref1["surv1"], ref1["Sbar1"], T1, what="level-1")
+        np.testing.assert_allclose(sel.dbg_S1.cpu().numpy(), ref1["Sbar1"], rtol=2e-5, atol=1e-12)
+        forced = g1
+    ref = oracle.lookup(Q64, idx, scale, T, T1, forced_l1=forced)
+    g = gpu_sets(sel, B, H, idx.c2)
+    ndiff = assert_selection_parity(g, ref["sel2"], ref["Sbar2"], T)
+    S_gpu = sel.dbg_S.cpu().numpy()
+    assert np.array_equal(np.isnan(S_gpu), np.isnan(ref["Sbar2"]))
+    m = ~np.isnan(ref["Sbar2"])
+    np.testing.assert_allclose(S_gpu[m], ref["Sbar2"][m], rtol=2e-5, atol=1e-12)
+    lse = sel.dbg_lse.cpu().numpy()
+    fin = np.isfinite(ref["lse"])
+    assert np.array_equal(np.isfinite(lse), fin)
+    np.testing.assert_allclose(lse[fin], ref["lse"][fin], atol=1e-4, rtol=1e-5)
+    # k = sum N over the selected clusters; key_idx is the concatenation of their ranges
+    nk = sel.n_keys.cpu().numpy()
+    ki = sel.key_idx.cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            cl = np.nonzero(g[b, h])[0]
+            assert nk[b, h] == idx.N2[h][cl].sum()
+            exp = np.concatenate([np.arange(idx.key_off[h, i], idx.key_off[h, i + 1]) for i in cl]
+                                 + [np.zeros(0, np.int64)])
+            assert np.array_equal(ki[b, h, :nk[b, h]], exp)
+    return ndiff
+
+
+def _check_attention(P, sel, O, LSE, scale, causal, B, tol_abs, tol_rel):
+    idx = P["idx"]
+    mask = key_mask_from_gpu(sel, idx, B, idx.H)
+    Ku = None if P["Ku"] is None else oracle.to_f64(P["Ku"])
+    Vu = None if P["Vu"] is None else oracle.to_f64(P["Vu"])
+    Oref, Lref, _ = oracle.attention(oracle.to_f64(P["Q"]), oracle.to_f64(P["fc"].K),
+                                     oracle.to_f64(P["fc"].V), mask, Ku, Vu, causal, scale)
+    Og = O.float().cpu().numpy().astype(np.float64)
+    Lg = LSE.cpu().numpy().astype(np.float64)
+    fin = np.isfinite(Lref)
+    assert np.array_equal(np.isfinite(Lg), fin)
+    assert np.abs(Og - Oref).max() <= tol_abs, np.abs(Og - Oref).max()
+    if tol_rel is not None:
+        assert rel_l2(Og, Oref) <= tol_rel, rel_l2(Og, Oref)
+    np.testing.assert_allclose(Lg[fin], Lref[fin], atol=1e-3, rtol=0)
+
+
+def _device(P):
+    sqz = _sqz()
+    t = {k: (None if P[k] is None else sqz.to_device(P[k])) for k in ("Q", "Ku", "Vu")}
+    idx = P["idx"]
+    t["Kp"] = sqz.to_device(oracle.permute_kv(P["fc"].K, idx))
+    t["Vp"] = sqz.to_device(oracle.permute_kv(P["fc"].V, idx))
+    t["idx"] = gpu_index(idx)
+    return t
+
+
+DECODE_CASES = [
+    # id, H, L, d, c2, c1, dtype, B, n_u, retention
+    ("cfg1_fp32", 1, 1024, 64, 32, 0, synth.F32, 1, 16, 0.3),
+    ("bf16_d128", 4, 3000, 128, 97, 0, synth.BF16, 3, 37, 0.3),
+    ("bf16_d64_B9", 2, 2500, 64, 61, 0, synth.BF16, 9, 5, 0.2),
+    ("hier_bf16", 3, 4000, 128, 200, 40, synth.BF16, 2, 33, 0.1),
+    ("hier_fp32_B8", 2, 3000, 64, 150, 30, synth.F32, 8, 0, 0.15),
+]
+
+
+@pytest.mark.parametrize("case", DECODE_CASES, ids=lambda c: c[0])
+def test_decode_lookup_and_attention(case):
+    sqz = _sqz()
+    _, H, L, d, c2, c1, dt, B, n_u, ret = case
+    P = oracle_problem(H, L, d, c2, c1, dt, seed=zlib.crc32(case[0].encode()) % 1000, B=B, n_u=n_u)
+    scale = 1.0 / np.sqrt(d)
+    T, T1 = _calibrate(P, scale, ret)
+    t = _device(P)
+    sel = sqz.centroid_lookup(t["idx"], t["Q"], scale, T, T1, debug=True)
+    torch.cuda.synchronize()
+    _check_lookup(P, sel, scale, T, T1, B)
+    O, LSE = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, t["Ku"], t["Vu"], scale,
+                                  partial=True)
+    torch.cuda.synchronize()
+    fp32 = dt == synth.F32
+    _check_attention(P, sel, O, LSE, scale, False, B, 1e-4 if fp32 else 2e-2,
+                     None if fp32 else 5e-3)
+
+
+PREFILL_CASES = [
+    ("bf16_single", 2, 2048, 128, 100, 0, synth.BF16, 1, 200, 200, 0.3),
+    ("fp32_d64", 1, 1500, 64, 40, 0, synth.F32, 2, 70, 90, 0.3),
+    ("hier_bf16", 2, 3000, 128, 150, 30, synth.BF16, 1, 130, 130, 0.15),
+]
+
+
+@pytest.mark.parametrize("case", PREFILL_CASES, ids=lambda c: c[0])
+def test_prefill_lookup_and_attention(case):
+    sqz = _sqz()
+    _, H, L, d, c2, c1, dt, B, n_q, n_u, ret = case
+    P = oracle_problem(H, L, d, c2, c1, dt, seed=zlib.crc32(case[0].encode()) % 1000 + 7, B=B, n_u=n_u, n_q=n_q,
+                       prefill=True)
+    scale = 1.0 / np.sqrt(d)
+    T, T1 = _calibrate(P, scale, ret, prefill=True)
+    t = _device(P)
+    sel = sqz.centroid_lookup(t["idx"], t["Q"], scale, T, T1, debug=True)
+    torch.cuda.synchronize()
+    _check_lookup(P, sel, scale, T, T1, B)
+    O, LSE = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, t["Ku"], t["Vu"], scale,
+                                  causal=True)
+    torch.cuda.synchronize()
+    fp32 = dt == synth.F32
+    _check_attention(P, sel, O, LSE, scale, True, B, 1e-4 if fp32 else 2e-2,
+                     None if fp32 else 5e-3)
+
+
+def test_threshold_zero_is_dense_attention():
+    """North star: T = 0 selects every key and reproduces dense attention."""
+    sqz = _sqz()
+    P = oracle_problem(2, 1800, 128, 60, 0, synth.BF16, seed=5, B=2, n_u=9)
+    t = _device(P)
+    scale = 1 / np.sqrt(128)
+    sel = sqz.centroid_lookup(t["idx"], t["Q"], scale, 0.0, debug=True)
+    O, LSE = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, t["Ku"], t["Vu"], scale)
+    torch.cuda.synchronize()
+    assert (sel.n_keys.cpu().numpy() == 1800).all()
+    Oref, Lref, _ = oracle.attention(oracle.to_f64(P["Q"]), oracle.to_f64(P["fc"].K),
+                                     oracle.to_f64(P["fc"].V), None, oracle.to_f64(P["Ku"]),
+                                     oracle.to_f64(P["Vu"]), False, scale)
+    assert np.abs(O.float().cpu().numpy() - Oref).max() <= 2e-2
+    np.testing.assert_allclose(LSE.cpu().numpy(), Lref, atol=1e-3)
+
+
+def test_empty_selection_edges():
+    sqz = _sqz()
+    P = oracle_problem(1, 512, 64, 16, 0, synth.F32, seed=6, B=1, n_u=0)
+    t = _device(P)
+    scale = 1 / 8.0
+    sel = sqz.centroid_lookup(t["idx"], t["Q"], scale, 1.0, debug=True)  # S_i <= 1/N_i < 1
+    assert int(sel.n_keys.sum()) == 0 and int(sel.n_clusters.sum()) == 0
+    O, LSE = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, None, None, scale,
+                                  partial=True)
+    torch.cuda.synchronize()
+    assert torch.isneginf(LSE).all() and (O == 0).all()
+    sqz.attention_status()  # partial mode: not an error
+    sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, None, None, scale, partial=False)
+    with pytest.raises(sqz.SqzError) as e:
+        sqz.attention_status()
+    assert e.value.code == sqz.SQZ_ERR_EMPTY
+    sqz.attention_status()  # flag cleared
+
+
+def test_merge_partials_matches_oracle():
+    sqz = _sqz()
+    rng = np.random.default_rng(3)
+    P, rows, d = 5, 77, 128
+    Op = rng.standard_normal((P, rows, d)).astype(np.float32)
+    Lp = (rng.standard_normal((P, rows)) * 4).astype(np.float32)
+    Lp[1, :10] = -np.inf
+    Lp[:, 20] = -np.inf
+    O, L = sqz.merge_partials(torch.from_numpy(Op).cuda(), torch.from_numpy(Lp).cuda())
+    Oref, Lref = oracle.merge(Op.astype(np.float64), Lp.astype(np.float64))
+    np.testing.assert_allclose(O.cpu().numpy(), Oref, atol=1e-5)
+    fin = np.isfinite(Lref)
+    assert np.array_equal(np.isfinite(L.cpu().numpy()), fin)
+    np.testing.assert_allclose(L.cpu().numpy()[fin], Lref[fin], atol=1e-5)
+
+
+def test_invalid_arguments_rejected():
+    sqz = _sqz()
+    P = oracle_problem(1, 256, 64, 8, 0, synth.F32, seed=8)
+    t = _device(P)
+    with pytest.raises(sqz.SqzError) as e:
+        sqz.centroid_lookup(t["idx"], t["Q"], 0.125, -1.0)
+    assert e.value.code == sqz.SQZ_ERR_INVALID_ARG and "T" in str(e.value)
+    with pytest.raises(sqz.SqzError):
+        sqz.centroid_lookup(t["idx"], t["Q"], 0.125, float("nan"))
