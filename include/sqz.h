@@ -23,7 +23,9 @@
  *     given by the matching *_workspace() query.  Workspaces must be zeroed
  *     ONCE before first use (sqz_workspace_init); the library leaves its
  *     counters zeroed again when each call completes, so a workspace can be
- *     reused by consecutive calls on the same stream (not concurrently).
+ *     reused by consecutive calls with the SAME geometry (B, n_q, n_u and
+ *     index shape) on the same stream (not concurrently); re-zero it before
+ *     using it with another geometry.
  *   - Return codes: SQZ_OK, or an error code; sqz_last_error() returns a
  *     thread-local message naming the offending argument.  Argument errors
  *     are detected on the host before anything is enqueued.

@@ -16,9 +16,11 @@ from __future__ import annotations
 import numpy as np
 
 
-def weighted_threshold(S, N, retention: float) -> float:
+def weighted_threshold(S, N, retention: float, total_weight: float = None) -> float:
     """S: [..., c] scores (NaN = not scanned, ignored), N: broadcastable [..., c]
-    key counts.  Returns T with sum_{S > T} N / sum N ~= retention."""
+    key counts.  Returns T with sum_{S > T} N / W ~= retention, where W is
+    `total_weight` (default: the weight of the scanned rows; pass the number of
+    keys x query-rows when Level-1 pruning left rows unscanned)."""
     S = np.asarray(S, dtype=np.float64)
     W = np.broadcast_to(np.asarray(N, dtype=np.float64), S.shape)
     m = ~np.isnan(S)
@@ -29,7 +31,7 @@ def weighted_threshold(S, N, retention: float) -> float:
         return float(s.max()) * 2.0
     order = np.argsort(-s, kind="stable")
     s, w = s[order], w[order]
-    cum = np.cumsum(w) / w.sum()
+    cum = np.cumsum(w) / (w.sum() if total_weight is None else float(total_weight))
     k = int(np.searchsorted(cum, retention))  # first index reaching the target
     k = min(k, len(s) - 1)
     hi = s[k]

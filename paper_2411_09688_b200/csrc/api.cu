@@ -110,7 +110,7 @@ LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base) {
 // ---------------- attention workspace ----------------
 struct AttnWs {
     float *part_o, *part_lse;
-    int32_t *status;
+    int32_t *status, *row_cnt;
     int32_t kch, max_chunks;
     size_t bytes;
 };
@@ -118,9 +118,10 @@ AttnWs attn_carve(const sqz_index *idx, int B, int n_q, int n_u, char *base) {
     Carve cv{base};
     AttnWs w;
     w.kch = attention_kch(n_q);
-    w.max_chunks = (int)((idx->L + w.kch - 1) / w.kch + (n_u + w.kch - 1) / w.kch);
+    w.max_chunks = attention_max_parts(idx->L, n_u, n_q);
     const size_t rows = (size_t)B * idx->H * n_q;
     w.status = cv.take<int32_t>(64);
+    w.row_cnt = cv.take<int32_t>(rows);
     w.part_lse = cv.take<float>(rows * w.max_chunks);
     w.part_o = cv.take<float>(rows * w.max_chunks * idx->d);
     w.bytes = cv.used + 256;
@@ -313,7 +314,7 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
     a.causal = p->causal ? 1 : 0; a.partial = p->partial ? 1 : 0; a.out_dtype = p->out_dtype;
     a.L = idx->L; a.scale = p->scale;
     a.kch = w.kch; a.max_chunks = w.max_chunks;
-    a.part_o = w.part_o; a.part_lse = w.part_lse; a.status = w.status;
+    a.part_o = w.part_o; a.part_lse = w.part_lse; a.status = w.status; a.row_cnt = w.row_cnt;
     a.O = O; a.LSE = LSE;
     cudaError_t e = launch_attention(a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "sparse attention launch");

@@ -59,11 +59,13 @@ struct AttnArgs {
     float *part_o;    // [rows, max_chunks, d]
     float *part_lse;  // [rows, max_chunks]
     int32_t *status;  // [1]
+    int32_t *row_cnt; // [rows] self-cleaning chunk tickets
     void *O;
     float *LSE;
 };
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st);
 int attention_kch(int n_q);
+int attention_max_parts(int64_t L, int n_u, int n_q);
 cudaError_t launch_merge(int P, const float *O_parts, const float *LSE_parts, int64_t rows, int d,
                          void *O, float *LSE, int out_dtype, cudaStream_t st);
 

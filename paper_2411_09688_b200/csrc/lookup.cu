@@ -1,13 +1,15 @@
 // lookup.cu -- centroid lookup kernels (section 4.1).
 //
 // Decode (n_q == 1, "generation stage"):
-//   k_scan_decode: one CTA per (chunk of CH centroid rows, head, group of NB
-//   queries).  Centroid rows are read once per head for the whole query group
+//   k_lookup_decode: one 8-CTA thread-block cluster per (group of NB queries,
+//   head).  Centroid rows are read once per head for the whole query group
 //   (the batch shares the fixed context) with 8/16-byte coalesced
 //   loads; logits s_i = scale*q.C_i are fp32 FFMA over exact bf16->fp32
-//   products.  Each CTA stores its logits and a per-query (m, D = sum N e^(s-m))
-//   partial; the LAST CTA of each (group, head) (atomic ticket) folds the
-//   partials in a fixed order and runs the threshold + compaction epilogue:
+//   products and stay in shared memory ("cache exp(qC) during the first pass",
+//   P:342, kept as logits).  The per-CTA (m, D = sum N e^(s-m)) partials are
+//   folded through distributed shared memory, then every CTA thresholds its
+//   own rows in parallel ("the second pass can be parallelized across the
+//   cluster dimension"):
 //   select i  <=>  (s_i - m) > log D + log T      (single-pass form, P:343,
 //   max folded into the threshold as in App. C; no second exp).
 // Prefill (n_q > 1):
@@ -17,6 +19,8 @@
 //   floats; the last CTA per (b,h) reduces the tiles and thresholds S-bar > T.
 // Both run on an explicit row list for the Level-2 pass of the hierarchy
 // (Eq. 3: only the children of the Level-1 survivors).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -79,7 +83,8 @@ __device__ __forceinline__ float transpose_reduce(float (&v)[NV], int lane) {
     return v[0];
 }
 template <int NV> __device__ __forceinline__ int transpose_index(int lane) {
-    constexpr int lg = NV == 1 ? 0 : NV == 2 ? 1 : NV == 4 ? 2 : 3;
+    static_assert(NV == 1 || NV == 2 || NV == 4 || NV == 8 || NV == 16, "NV");
+    constexpr int lg = NV == 1 ? 0 : NV == 2 ? 1 : NV == 4 ? 2 : NV == 8 ? 3 : 4;
     return (lane >> (5 - lg)) & (NV - 1);
 }
 
@@ -92,24 +97,52 @@ __device__ __forceinline__ void md_combine(float &m, float &D, float m2, float D
 }
 
 // --------------------------------------------------------------------------
-// Epilogue: threshold + ascending compaction + range expansion, one CTA.
-// sel(row) is given by the functor; every selected row's range
-// [off[row], off[row+1]) is expanded into exp_list (keys or Level-2 rows).
+// Block-wide ordered compaction of one tile of NT rows: every thread brings
+// (sel, n = expanded count); returns its position among the tile's selected rows,
+// its exclusive prefix of n, and the tile totals.
 // --------------------------------------------------------------------------
+__device__ __forceinline__ void tile_scan(bool sel, int n, int &pos, int &kpre, int &tot_c,
+                                          int &tot_k) {
+    __shared__ int s_wc[NW], s_wk[NW];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned bal = __ballot_sync(FULL, sel);
+    const int wpre = __popc(bal & ((1u << lane) - 1u));
+    int inc = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) { s_wc[warp] = __popc(bal); s_wk[warp] = inc; }
+    __syncthreads();
+    int wb = 0, kb = 0, tc = 0, tk = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        if (w < warp) { wb += s_wc[w]; kb += s_wk[w]; }
+        tc += s_wc[w];
+        tk += s_wk[w];
+    }
+    pos = wb + wpre;
+    kpre = kb + inc - n;
+    tot_c = tc;
+    tot_k = tk;
+    __syncthreads();
+}
+
+// Epilogue of the prefill path (one CTA per (b,h)): threshold + ascending
+// compaction + range expansion, tile by tile, with the ranges staged in smem.
 template <bool ROWLIST, typename SelFn>
 __device__ void finalize_rows(const LevelArgs &lv, int bh, int h, int nrows, SelFn selfn) {
-    __shared__ int s_wcnt[NW], s_wsum[NW];
-    __shared__ int s_run, s_runN;
+    __shared__ int s_st[NT], s_n[NT], s_kp[NT];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int32_t *off = lv.off + (size_t)h * (lv.c + 1);
     int32_t *list = lv.list + (size_t)bh * lv.c;
-    int32_t *pref = lv.sel_pref + (size_t)bh * lv.c;
+    int32_t *exp_list = lv.exp_list + (size_t)bh * lv.exp_stride;
     const int32_t *rows = ROWLIST ? lv.rows + (size_t)bh * lv.row_stride : nullptr;
-    if (lv.dbg_S && ROWLIST) {
+    if (lv.dbg_S && ROWLIST)
         for (int r = tid; r < lv.c; r += NT) lv.dbg_S[(size_t)bh * lv.c + r] = NAN;
-    }
-    if (tid == 0) { s_run = 0; s_runN = 0; }
     __syncthreads();
+    int run = 0, runk = 0;
     for (int base = 0; base < nrows; base += NT) {
         const int r = base + tid;
         const bool valid = r < nrows;
@@ -118,62 +151,84 @@ __device__ void finalize_rows(const LevelArgs &lv, int bh, int h, int nrows, Sel
         const bool sel = valid && selfn(row, dbg);
         if (valid && lv.dbg_S) lv.dbg_S[(size_t)bh * lv.c + row] = dbg;
         if (valid && lv.bitmap) lv.bitmap[(size_t)bh * lv.c + row] = sel ? 1 : 0;
-        const int cnt = sel ? (off[row + 1] - off[row]) : 0;
-        const unsigned bal = __ballot_sync(FULL, sel);
-        const int wpre = __popc(bal & ((1u << lane) - 1u));
-        int inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(FULL, inc, o);
-            if (lane >= o) inc += t;
-        }
-        if (lane == 31) { s_wcnt[warp] = __popc(bal); s_wsum[warp] = inc; }
-        __syncthreads();
-        int wb = 0, nb = 0;
-        for (int w = 0; w < warp; ++w) { wb += s_wcnt[w]; nb += s_wsum[w]; }
+        int st = 0, n = 0;
+        if (sel) { st = off[row]; n = off[row + 1] - st; }
+        int pos, kpre, tc, tk;
+        tile_scan(sel, n, pos, kpre, tc, tk);
         if (sel) {
-            const int pos = s_run + wb + wpre;
-            list[pos] = row;
-            pref[pos] = s_runN + nb + inc - cnt;
+            list[run + pos] = row;
+            s_st[pos] = st;
+            s_n[pos] = n;
+            s_kp[pos] = runk + kpre;
         }
         __syncthreads();
-        if (tid == 0) {
-            int tc = 0, tn = 0;
-            for (int w = 0; w < NW; ++w) { tc += s_wcnt[w]; tn += s_wsum[w]; }
-            s_run += tc;
-            s_runN += tn;
+        for (int j = warp; j < tc; j += NW) {
+            const int st_j = s_st[j], n_j = s_n[j], kp_j = s_kp[j];
+            for (int t = lane; t < n_j; t += 32) exp_list[kp_j + t] = st_j + t;
         }
         __syncthreads();
+        run += tc;
+        runk += tk;
     }
-    const int nsel = s_run;
     if (tid == 0) {
-        lv.n_list[bh] = nsel;
-        lv.n_exp[bh] = s_runN;
-    }
-    int32_t *exp_list = lv.exp_list + (size_t)bh * lv.exp_stride;
-    for (int j = warp; j < nsel; j += NW) {
-        const int i = list[j];
-        const int st = off[i], n = off[i + 1] - st, b0 = pref[j];
-        for (int t = lane; t < n; t += 32) exp_list[b0 + t] = st + t;
+        lv.n_list[bh] = run;
+        lv.n_exp[bh] = runk;
     }
 }
 
 // --------------------------------------------------------------------------
-// Decode scan: logits + (m, D) partials, last CTA thresholds.
+// Decode lookup: one thread-block CLUSTER of NC CTAs per (query group, head).
+// Each CTA scans a contiguous slice of the row space (logits kept in smem),
+// the per-query (m, D) partials are combined through distributed shared
+// memory in rank order (deterministic, identical in every CTA), each CTA
+// thresholds and compacts its own rows, and the cluster-wide output offsets
+// come from a DSMEM prefix over the ranks.  No global scratch round trip, no
+// serial last-CTA epilogue.
 // --------------------------------------------------------------------------
+constexpr int NC = 8;  // CTAs per cluster (portable maximum)
+
+template <int NB> struct DecodeSmem {
+    float2 md[NB];
+    int cnt[NB], keys[NB];
+};
+
 template <typename T, int D, int NB, bool ROWLIST>
-__global__ void __launch_bounds__(NT) k_scan_decode(LookupShape s, const T *__restrict__ Q,
-                                                    LevelArgs lv) {
-    const int chunk = blockIdx.x, h = blockIdx.y, g = blockIdx.z;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__restrict__ Q,
+                                                      LevelArgs lv, int rpc) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int h = blockIdx.y, g = blockIdx.z;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int H = s.H, c = lv.c;
     const int b0 = g * NB;
     const int nb = min(NB, s.B - b0);
     const T *C = reinterpret_cast<const T *>(lv.C) + (size_t)h * c * D;
     const int32_t *N = lv.N + (size_t)h * c;
-    const int nrows = ROWLIST ? ldcg(lv.n_rows + (size_t)b0 * H + h) : c;
-    const int32_t *rows = ROWLIST ? lv.rows + ((size_t)b0 * H + h) * lv.row_stride : nullptr;
+    const int32_t *off = lv.off + (size_t)h * (c + 1);
 
+    extern __shared__ __align__(16) unsigned char dyn[];
+    float *s_log = reinterpret_cast<float *>(dyn);                 // [NB][rpc]
+    int *s_row = reinterpret_cast<int *>(s_log + NB * rpc);        // [rpc] (ROWLIST)
+    int *s_sel = s_row + rpc;                                      // [NB][rpc]
+    int *s_st = s_sel + NB * rpc;                                  // [NB][rpc]
+    int *s_n = s_st + NB * rpc;                                    // [NB][rpc]
+    int *s_kp = s_n + NB * rpc;                                    // [NB][rpc]
+    __shared__ DecodeSmem<NB> sh;
+    __shared__ float s_M[NB], s_lD[NB];
+    __shared__ float s_wm[NW][NB], s_wd[NW][NB];
+
+    const int nrows = ROWLIST ? ldcg(lv.n_rows + (size_t)b0 * H + h) : c;
+    const int r0 = rank * rpc;
+    const int nloc = max(0, min(rpc, nrows - r0));
+    const int32_t *rows = ROWLIST ? lv.rows + ((size_t)b0 * H + h) * lv.row_stride : nullptr;
+    if (ROWLIST && lv.dbg_S) {  // rows outside the candidate list are "not scanned"
+        const int per = (c + NC - 1) / NC;
+        for (int r = rank * per + tid; r < min(c, (rank + 1) * per); r += NT)
+            lv.dbg_S[((size_t)b0 * H + h) * c + r] = NAN;
+    }
+
+    // ---- scan: logits of the CTA's rows for the NB queries ----
     float q[NB][D / 32];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -182,83 +237,142 @@ __global__ void __launch_bounds__(NT) k_scan_decode(LookupShape s, const T *__re
 #pragma unroll
             for (int k = 0; k < D / 32; ++k) q[i][k] = 0.f;
     }
-    const int myq = transpose_index<NB>(lane);
-    float m = -INFINITY, Dsum = 0.f;  // for query myq (lanes sharing myq hold equal values)
-    const int r0 = chunk * CH;
-    for (int rr = warp; rr < CH; rr += NW) {
-        const int r = r0 + rr;
-        if (r >= nrows) break;
-        const int row = ROWLIST ? ldcg(rows + r) : r;
-        float cf[D / 32];
-        Lane<T, D>::load(C + (size_t)row * D, lane, cf);
-        float v[NB];
+    // A warp loads U = 16 rows at once (one memory round trip), forms the
+    // U x NB partial dot products, and reduces them 16 at a time with the
+    // transposed butterfly: value v = row_local * NB + query.
+    constexpr int U = 16;
+    constexpr int RPT = 16 / NB;  // rows per 16-value transpose
+    for (int rr0 = warp * U; rr0 < nloc; rr0 += NW * U) {
+        float cf[U][D / 32];
+        int rowid[U];
 #pragma unroll
-        for (int i = 0; i < NB; ++i) {
-            float acc = 0.f;
+        for (int u = 0; u < U; ++u) {
+            const int rr = rr0 + u;
+            rowid[u] = -1;
+            if (rr < nloc) {
+                rowid[u] = ROWLIST ? ldcg(rows + r0 + rr) : r0 + rr;
+                Lane<T, D>::load(C + (size_t)rowid[u] * D, lane, cf[u]);
+            } else {
 #pragma unroll
-            for (int k = 0; k < D / 32; ++k) acc = fmaf(q[i][k], cf[k], acc);
-            v[i] = acc;
+                for (int k = 0; k < D / 32; ++k) cf[u][k] = 0.f;
+            }
         }
-        const float sv = transpose_reduce<NB>(v, lane) * s.scale;
-        if (myq < nb) {
-            if ((lane & ((32 / NB) - 1)) == 0)
-                lv.logits[((size_t)(b0 + myq) * H + h) * c + row] = sv;
-            md_combine(m, Dsum, sv, (float)N[row]);
+#pragma unroll
+        for (int gq = 0; gq < U / RPT; ++gq) {
+            float v[16];
+#pragma unroll
+            for (int u = 0; u < RPT; ++u)
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int k = 0; k < D / 32; ++k) acc = fmaf(q[i][k], cf[gq * RPT + u][k], acc);
+                    v[u * NB + i] = acc;
+                }
+            const float sv = transpose_reduce<16>(v, lane) * s.scale;
+            const int vi = transpose_index<16>(lane);
+            const int rr = rr0 + gq * RPT + vi / NB;
+            if ((lane & 1) == 0 && rr < nloc) s_log[(vi % NB) * rpc + rr] = sv;
+        }
+        if (ROWLIST && lane < U && rr0 + lane < nloc) s_row[rr0 + lane] = ldcg(rows + r0 + rr0 + lane);
+    }
+    __syncthreads();
+    // (m, D) of the CTA's rows per query: block max, then one exp per row.
+    for (int i = 0; i < nb; ++i) {
+        float mx = -INFINITY;
+        for (int rr = tid; rr < nloc; rr += NT) mx = fmaxf(mx, s_log[i * rpc + rr]);
+        mx = warp_max(mx);
+        if (lane == 0) s_wm[warp][i] = mx;
+        __syncthreads();
+        float M = -INFINITY;
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, s_wm[w][i]);
+        float e = 0.f;
+        if (M != -INFINITY)
+            for (int rr = tid; rr < nloc; rr += NT) {
+                const int row = ROWLIST ? s_row[rr] : r0 + rr;
+                e += (float)__ldg(N + row) * expf(s_log[i * rpc + rr] - M);
+            }
+        e = warp_sum(e);
+        if (lane == 0) s_wd[warp][i] = e;
+        __syncthreads();
+        if (tid == 0) {
+            float dd = 0.f;
+            for (int w = 0; w < NW; ++w) dd += s_wd[w][i];
+            sh.md[i] = make_float2(M, dd);
         }
     }
-    // fold the 8 warps in fixed order
-    __shared__ float s_m[NW][NB], s_d[NW][NB];
-    __shared__ int s_last;
-    if ((lane & ((32 / NB) - 1)) == 0) { s_m[warp][myq] = m; s_d[warp][myq] = Dsum; }
-    __syncthreads();
-    if (threadIdx.x < nb) {
-        const int i = threadIdx.x;
+    cluster.sync();
+    // ---- global (m, D) per query, ranks folded in order ----
+    if (tid < nb) {
         float mm = -INFINITY, dd = 0.f;
-        for (int w = 0; w < NW; ++w) md_combine(mm, dd, s_m[w][i], s_d[w][i]);
-        lv.part[((size_t)(b0 + i) * H + h) * gridDim.x + chunk] = make_float2(mm, dd);
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int t = atomicAdd(lv.tick + (size_t)g * H + h, 1);
-        s_last = (t == (int)gridDim.x - 1);
-        if (s_last) lv.tick[(size_t)g * H + h] = 0;
+        for (int r = 0; r < NC; ++r) {
+            const DecodeSmem<NB> *o = cluster.map_shared_rank(&sh, r);
+            md_combine(mm, dd, o->md[tid].x, o->md[tid].y);
+        }
+        s_M[tid] = mm;
+        s_lD[tid] = logf(dd);
+        if (rank == 0 && lv.dbg_lse) lv.dbg_lse[(size_t)(b0 + tid) * H + h] = mm + logf(dd);
     }
     __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-
+    // ---- threshold + ordered compaction of the CTA's rows ----
+    const bool all = !(lv.T > 0.f);
+    const float logT = all ? 0.f : logf(lv.T);
     for (int i = 0; i < nb; ++i) {
         const int bh = (b0 + i) * H + h;
-        __shared__ float s_M, s_lD;
-        if (warp == 0) {
-            float mm = -INFINITY, dd = 0.f;
-            for (int j = lane; j < (int)gridDim.x; j += 32) {
-                float2 p = ldcg(lv.part + (size_t)bh * gridDim.x + j);
-                md_combine(mm, dd, p.x, p.y);
+        const float M = s_M[i], lD = s_lD[i], thr = lD + logT;
+        int run = 0, runk = 0;
+        for (int base = 0; base < nloc; base += NT) {
+            const int rr = base + tid;
+            const bool valid = rr < nloc;
+            const int row = valid ? (ROWLIST ? s_row[rr] : r0 + rr) : 0;
+            const float x = valid ? s_log[i * rpc + rr] - M : 0.f;
+            const bool sel = valid && (all || x > thr);
+            if (valid && lv.dbg_S) lv.dbg_S[(size_t)bh * c + row] = expf(x - lD);
+            if (valid && lv.bitmap) lv.bitmap[(size_t)bh * c + row] = sel ? 1 : 0;
+            int st = 0, n = 0;
+            if (sel) { st = __ldg(off + row); n = __ldg(off + row + 1) - st; }
+            int pos, kpre, tc, tk;
+            tile_scan(sel, n, pos, kpre, tc, tk);
+            if (sel) {
+                s_sel[i * rpc + run + pos] = row;
+                s_st[i * rpc + run + pos] = st;
+                s_n[i * rpc + run + pos] = n;
+                s_kp[i * rpc + run + pos] = runk + kpre;
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                float m2 = __shfl_xor_sync(FULL, mm, o), d2 = __shfl_xor_sync(FULL, dd, o);
-                md_combine(mm, dd, m2, d2);
-            }
-            if (lane == 0) { s_M = mm; s_lD = logf(dd); }
+            run += tc;
+            runk += tk;
         }
-        __syncthreads();
-        const float M = s_M, lD = s_lD;
-        const bool all = !(lv.T > 0.f);
-        const float thr = all ? -INFINITY : lD + logf(lv.T);
-        if (threadIdx.x == 0 && lv.dbg_lse) lv.dbg_lse[bh] = M + lD;
-        const float *lg = lv.logits + (size_t)bh * c;
-        const int nr = ROWLIST ? ldcg(lv.n_rows + bh) : c;
-        finalize_rows<ROWLIST>(lv, bh, h, nr, [&](int row, float &dbg) {
-            const float x = ldcg(lg + row) - M;
-            dbg = expf(x - lD);
-            return all || (x > thr);
-        });
-        __syncthreads();
+        if (tid == 0) { sh.cnt[i] = run; sh.keys[i] = runk; }
     }
+    cluster.sync();
+    // ---- cluster-wide offsets, then write the lists and expand the ranges ----
+    for (int i = 0; i < nb; ++i) {
+        const int bh = (b0 + i) * H + h;
+        int oc = 0, ok = 0, tc = 0, tk = 0;
+        for (int r = 0; r < NC; ++r) {
+            const DecodeSmem<NB> *o = cluster.map_shared_rank(&sh, r);
+            const int cr = o->cnt[i], kr = o->keys[i];
+            if (r < rank) { oc += cr; ok += kr; }
+            tc += cr;
+            tk += kr;
+        }
+        const int mine = sh.cnt[i];
+        int32_t *list = lv.list + (size_t)bh * c + oc;
+        int32_t *exp_list = lv.exp_list + (size_t)bh * lv.exp_stride + ok;
+        for (int j = tid; j < mine; j += NT) list[j] = s_sel[i * rpc + j];
+        for (int j = warp; j < mine; j += NW) {
+            const int st = s_st[i * rpc + j], n = s_n[i * rpc + j], kp = s_kp[i * rpc + j];
+            for (int t = lane; t < n; t += 32) exp_list[kp + t] = st + t;
+        }
+        if (rank == 0 && tid == 0) {
+            lv.n_list[bh] = tc;
+            lv.n_exp[bh] = tk;
+        }
+    }
+    cluster.sync();  // keep this CTA's smem alive until every rank has read it
 }
+
+static size_t decode_smem_bytes(int NB, int rpc) { return (size_t)rpc * 4 * (NB + 1 + 4 * NB) + 16; }
 
 // --------------------------------------------------------------------------
 // Prefill pass 1: LSE_t over the row space for every query row.
@@ -392,6 +506,32 @@ __global__ void __launch_bounds__(NT) k_prefill_colsum(LookupShape s, const T *_
 }
 
 // --------------------------------------------------------------------------
+template <typename T, int D, int NB, bool RL>
+static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
+                                 int groups, cudaStream_t st) {
+    const int rpc = (rowspace + NC - 1) / NC;
+    const size_t smem = decode_smem_bytes(NB, rpc);
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    auto kern = k_lookup_decode<T, D, NB, RL>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(NC, s.H, groups);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = NC;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, s, Q, lv, rpc);
+}
+
 template <typename T, int D>
 static cudaError_t launch_level_t(const LookupShape &s, const T *Q, const LevelArgs &lv,
                                   cudaStream_t st) {
@@ -399,33 +539,21 @@ static cudaError_t launch_level_t(const LookupShape &s, const T *Q, const LevelA
     const int rowspace = rl ? lv.row_stride : lv.c;
     const int nch = (rowspace + CH - 1) / CH;
     if (s.n_q == 1) {
-        if (rl) {
-            dim3 grid(nch, s.H, s.B);
-            k_scan_decode<T, D, 1, true><<<grid, NT, 0, st>>>(s, Q, lv);
-        } else if (s.B >= 8) {
-            dim3 grid(nch, s.H, (s.B + 7) / 8);
-            k_scan_decode<T, D, 8, false><<<grid, NT, 0, st>>>(s, Q, lv);
-        } else if (s.B >= 4) {
-            dim3 grid(nch, s.H, (s.B + 3) / 4);
-            k_scan_decode<T, D, 4, false><<<grid, NT, 0, st>>>(s, Q, lv);
-        } else if (s.B >= 2) {
-            dim3 grid(nch, s.H, (s.B + 1) / 2);
-            k_scan_decode<T, D, 2, false><<<grid, NT, 0, st>>>(s, Q, lv);
-        } else {
-            dim3 grid(nch, s.H, s.B);
-            k_scan_decode<T, D, 1, false><<<grid, NT, 0, st>>>(s, Q, lv);
-        }
+        if (rl) return launch_decode<T, D, 1, true>(s, Q, lv, rowspace, s.B, st);
+        if (s.B >= 8) return launch_decode<T, D, 8, false>(s, Q, lv, rowspace, (s.B + 7) / 8, st);
+        if (s.B >= 4) return launch_decode<T, D, 4, false>(s, Q, lv, rowspace, (s.B + 3) / 4, st);
+        if (s.B >= 2) return launch_decode<T, D, 2, false>(s, Q, lv, rowspace, (s.B + 1) / 2, st);
+        return launch_decode<T, D, 1, false>(s, Q, lv, rowspace, s.B, st);
+    }
+    const int nqt = (s.n_q + QT - 1) / QT;
+    dim3 g1(nqt, s.B * s.H);
+    dim3 g2(nch, nqt, s.B * s.H);
+    if (rl) {
+        k_prefill_rowlse<T, D, true><<<g1, NT, 0, st>>>(s, Q, lv);
+        k_prefill_colsum<T, D, true><<<g2, NT, 0, st>>>(s, Q, lv);
     } else {
-        const int nqt = (s.n_q + QT - 1) / QT;
-        dim3 g1(nqt, s.B * s.H);
-        dim3 g2(nch, nqt, s.B * s.H);
-        if (rl) {
-            k_prefill_rowlse<T, D, true><<<g1, NT, 0, st>>>(s, Q, lv);
-            k_prefill_colsum<T, D, true><<<g2, NT, 0, st>>>(s, Q, lv);
-        } else {
-            k_prefill_rowlse<T, D, false><<<g1, NT, 0, st>>>(s, Q, lv);
-            k_prefill_colsum<T, D, false><<<g2, NT, 0, st>>>(s, Q, lv);
-        }
+        k_prefill_rowlse<T, D, false><<<g1, NT, 0, st>>>(s, Q, lv);
+        k_prefill_colsum<T, D, false><<<g2, NT, 0, st>>>(s, Q, lv);
     }
     return cudaGetLastError();
 }

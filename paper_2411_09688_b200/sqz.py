@@ -249,10 +249,12 @@ class Selection:
 
 
 class Workspaces:
-    """Cached zero-initialised workspaces (the library keeps them re-usable)."""
+    """Cached zero-initialised workspaces, one per call geometry (the library
+    leaves a workspace re-usable by later calls with the same geometry)."""
 
     def __init__(self):
         self._ws = {}
+        self.last_attn = None
 
     def get(self, key, nbytes, device):
         t = self._ws.get(key)
@@ -287,7 +289,8 @@ def centroid_lookup(idx: Index, Q: torch.Tensor, scale: float, T: float, T1: flo
         sel = Selection.empty(idx, B, n_q, debug, Q.device)
     s = idx.struct()
     if ws is None:
-        ws = _WS.get(("lookup", Q.device), lookup_workspace_bytes(idx, B, n_q), Q.device)
+        ws = _WS.get(("lookup", Q.device, idx.H, idx.L, idx.c1, idx.c2, B, n_q),
+                     lookup_workspace_bytes(idx, B, n_q), Q.device)
     p = sqz_lookup_params(scale, T, T1)
     ss = sel.struct()
     _check(lib().sqz_centroid_lookup(ctypes.byref(s), _p(Q), B, n_q, ctypes.byref(p),
@@ -310,7 +313,9 @@ def sparse_attention(Q, Kp, Vp, idx: Index, sel: Selection, Ku=None, Vu=None, sc
         LSE = torch.empty(B, H, n_q, dtype=torch.float32, device=Q.device)
     s = idx.struct()
     if ws is None:
-        ws = _WS.get(("attn", Q.device), attention_workspace_bytes(idx, B, n_q, n_u), Q.device)
+        ws = _WS.get(("attn", Q.device, idx.H, idx.L, B, n_q, n_u),
+                     attention_workspace_bytes(idx, B, n_q, n_u), Q.device)
+        _WS.last_attn = ws
     p = sqz_attn_params(scale, int(causal), int(partial), out_dtype)
     ss = sel.struct()
     _check(lib().sqz_sparse_attention(_p(Q), B, n_q, _p(Kp), _p(Vp), ctypes.byref(s),
@@ -319,13 +324,11 @@ def sparse_attention(Q, Kp, Vp, idx: Index, sel: Selection, Ku=None, Vu=None, sc
     return O, LSE
 
 
-def attention_status(ws: torch.Tensor = None, device="cuda"):
+def attention_status(ws: torch.Tensor = None):
+    """sqz_attention_status on `ws` (default: the workspace of the last
+    sparse_attention call made through this module)."""
     if ws is None:
-        ws = _WS._ws.get(("attn", torch.device(device) if isinstance(device, str) else device))
-        if ws is None:
-            for k, v in _WS._ws.items():
-                if k[0] == "attn":
-                    ws = v
+        ws = _WS.last_attn
     _check(lib().sqz_attention_status(_p(ws), ws.numel(), _stream()))
 
 
