@@ -435,10 +435,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--kmeans-iters", type=int, default=30)
+    ap.add_argument("--retention", type=float, default=None,
+                    help="override the config's retention target (1.0 = T = 0, dense)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.retention is not None:
+        cfg["retention"] = args.retention
+        cfg["workload"] += f" [retention override {args.retention}]"
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -1,0 +1,535 @@
+// attention.cu -- sparse attention over the selected fixed-context keys plus
+// the user KV (section 4.2), split-KV + merge, one kernel launch.
+//
+// Every query row owns a key STREAM: its selected fixed keys (key_idx,
+// cluster-major positions into Kp/Vp) followed by its visible user keys
+// (causal, bottom-right aligned in prefill, R8).  The streams are split into
+// segments; each segment yields a normalised partial (o, lse) and the CTA that
+// completes a row's last segment merges the row's partials with the partial
+// maxima/denominators (atomic ticket, so a call is ONE launch).
+//
+// Decode (n_q == 1): PERSISTENT CTAs (grid = SMs x occupancy) split the
+// concatenation of all rows' streams into equal contiguous key ranges -- "a
+// fixed number of desired keys and values ... for a single SM": a head
+// with more selected keys is spread over more SMs, every CTA moves the same
+// number of bytes, and a CTA pays the per-segment setup once or twice.  The
+// ranges are derived on the device from n_keys, so nothing returns to the
+// host.  Prefill rows use a 2-D grid of (row, fixed-size segment).
+//
+// Data movement is TMA-staged: a producer warp turns each 32-key slice of a
+// segment into runs of consecutive positions (selected clusters are contiguous
+// in the cluster-major layout, so a slice is usually 1-2 runs) and issues one
+// cp.async.bulk per run for K and for V into a NSTAGE-deep shared-memory ring,
+// completing on an mbarrier (bytes-counted).  Four consumer warps read the
+// stage from shared memory (a G = d/8 lane group per key row, conflict-free
+// 16-byte reads), reduce the partial dot products with a transposed butterfly
+// and run the online softmax in the log2 domain; they release the stage with
+// an mbarrier arrive.  The kernel is launched with programmatic stream
+// serialization; griddepcontrol.wait orders it after the lookup kernel.
+#include "common.cuh"
+#include "internal.h"
+#include "tma.cuh"
+
+namespace sqz {
+
+constexpr int NCW = 4;             // consumer warps
+constexpr int NCT = NCW * 32;      // consumer threads
+constexpr int AT_NT = NCT + 32;    // + one producer warp
+constexpr int AT_NW = AT_NT / 32;
+constexpr int KS = 32;             // keys per pipeline stage
+constexpr int NSTAGE = 4;          // ring depth
+constexpr int KPWS = KS / NCW;     // keys per consumer warp per stage
+constexpr int MAX_PERSIST_CTAS = 1184;  // 148 SMs x 8
+constexpr int MIN_KEYS = 256;           // minimum keys per persistent CTA
+
+int attention_kch(int n_q) { return n_q == 1 ? 256 : 1024; }
+int attention_max_parts(int64_t L, int n_u, int n_q) {
+    const int kch = attention_kch(n_q);
+    const int grid_parts = (int)((L + n_u + kch - 1) / kch);
+    return n_q == 1 ? (grid_parts > MAX_PERSIST_CTAS ? grid_parts : MAX_PERSIST_CTAS) : grid_parts;
+}
+
+template <typename T, int D> struct Ring {
+    static constexpr int ROWB = D * (int)sizeof(T);
+    static constexpr int STAGE_ELEMS = 2 * KS * D;  // K then V
+    static constexpr size_t BYTES = (size_t)NSTAGE * STAGE_ELEMS * sizeof(T);
+};
+
+// NV values per lane, reduced over aligned groups of G lanes; lane ends with
+// the group sum of value index (sub >> (log2 G - log2 NV)) & (NV - 1).
+template <int NV, int G>
+__device__ __forceinline__ float group_transpose_reduce(float (&v)[NV], int lane) {
+    int stride = G / 2;
+#pragma unroll
+    for (int w = NV; w > 1; w >>= 1) {
+        const bool hi = lane & stride;
+#pragma unroll
+        for (int k = 0; k < w / 2; ++k) {
+            float keep = hi ? v[k + w / 2] : v[k];
+            float send = hi ? v[k] : v[k + w / 2];
+            v[k] = keep + __shfl_xor_sync(FULL, send, stride);
+        }
+        stride >>= 1;
+    }
+#pragma unroll
+    for (; stride >= 1; stride >>= 1) v[0] += __shfl_xor_sync(FULL, v[0], stride);
+    return v[0];
+}
+
+__device__ __forceinline__ void lds8(const __nv_bfloat16 *p, float (&f)[8]) {
+    const uint4 u = *reinterpret_cast<const uint4 *>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = __uint_as_float(w[i] << 16);
+        f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+}
+__device__ __forceinline__ void lds8(const float *p, float (&f)[8]) {
+    const float4 a = reinterpret_cast<const float4 *>(p)[0];
+    const float4 b = reinterpret_cast<const float4 *>(p)[1];
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+// A row's key stream: nkf selected fixed keys, then nu visible user keys.
+struct RowInfo {
+    int bh, h, nkf, nu;
+    __device__ __forceinline__ int total() const { return nkf + nu; }
+};
+__device__ __forceinline__ RowInfo row_info(const AttnArgs &a, int row) {
+    RowInfo r;
+    r.bh = row / a.n_q;
+    r.h = r.bh % a.H;
+    const int t = row % a.n_q;
+    r.nkf = ldcg(a.n_keys + r.bh);
+    int vis = a.causal ? t + a.n_u - a.n_q + 1 : a.n_u;
+    r.nu = max(0, min(vis, a.n_u));
+    return r;
+}
+
+// One segment [a0, a1) of a row's stream, its partial slot and the number of
+// partials the row has.
+struct Seg {
+    int row, a0, a1, slot, nparts;
+};
+
+// Merge of one row's partials by the NCT consumer threads:
+// O = sum_p e^(lse_p - M) o_p / L, LSE = M + log L.
+template <int D>
+__device__ void merge_row(const AttnArgs &a, int row, int P, float *s_w, float *s_red) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float *lse = a.part_lse + (size_t)row * a.max_chunks;
+    float mx = -INFINITY;
+    for (int p = tid; p < P; p += NCT) mx = fmaxf(mx, ldcg(lse + p));
+    mx = warp_max(mx);
+    if (lane == 0) s_red[warp] = mx;
+    named_bar(1, NCT);
+    float M = -INFINITY;
+    for (int w = 0; w < NCW; ++w) M = fmaxf(M, s_red[w]);
+    named_bar(1, NCT);
+    float acc = 0.f, lsum = 0.f;
+    for (int p0 = 0; p0 < P; p0 += NCT) {
+        const int p = p0 + tid;
+        const float w = (p < P && M != -INFINITY) ? expf(ldcg(lse + p) - M) : 0.f;
+        s_w[tid] = w;
+        lsum += w;
+        named_bar(1, NCT);
+        const int np = min(NCT, P - p0);
+        if (tid < D) {
+            const float *op = a.part_o + ((size_t)row * a.max_chunks + p0) * D + tid;
+#pragma unroll 8
+            for (int j = 0; j < np; ++j) acc = fmaf(s_w[j], ldcg(op + (size_t)j * D), acc);
+        }
+        named_bar(1, NCT);
+    }
+    lsum = warp_sum(lsum);
+    if (lane == 0) s_red[warp] = lsum;
+    named_bar(1, NCT);
+    float L = 0.f;
+    for (int w = 0; w < NCW; ++w) L += s_red[w];
+    if (tid < D) {
+        const float v = (M == -INFINITY) ? 0.f : acc / L;
+        if (a.out_dtype == SQZ_BF16)
+            reinterpret_cast<__nv_bfloat16 *>(a.O)[(size_t)row * D + tid] = __float2bfloat16_rn(v);
+        else
+            reinterpret_cast<float *>(a.O)[(size_t)row * D + tid] = v;
+    }
+    if (tid == 0) {
+        a.LSE[row] = (M == -INFINITY) ? -INFINITY : M + logf(L);
+        if (M == -INFINITY && !a.partial) atomicOr(a.status, 1);
+    }
+    named_bar(1, NCT);
+}
+
+// Rows with no key at all (no selected fixed key, no visible user key) get the
+// identity partial O = 0, LSE = -inf (an error for final outputs).
+template <int D>
+__device__ void empty_row(const AttnArgs &a, int row) {
+    for (int k = threadIdx.x; k < D; k += blockDim.x) {
+        if (a.out_dtype == SQZ_BF16)
+            reinterpret_cast<__nv_bfloat16 *>(a.O)[(size_t)row * D + k] = __float2bfloat16_rn(0.f);
+        else
+            reinterpret_cast<float *>(a.O)[(size_t)row * D + k] = 0.f;
+    }
+    if (threadIdx.x == 0) {
+        a.LSE[row] = -INFINITY;
+        if (!a.partial) atomicOr(a.status, 1);
+    }
+}
+
+// Iterates the segments of this CTA.
+template <bool PERSIST> struct SegIter {
+    const AttnArgs *a;
+    const int *pref;   // PERSIST: exclusive prefix of row stream lengths, [rows + 1]
+    int rows, r;
+    long long ks, ke, K;
+    int G;
+    bool done;
+    __device__ __forceinline__ int cta_of(long long x) const {  // CTA whose range holds key x
+        return (int)(((x + 1) * (long long)G - 1) / K);
+    }
+    __device__ void init(const AttnArgs &aa, const int *p, int nrows) {
+        a = &aa;
+        pref = p;
+        rows = nrows;
+        done = false;
+        if (PERSIST) {
+            // at least MIN_KEYS keys per CTA: small problems use fewer CTAs
+            K = pref[rows];
+            G = (int)min((long long)gridDim.x, max(1LL, (K + MIN_KEYS - 1) / MIN_KEYS));
+            if ((int)blockIdx.x >= G || K == 0) { r = rows; ke = 0; return; }
+            ks = (long long)blockIdx.x * K / G;
+            ke = (long long)(blockIdx.x + 1) * K / G;
+            int lo = 0, hi = rows - 1;  // last row with pref <= ks
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (pref[mid] <= ks) lo = mid; else hi = mid - 1;
+            }
+            r = lo;
+        }
+    }
+    __device__ bool next(Seg &s) {
+        if (PERSIST) {
+            while (r < rows && pref[r] < ke) {
+                const long long rs = pref[r], re = pref[r + 1];
+                const int row = r++;
+                if (re <= ks || re == rs) continue;
+                s.row = row;
+                s.a0 = (int)(max(ks, rs) - rs);
+                s.a1 = (int)(min(ke, re) - rs);
+                const int wf = cta_of(rs), wl = cta_of(re - 1);
+                s.slot = (int)blockIdx.x - wf;
+                s.nparts = wl - wf + 1;
+                return true;
+            }
+            return false;
+        }
+        if (done) return false;
+        done = true;
+        const RowInfo ri = row_info(*a, blockIdx.x);
+        const int n = ri.total();
+        s.row = blockIdx.x;
+        s.a0 = blockIdx.y * a->kch;
+        s.a1 = min(n, s.a0 + a->kch);
+        s.slot = blockIdx.y;
+        s.nparts = (n + a->kch - 1) / a->kch;
+        return s.a0 < n;
+    }
+};
+
+template <typename T, int D, bool PERSIST>
+__global__ void __launch_bounds__(AT_NT) k_attend(AttnArgs a, int rows) {
+    using R = Ring<T, D>;
+    constexpr int G = D / 8;            // lanes per key row (8 elements each)
+    constexpr int KPW = 32 / G;         // key rows per warp instruction
+    constexpr int NS = KPWS / KPW;      // key slots per lane per stage
+    constexpr int LPS = G / NS;         // lanes holding each reduced key
+    constexpr int LG_G = G == 16 ? 4 : 3;
+    constexpr int LG_NS = NS == 4 ? 2 : NS == 2 ? 1 : 0;
+
+    extern __shared__ __align__(128) unsigned char dyn[];
+    T *ring = reinterpret_cast<T *>(dyn);
+    uint64_t *full = reinterpret_cast<uint64_t *>(dyn + R::BYTES);
+    uint64_t *empty = full + NSTAGE;
+    int *s_pref = reinterpret_cast<int *>(empty + NSTAGE);
+    __shared__ float s_m[NCW], s_l[NCW], s_o[NCW * D], s_w[NCT], s_red[NCW];
+    __shared__ int s_last;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        mbar_fence_init();
+    }
+    // the selection comes from the preceding lookup kernel (programmatic
+    // dependent launch: everything above this line overlaps its tail)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    if (PERSIST) {
+        // exclusive prefix of the row stream lengths (rows <= a few thousand)
+        __shared__ int s_ws[AT_NW];
+        if (tid == 0) s_pref[0] = 0;
+        for (int base = 0; base < rows; base += AT_NT) {
+            __syncthreads();
+            const int r = base + tid;
+            const int len = r < rows ? row_info(a, r).total() : 0;
+            int inc = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(FULL, inc, o);
+                if (lane >= o) inc += t;
+            }
+            if (lane == 31) s_ws[warp] = inc;
+            __syncthreads();
+            int wb = 0;
+            for (int w = 0; w < warp; ++w) wb += s_ws[w];
+            const int basev = s_pref[base];
+            __syncthreads();
+            if (r < rows) s_pref[r + 1] = basev + wb + inc;
+        }
+        __syncthreads();
+        for (int r = blockIdx.x; r < rows; r += gridDim.x)
+            if (s_pref[r + 1] == s_pref[r]) empty_row<D>(a, r);
+    } else {
+        if (blockIdx.y == 0 && row_info(a, blockIdx.x).total() == 0) empty_row<D>(a, blockIdx.x);
+    }
+    __syncthreads();
+
+    SegIter<PERSIST> it;
+    it.init(a, s_pref, rows);
+    Seg sg;
+
+    if (warp == NCW) {
+        // ================= producer warp: TMA bulk copies =================
+        const uint64_t pol = policy_evict_first();
+        int st = 0;
+        uint32_t ph = 0;
+        while (it.next(sg)) {
+            const RowInfo ri = row_info(a, sg.row);
+            const T *Kf = reinterpret_cast<const T *>(a.Kp) + (size_t)ri.h * a.L * D;
+            const T *Vf = reinterpret_cast<const T *>(a.Vp) + (size_t)ri.h * a.L * D;
+            const T *Ku = reinterpret_cast<const T *>(a.Ku) + (size_t)ri.bh * a.n_u * D;
+            const T *Vu = reinterpret_cast<const T *>(a.Vu) + (size_t)ri.bh * a.n_u * D;
+            const int32_t *kidx = a.key_idx + (size_t)ri.bh * a.L;
+            for (int g0 = sg.a0; g0 < sg.a1; g0 += 8 * KS) {
+                // stream positions of the next 8 stages: one load latency per 8 stages
+                int posr[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = g0 + u * KS + lane;
+                    posr[u] = k < sg.a1 ? (k < ri.nkf ? ldcg(kidx + k) : k - ri.nkf) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j0 = g0 + u * KS;
+                    if (j0 >= sg.a1) break;
+                    mbar_wait(&empty[st], ph ^ 1);
+                    const int nk = min(KS, sg.a1 - j0);
+                    const int k = j0 + lane;
+                    const bool user = k >= ri.nkf;
+                    const int pos = posr[u];
+                    const int prev = __shfl_up_sync(FULL, pos, 1);
+                    const bool prev_user = __shfl_up_sync(FULL, (int)user, 1);
+                    const bool start = lane < nk && (lane == 0 || pos != prev + 1 || user != prev_user);
+                    const unsigned starts = __ballot_sync(FULL, start);
+                    if (lane == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * nk * R::ROWB));
+                    __syncwarp();
+                    if (start) {
+                        const unsigned later = starts & ~((2u << lane) - 1u);
+                        const int end = later ? __ffs(later) - 1 : nk;
+                        const uint32_t bytes = (uint32_t)((end - lane) * R::ROWB);
+                        T *sK = ring + (size_t)st * R::STAGE_ELEMS + (size_t)lane * D;
+                        T *sV = sK + KS * D;
+                        bulk_g2s(sK, (user ? Ku : Kf) + (size_t)pos * D, bytes, &full[st], pol);
+                        bulk_g2s(sV, (user ? Vu : Vf) + (size_t)pos * D, bytes, &full[st], pol);
+                    }
+                    if (++st == NSTAGE) { st = 0; ph ^= 1; }
+                }
+            }
+        }
+        return;
+    }
+
+    // ================= consumer warps =================
+    const int g = lane / G, sub = lane % G;
+    const int myslot = sub >> (LG_G - LG_NS);
+    int st = 0;
+    uint32_t ph = 0;
+    while (it.next(sg)) {
+        float q[8];
+        load8(reinterpret_cast<const T *>(a.Q) + (size_t)sg.row * D + sub * 8, q);
+        const float sc = a.scale * LOG2E;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q[k] *= sc;
+        float m_run = -INFINITY, l_lane = 0.f, o[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = 0.f;
+
+        for (int j0 = sg.a0; j0 < sg.a1; j0 += KS) {
+            mbar_wait(&full[st], ph);
+            const int nk = min(KS, sg.a1 - j0);
+            const T *sK = ring + (size_t)st * R::STAGE_ELEMS;
+            const T *sV = sK + KS * D;
+            const int kb = warp * KPWS;  // this warp's keys in the stage
+            if (kb < nk) {
+                float v[NS];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    const int kk = kb + s * KPW + g;
+                    float f[8];
+                    lds8(sK + kk * D + sub * 8, f);
+                    float acc = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) acc = fmaf(q[k], f[k], acc);
+                    v[s] = acc;
+                }
+                float z = group_transpose_reduce<NS, G>(v, lane);
+                if (kb + myslot * KPW + g >= nk) z = -INFINITY;
+                const float mx = warp_max(z);
+                const float m_new = fmaxf(m_run, mx);
+                const float alpha = fast_exp2(m_run - m_new);  // m_run = -inf -> 0
+                const float p = fast_exp2(z - m_new);          // z = -inf -> 0
+                l_lane = l_lane * alpha + p;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) o[k] *= alpha;
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    const float ps = __shfl_sync(FULL, p, g * G + s * LPS);
+                    const int kk = kb + s * KPW + g;
+                    if (kk < nk) {
+                        float f[8];
+                        lds8(sV + kk * D + sub * 8, f);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) o[k] = fmaf(ps, f[k], o[k]);
+                    }
+                }
+                m_run = m_new;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == NSTAGE) { st = 0; ph ^= 1; }
+        }
+        // ---- segment epilogue: fold key groups, then the consumer warps ----
+#pragma unroll
+        for (int s2 = G; s2 < 32; s2 <<= 1)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] += __shfl_xor_sync(FULL, o[k], s2);
+        const float l_w = warp_sum(l_lane) * (1.0f / LPS);
+        if (lane == 0) { s_m[warp] = m_run; s_l[warp] = l_w; }
+        if (g == 0) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s_o[warp * D + sub * 8 + k] = o[k];
+        }
+        named_bar(1, NCT);
+        if (tid < D) {
+            float M = -INFINITY;
+            for (int w = 0; w < NCW; ++w) M = fmaxf(M, s_m[w]);
+            float L = 0.f, O = 0.f;
+            for (int w = 0; w < NCW; ++w) {
+                const float e = (s_m[w] == -INFINITY) ? 0.f : exp2f(s_m[w] - M);
+                L += s_l[w] * e;
+                O += s_o[w * D + tid] * e;
+            }
+            const size_t slot = (size_t)sg.row * a.max_chunks + sg.slot;
+            a.part_o[slot * D + tid] = L > 0.f ? O / L : 0.f;
+            if (tid == 0) a.part_lse[slot] = L > 0.f ? (M + log2f(L)) * LN2 : -INFINITY;
+        }
+        // the CTA that completes a row's last segment merges its partials
+        __threadfence();
+        named_bar(1, NCT);
+        if (tid == 0) {
+            const int t = atomicAdd(a.row_cnt + sg.row, 1);
+            s_last = (t == sg.nparts - 1);
+            if (s_last) a.row_cnt[sg.row] = 0;
+        }
+        named_bar(1, NCT);
+        if (s_last) {
+            __threadfence();
+            merge_row<D>(a, sg.row, sg.nparts, s_w, s_red);
+        }
+    }
+}
+
+template <typename T, int D>
+static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
+    const int rows = a.B * a.H * a.n_q;
+    if (rows == 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(AT_NT);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const size_t ring = Ring<T, D>::BYTES + 2 * NSTAGE * sizeof(uint64_t);
+    if (a.n_q == 1 && rows <= 8192) {
+        const size_t dsm = ring + (size_t)(rows + 1) * sizeof(int);
+        auto kern = k_attend<T, D, true>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+        if (e != cudaSuccess) return e;
+        int dev = 0, nsm = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, AT_NT, dsm);
+        if (occ < 1) occ = 1;
+        cfg.gridDim = dim3(std::min(nsm * occ, MAX_PERSIST_CTAS));
+        cfg.dynamicSmemBytes = dsm;
+        return cudaLaunchKernelEx(&cfg, kern, a, rows);
+    }
+    auto kern = k_attend<T, D, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring);
+    if (e != cudaSuccess) return e;
+    cfg.gridDim = dim3(rows, a.max_chunks);
+    cfg.dynamicSmemBytes = ring;
+    return cudaLaunchKernelEx(&cfg, kern, a, rows);
+}
+
+cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st) {
+    if (a.dtype == SQZ_BF16) {
+        if (a.d == 128) return launch_t<__nv_bfloat16, 128>(a, st);
+        return launch_t<__nv_bfloat16, 64>(a, st);
+    }
+    if (a.d == 128) return launch_t<float, 128>(a, st);
+    return launch_t<float, 64>(a, st);
+}
+
+// Generic merge of P partial results (multi-shard / multi-call).
+template <typename TO>
+__global__ void k_merge_parts(int P, const float *__restrict__ Op, const float *__restrict__ Lp,
+                              int64_t rows, int d, TO *O, float *LSE) {
+    const int64_t row = blockIdx.x;
+    float M = -INFINITY;
+    for (int p = 0; p < P; ++p) M = fmaxf(M, Lp[(size_t)p * rows + row]);
+    float L = 0.f;
+    if (M != -INFINITY)
+        for (int p = 0; p < P; ++p) L += expf(Lp[(size_t)p * rows + row] - M);
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+        float acc = 0.f;
+        if (M != -INFINITY)
+            for (int p = 0; p < P; ++p) {
+                const float w = expf(Lp[(size_t)p * rows + row] - M);
+                if (w > 0.f) acc += w * Op[((size_t)p * rows + row) * d + k];
+            }
+        O[(size_t)row * d + k] = from_f32<TO>(M == -INFINITY ? 0.f : acc / L);
+    }
+    if (threadIdx.x == 0) LSE[row] = (M == -INFINITY) ? -INFINITY : M + logf(L);
+}
+
+cudaError_t launch_merge(int P, const float *O_parts, const float *LSE_parts, int64_t rows, int d,
+                         void *O, float *LSE, int out_dtype, cudaStream_t st) {
+    if (rows == 0) return cudaSuccess;
+    const int nt = d >= 128 ? 128 : 64;
+    if (out_dtype == SQZ_BF16)
+        k_merge_parts<__nv_bfloat16><<<(unsigned)rows, nt, 0, st>>>(P, O_parts, LSE_parts, rows, d,
+                                                                    (__nv_bfloat16 *)O, LSE);
+    else
+        k_merge_parts<float><<<(unsigned)rows, nt, 0, st>>>(P, O_parts, LSE_parts, rows, d,
+                                                           (float *)O, LSE);
+    return cudaGetLastError();
+}
+
+}  // namespace sqz
