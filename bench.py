@@ -207,6 +207,22 @@ def cpu_oracle_run(cfg, steps=None, warmup=0, seconds=12.0, h_sample=4):
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
+def capture_graph(fn):
+    """Capture `fn` (a sequence of libsqz calls on the current stream) into a CUDA
+    graph; one eager warm-up call first fills the library's host-side caches."""
+    import torch
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, capture_error_mode="thread_local"):
+        fn()
+    return g
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -304,26 +320,49 @@ def run_gpu(args, cfg, rank, world, local_rank):
         step(i)
     torch.cuda.synchronize()
     K_ = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K_)]
+    # The step is replayed as a CUDA graph (one per test input): the two kernels
+    # are chained by programmatic dependent launch and no host launch latency
+    # sits between them.  The eager (per-call) figure is reported beside it.
+    graphs = [capture_graph(lambda i=i: step(i)) for i in range(n_inputs)] if args.graph else None
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K_)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         for i in range(K_):
             flush.zero_()
-            q = Qt[i % n_inputs]
             ev[i][0].record()
-            sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel)
+            if graphs:
+                graphs[i % n_inputs].replay()
+            else:
+                step(i)
             ev[i][1].record()
-            sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale,
-                                 causal=cfg["mode"] == "prefill", O=O, LSE=LSE)
-            ev[i][2].record()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    t_step = sum(e[0].elapsed_time(e[2]) for e in ev) / K_  # ms
-    t_look = sum(e[0].elapsed_time(e[1]) for e in ev) / K_
-    t_attn = sum(e[1].elapsed_time(e[2]) for e in ev) / K_
+    t_step = sum(e[0].elapsed_time(e[1]) for e in ev) / K_  # ms
+    eve = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K_)]
+    for i in range(K_):
+        flush.zero_()
+        eve[i][0].record()
+        step(i)
+        eve[i][1].record()
+    torch.cuda.synchronize()
+    t_eager = sum(e[0].elapsed_time(e[1]) for e in eve) / K_
+    # per-phase attribution (separate pass: the middle event breaks the PDL overlap)
+    evp = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K_)]
+    for i in range(K_):
+        flush.zero_()
+        q = Qt[i % n_inputs]
+        evp[i][0].record()
+        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel)
+        evp[i][1].record()
+        sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale,
+                             causal=cfg["mode"] == "prefill", O=O, LSE=LSE)
+        evp[i][2].record()
+    torch.cuda.synchronize()
+    t_look = sum(e[0].elapsed_time(e[1]) for e in evp) / K_
+    t_attn = sum(e[1].elapsed_time(e[2]) for e in evp) / K_
     # ---- end to end through the public API with host buffers ----
     pin = dict(pin_memory=True)
     hQ = torch.empty((n_inputs,) + tuple(Qt.shape[1:]), dtype=Qt.dtype, **pin)
@@ -345,13 +384,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         hVn.copy_(Vu.cpu())
         h2d = hQ[0].numel() * esz + 2 * hKn.numel() * esz
     d2h = hO.numel() * O.element_size() + hL.numel() * 4
-    ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K_)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for i in range(K_):
-        flush.zero_()
-        ev2[i][0].record()
+    def e2e_step(i):
         dQ.copy_(hQ[i % n_inputs], non_blocking=True)
         if cfg["mode"] == "decode":
             Ku[:, :, -1:].copy_(hKn, non_blocking=True)
@@ -364,6 +397,20 @@ def run_gpu(args, cfg, rank, world, local_rank):
                              causal=cfg["mode"] == "prefill", O=O, LSE=LSE)
         hO.copy_(O, non_blocking=True)
         hL.copy_(LSE, non_blocking=True)
+
+    e2e_graphs = ([capture_graph(lambda i=i: e2e_step(i)) for i in range(n_inputs)]
+                  if args.graph else None)
+    ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K_)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(K_):
+        flush.zero_()
+        ev2[i][0].record()
+        if e2e_graphs:
+            e2e_graphs[i % n_inputs].replay()
+        else:
+            e2e_step(i)
         ev2[i][1].record()
     torch.cuda.synchronize()
     if world > 1:
@@ -371,9 +418,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
     t_e2e = sum(e[0].elapsed_time(e[1]) for e in ev2) / K_
     # ---- max over ranks ----
     if world > 1:
-        tt = torch.tensor([t_step, t_look, t_attn, t_e2e], device=dev)
+        tt = torch.tensor([t_step, t_look, t_attn, t_e2e, t_eager], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step, t_look, t_attn, t_e2e = tt.tolist()
+        t_step, t_look, t_attn, t_e2e, t_eager = tt.tolist()
     hbm, bf16, peak_kind = load_peaks()
     tokens = B * n_q * world
     if cfg["mode"] == "decode":
@@ -416,7 +463,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    "T": T, "T1": T1, "mean_selected_keys_per_step": k_mean,
                    "retention_realized": k_mean / (B * H * L), "kmeans_iters": list(iters),
                    "index_build_s": round(t_index, 2)},
-        "phases_ms": {"lookup": round(t_look, 5), "sparse_attention": round(t_attn, 5)},
+        "phases_ms": {"lookup": round(t_look, 5), "sparse_attention": round(t_attn, 5),
+                      "eager_step": round(t_eager, 5), "graph_replay": bool(args.graph)},
         "whole_step": whole,
         "roofline": roof,
         "e2e": {"value": round(e2e_v, 3), "unit": unit, "h2d_bytes_per_step": int(h2d),
@@ -438,6 +486,8 @@ def main():
     ap.add_argument("--retention", type=float, default=None,
                     help="override the config's retention target (1.0 = T = 0, dense)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time eager per-call launches instead of CUDA-graph replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config])

@@ -315,6 +315,7 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
     a.L = idx->L; a.scale = p->scale;
     a.kch = w.kch; a.max_chunks = w.max_chunks;
     a.part_o = w.part_o; a.part_lse = w.part_lse; a.status = w.status; a.row_cnt = w.row_cnt;
+    a.sched = w.status + 1;
     a.O = O; a.LSE = LSE;
     cudaError_t e = launch_attention(a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "sparse attention launch");

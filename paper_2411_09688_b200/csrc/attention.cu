@@ -16,29 +16,24 @@
 // ranges are derived on the device from n_keys, so nothing returns to the
 // host.  Prefill rows use a 2-D grid of (row, fixed-size segment).
 //
-// Data movement is TMA-staged: a producer warp turns each 32-key slice of a
-// segment into runs of consecutive positions (selected clusters are contiguous
-// in the cluster-major layout, so a slice is usually 1-2 runs) and issues one
-// cp.async.bulk per run for K and for V into a NSTAGE-deep shared-memory ring,
-// completing on an mbarrier (bytes-counted).  Four consumer warps read the
-// stage from shared memory (a G = d/8 lane group per key row, conflict-free
-// 16-byte reads), reduce the partial dot products with a transposed butterfly
-// and run the online softmax in the log2 domain; they release the stage with
-// an mbarrier arrive.  The kernel is launched with programmatic stream
-// serialization; griddepcontrol.wait orders it after the lookup kernel.
+// Data movement: each warp streams 16 keys per round; a group of G = d/8 lanes
+// reads one key row (256 B at d=128 bf16) with 16-byte non-allocating loads,
+// the K and V rows of all 16 keys are in flight before the first FMA, and the
+// next round's key positions are prefetched.  The 16 partial dot products are
+// reduced with a transposed butterfly (8 shuffles) and the online softmax runs
+// in the log2 domain (ex2.approx).  The kernel is launched with programmatic
+// stream serialization; griddepcontrol.wait orders it after the lookup kernel.
 #include "common.cuh"
 #include "internal.h"
 #include "tma.cuh"
 
 namespace sqz {
 
-constexpr int NCW = 4;             // consumer warps
-constexpr int NCT = NCW * 32;      // consumer threads
-constexpr int AT_NT = NCT + 32;    // + one producer warp
-constexpr int AT_NW = AT_NT / 32;
-constexpr int KS = 32;             // keys per pipeline stage
-constexpr int NSTAGE = 4;          // ring depth
-constexpr int KPWS = KS / NCW;     // keys per consumer warp per stage
+SQZ_TRACE_DECL(g_trace_attn)
+
+constexpr int NCW = 4;                  // warps per CTA
+constexpr int NCT = NCW * 32;           // threads per CTA
+constexpr int KR = 16;                  // keys per warp round
 constexpr int MAX_PERSIST_CTAS = 1184;  // 148 SMs x 8
 constexpr int MIN_KEYS = 256;           // minimum keys per persistent CTA
 
@@ -46,14 +41,36 @@ int attention_kch(int n_q) { return n_q == 1 ? 256 : 1024; }
 int attention_max_parts(int64_t L, int n_u, int n_q) {
     const int kch = attention_kch(n_q);
     const int grid_parts = (int)((L + n_u + kch - 1) / kch);
-    return n_q == 1 ? (grid_parts > MAX_PERSIST_CTAS ? grid_parts : MAX_PERSIST_CTAS) : grid_parts;
+    return n_q == 1 ? std::max(grid_parts, MAX_PERSIST_CTAS) : grid_parts;
 }
 
-template <typename T, int D> struct Ring {
-    static constexpr int ROWB = D * (int)sizeof(T);
-    static constexpr int STAGE_ELEMS = 2 * KS * D;  // K then V
-    static constexpr size_t BYTES = (size_t)NSTAGE * STAGE_ELEMS * sizeof(T);
-};
+template <typename T> struct Raw { uint4 v[sizeof(T) == 2 ? 1 : 2]; };
+__device__ __forceinline__ uint4 ld_nc_v4(const void *p) {
+    uint4 u;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                 : "l"(p));
+    return u;
+}
+template <typename T> __device__ __forceinline__ void ld_raw(Raw<T> &r, const T *p) {
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(r.v) / sizeof(uint4)); ++i)
+        r.v[i] = ld_nc_v4(reinterpret_cast<const uint4 *>(p) + i);
+}
+__device__ __forceinline__ void cvt(const Raw<__nv_bfloat16> &r, float (&f)[8]) {
+    const uint32_t w[4] = {r.v[0].x, r.v[0].y, r.v[0].z, r.v[0].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = __uint_as_float(w[i] << 16);
+        f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+}
+__device__ __forceinline__ void cvt(const Raw<float> &r, float (&f)[8]) {
+    f[0] = __uint_as_float(r.v[0].x); f[1] = __uint_as_float(r.v[0].y);
+    f[2] = __uint_as_float(r.v[0].z); f[3] = __uint_as_float(r.v[0].w);
+    f[4] = __uint_as_float(r.v[1].x); f[5] = __uint_as_float(r.v[1].y);
+    f[6] = __uint_as_float(r.v[1].z); f[7] = __uint_as_float(r.v[1].w);
+}
 
 // NV values per lane, reduced over aligned groups of G lanes; lane ends with
 // the group sum of value index (sub >> (log2 G - log2 NV)) & (NV - 1).
@@ -76,33 +93,17 @@ __device__ __forceinline__ float group_transpose_reduce(float (&v)[NV], int lane
     return v[0];
 }
 
-__device__ __forceinline__ void lds8(const __nv_bfloat16 *p, float (&f)[8]) {
-    const uint4 u = *reinterpret_cast<const uint4 *>(p);
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        f[2 * i] = __uint_as_float(w[i] << 16);
-        f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-    }
-}
-__device__ __forceinline__ void lds8(const float *p, float (&f)[8]) {
-    const float4 a = reinterpret_cast<const float4 *>(p)[0];
-    const float4 b = reinterpret_cast<const float4 *>(p)[1];
-    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
-    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-}
-
 // A row's key stream: nkf selected fixed keys, then nu visible user keys.
 struct RowInfo {
     int bh, h, nkf, nu;
     __device__ __forceinline__ int total() const { return nkf + nu; }
 };
-__device__ __forceinline__ RowInfo row_info(const AttnArgs &a, int row) {
+__device__ __forceinline__ RowInfo row_info(const AttnArgs &a, int row, int nkf = -1) {
     RowInfo r;
     r.bh = row / a.n_q;
     r.h = r.bh % a.H;
     const int t = row % a.n_q;
-    r.nkf = ldcg(a.n_keys + r.bh);
+    r.nkf = nkf >= 0 ? nkf : ldcg(a.n_keys + r.bh);
     int vis = a.causal ? t + a.n_u - a.n_q + 1 : a.n_u;
     r.nu = max(0, min(vis, a.n_u));
     return r;
@@ -114,38 +115,44 @@ struct Seg {
     int row, a0, a1, slot, nparts;
 };
 
-// Merge of one row's partials by the NCT consumer threads:
-// O = sum_p e^(lse_p - M) o_p / L, LSE = M + log L.
+// Merge of one row's partials by the CTA: O = sum_p e^(lse_p - M) o_p / L,
+// LSE = M + log L.
 template <int D>
 __device__ void merge_row(const AttnArgs &a, int row, int P, float *s_w, float *s_red) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float *lse = a.part_lse + (size_t)row * a.max_chunks;
-    float mx = -INFINITY;
-    for (int p = tid; p < P; p += NCT) mx = fmaxf(mx, ldcg(lse + p));
-    mx = warp_max(mx);
-    if (lane == 0) s_red[warp] = mx;
-    named_bar(1, NCT);
-    float M = -INFINITY;
-    for (int w = 0; w < NCW; ++w) M = fmaxf(M, s_red[w]);
-    named_bar(1, NCT);
     float acc = 0.f, lsum = 0.f;
+    float M = -INFINITY;
     for (int p0 = 0; p0 < P; p0 += NCT) {
+        // one tile of <= NCT partials: lse values once, block max, weights in
+        // smem, then the o rows with independent (unrolled) loads
         const int p = p0 + tid;
-        const float w = (p < P && M != -INFINITY) ? expf(ldcg(lse + p) - M) : 0.f;
+        const float lv = p < P ? ldcg(lse + p) : -INFINITY;
+        const float mx = warp_max(lv);
+        if (lane == 0) s_red[warp] = mx;
+        __syncthreads();
+        float Mt = -INFINITY;
+        for (int w = 0; w < NCW; ++w) Mt = fmaxf(Mt, s_red[w]);
+        const float Mn = fmaxf(M, Mt);
+        const float corr = (M == -INFINITY) ? 0.f : expf(M - Mn);  // rescale earlier tiles
+        acc *= corr;
+        lsum *= corr;
+        M = Mn;
+        const float w = (lv == -INFINITY) ? 0.f : expf(lv - M);
         s_w[tid] = w;
         lsum += w;
-        named_bar(1, NCT);
+        __syncthreads();
         const int np = min(NCT, P - p0);
         if (tid < D) {
             const float *op = a.part_o + ((size_t)row * a.max_chunks + p0) * D + tid;
-#pragma unroll 8
+#pragma unroll 16
             for (int j = 0; j < np; ++j) acc = fmaf(s_w[j], ldcg(op + (size_t)j * D), acc);
         }
-        named_bar(1, NCT);
+        __syncthreads();
     }
     lsum = warp_sum(lsum);
     if (lane == 0) s_red[warp] = lsum;
-    named_bar(1, NCT);
+    __syncthreads();
     float L = 0.f;
     for (int w = 0; w < NCW; ++w) L += s_red[w];
     if (tid < D) {
@@ -159,7 +166,7 @@ __device__ void merge_row(const AttnArgs &a, int row, int P, float *s_w, float *
         a.LSE[row] = (M == -INFINITY) ? -INFINITY : M + logf(L);
         if (M == -INFINITY && !a.partial) atomicOr(a.status, 1);
     }
-    named_bar(1, NCT);
+    __syncthreads();
 }
 
 // Rows with no key at all (no selected fixed key, no visible user key) get the
@@ -181,7 +188,7 @@ __device__ void empty_row(const AttnArgs &a, int row) {
 // Iterates the segments of this CTA.
 template <bool PERSIST> struct SegIter {
     const AttnArgs *a;
-    const int *pref;   // PERSIST: exclusive prefix of row stream lengths, [rows + 1]
+    const int *pref;  // PERSIST: exclusive prefix of row stream lengths, [rows + 1]
     int rows, r;
     long long ks, ke, K;
     int G;
@@ -239,43 +246,40 @@ template <bool PERSIST> struct SegIter {
 };
 
 template <typename T, int D, bool PERSIST>
-__global__ void __launch_bounds__(AT_NT) k_attend(AttnArgs a, int rows) {
-    using R = Ring<T, D>;
-    constexpr int G = D / 8;            // lanes per key row (8 elements each)
-    constexpr int KPW = 32 / G;         // key rows per warp instruction
-    constexpr int NS = KPWS / KPW;      // key slots per lane per stage
-    constexpr int LPS = G / NS;         // lanes holding each reduced key
+__global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
+    constexpr int G = D / 8;          // lanes per key row (8 elements each)
+    constexpr int KPW = 32 / G;       // key rows per warp instruction
+    constexpr int NS = KR / KPW;      // key slots per lane per round
+    constexpr int LPS = G / NS;       // lanes holding each reduced key
     constexpr int LG_G = G == 16 ? 4 : 3;
-    constexpr int LG_NS = NS == 4 ? 2 : NS == 2 ? 1 : 0;
+    constexpr int LG_NS = NS == 8 ? 3 : NS == 4 ? 2 : NS == 2 ? 1 : 0;
 
-    extern __shared__ __align__(128) unsigned char dyn[];
-    T *ring = reinterpret_cast<T *>(dyn);
-    uint64_t *full = reinterpret_cast<uint64_t *>(dyn + R::BYTES);
-    uint64_t *empty = full + NSTAGE;
-    int *s_pref = reinterpret_cast<int *>(empty + NSTAGE);
+    extern __shared__ __align__(16) int dyn_i[];
+    int *s_pref = dyn_i;             // [rows + 1] (persistent)
+    int *s_nkf = dyn_i + rows + 1;   // [rows]     (persistent)
     __shared__ float s_m[NCW], s_l[NCW], s_o[NCW * D], s_w[NCT], s_red[NCW];
     __shared__ int s_last;
-
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) {
-        for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NCW);
-        }
-        mbar_fence_init();
-    }
+
+    SQZ_TRACE_AT(g_trace_attn, 0);
     // the selection comes from the preceding lookup kernel (programmatic
-    // dependent launch: everything above this line overlaps its tail)
+    // dependent launch: the launch itself overlaps its tail)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    SQZ_TRACE_AT(g_trace_attn, 1);
 
     if (PERSIST) {
         // exclusive prefix of the row stream lengths (rows <= a few thousand)
-        __shared__ int s_ws[AT_NW];
+        __shared__ int s_ws[NCW];
         if (tid == 0) s_pref[0] = 0;
-        for (int base = 0; base < rows; base += AT_NT) {
+        for (int base = 0; base < rows; base += NCT) {
             __syncthreads();
             const int r = base + tid;
-            const int len = r < rows ? row_info(a, r).total() : 0;
+            int len = 0;
+            if (r < rows) {
+                const RowInfo ri = row_info(a, r);
+                len = ri.total();
+                s_nkf[r] = ri.nkf;
+            }
             int inc = len;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -297,68 +301,25 @@ __global__ void __launch_bounds__(AT_NT) k_attend(AttnArgs a, int rows) {
         if (blockIdx.y == 0 && row_info(a, blockIdx.x).total() == 0) empty_row<D>(a, blockIdx.x);
     }
     __syncthreads();
+    SQZ_TRACE_AT(g_trace_attn, 2);
 
     SegIter<PERSIST> it;
     it.init(a, s_pref, rows);
     Seg sg;
-
-    if (warp == NCW) {
-        // ================= producer warp: TMA bulk copies =================
-        const uint64_t pol = policy_evict_first();
-        int st = 0;
-        uint32_t ph = 0;
-        while (it.next(sg)) {
-            const RowInfo ri = row_info(a, sg.row);
-            const T *Kf = reinterpret_cast<const T *>(a.Kp) + (size_t)ri.h * a.L * D;
-            const T *Vf = reinterpret_cast<const T *>(a.Vp) + (size_t)ri.h * a.L * D;
-            const T *Ku = reinterpret_cast<const T *>(a.Ku) + (size_t)ri.bh * a.n_u * D;
-            const T *Vu = reinterpret_cast<const T *>(a.Vu) + (size_t)ri.bh * a.n_u * D;
-            const int32_t *kidx = a.key_idx + (size_t)ri.bh * a.L;
-            for (int g0 = sg.a0; g0 < sg.a1; g0 += 8 * KS) {
-                // stream positions of the next 8 stages: one load latency per 8 stages
-                int posr[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int k = g0 + u * KS + lane;
-                    posr[u] = k < sg.a1 ? (k < ri.nkf ? ldcg(kidx + k) : k - ri.nkf) : 0;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int j0 = g0 + u * KS;
-                    if (j0 >= sg.a1) break;
-                    mbar_wait(&empty[st], ph ^ 1);
-                    const int nk = min(KS, sg.a1 - j0);
-                    const int k = j0 + lane;
-                    const bool user = k >= ri.nkf;
-                    const int pos = posr[u];
-                    const int prev = __shfl_up_sync(FULL, pos, 1);
-                    const bool prev_user = __shfl_up_sync(FULL, (int)user, 1);
-                    const bool start = lane < nk && (lane == 0 || pos != prev + 1 || user != prev_user);
-                    const unsigned starts = __ballot_sync(FULL, start);
-                    if (lane == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * nk * R::ROWB));
-                    __syncwarp();
-                    if (start) {
-                        const unsigned later = starts & ~((2u << lane) - 1u);
-                        const int end = later ? __ffs(later) - 1 : nk;
-                        const uint32_t bytes = (uint32_t)((end - lane) * R::ROWB);
-                        T *sK = ring + (size_t)st * R::STAGE_ELEMS + (size_t)lane * D;
-                        T *sV = sK + KS * D;
-                        bulk_g2s(sK, (user ? Ku : Kf) + (size_t)pos * D, bytes, &full[st], pol);
-                        bulk_g2s(sV, (user ? Vu : Vf) + (size_t)pos * D, bytes, &full[st], pol);
-                    }
-                    if (++st == NSTAGE) { st = 0; ph ^= 1; }
-                }
-            }
-        }
-        return;
-    }
-
-    // ================= consumer warps =================
     const int g = lane / G, sub = lane % G;
     const int myslot = sub >> (LG_G - LG_NS);
-    int st = 0;
-    uint32_t ph = 0;
     while (it.next(sg)) {
+        const RowInfo ri = row_info(a, sg.row, PERSIST ? s_nkf[sg.row] : -1);
+        const T *Kf = reinterpret_cast<const T *>(a.Kp) + (size_t)ri.h * a.L * D;
+        const T *Vf = reinterpret_cast<const T *>(a.Vp) + (size_t)ri.h * a.L * D;
+        const T *Ku = reinterpret_cast<const T *>(a.Ku) + (size_t)ri.bh * a.n_u * D;
+        const T *Vu = reinterpret_cast<const T *>(a.Vu) + (size_t)ri.bh * a.n_u * D;
+        const int32_t *kidx = a.key_idx + (size_t)ri.bh * a.L;
+        // source position of stream key k: >= 0 fixed key row, < 0 user key -1-u
+        auto pos_of = [&](int k) -> int {
+            if (k >= sg.a1) return 0;
+            return k < ri.nkf ? ldcg(kidx + k) : -1 - (k - ri.nkf);
+        };
         float q[8];
         load8(reinterpret_cast<const T *>(a.Q) + (size_t)sg.row * D + sub * 8, q);
         const float sc = a.scale * LOG2E;
@@ -368,51 +329,62 @@ __global__ void __launch_bounds__(AT_NT) k_attend(AttnArgs a, int rows) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) o[k] = 0.f;
 
-        for (int j0 = sg.a0; j0 < sg.a1; j0 += KS) {
-            mbar_wait(&full[st], ph);
-            const int nk = min(KS, sg.a1 - j0);
-            const T *sK = ring + (size_t)st * R::STAGE_ELEMS;
-            const T *sV = sK + KS * D;
-            const int kb = warp * KPWS;  // this warp's keys in the stage
-            if (kb < nk) {
-                float v[NS];
+        // lane l (< KR) holds the position of key l of this warp's current round
+        int j0 = sg.a0 + warp * KR;
+        int pos_cur = pos_of(j0 + (lane & (KR - 1)));
+        for (; j0 < sg.a1; j0 += NCW * KR) {
+            const int nk = min(KR, sg.a1 - j0);
+            Raw<T> kr[NS], vr[NS];
 #pragma unroll
-                for (int s = 0; s < NS; ++s) {
-                    const int kk = kb + s * KPW + g;
-                    float f[8];
-                    lds8(sK + kk * D + sub * 8, f);
-                    float acc = 0.f;
+            for (int s = 0; s < NS; ++s) {
+                const int kk = s * KPW + g;
+                const int pos = __shfl_sync(FULL, pos_cur, kk);
+                if (kk < nk) {
+                    const T *kp = pos >= 0 ? Kf + (size_t)pos * D : Ku + (size_t)(-1 - pos) * D;
+                    const T *vp = pos >= 0 ? Vf + (size_t)pos * D : Vu + (size_t)(-1 - pos) * D;
+                    ld_raw(kr[s], kp + sub * 8);
+                    ld_raw(vr[s], vp + sub * 8);
+                } else {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) acc = fmaf(q[k], f[k], acc);
-                    v[s] = acc;
+                    for (int i = 0; i < (int)(sizeof(kr[s].v) / sizeof(uint4)); ++i)
+                        kr[s].v[i] = vr[s].v[i] = make_uint4(0, 0, 0, 0);
                 }
-                float z = group_transpose_reduce<NS, G>(v, lane);
-                if (kb + myslot * KPW + g >= nk) z = -INFINITY;
-                const float mx = warp_max(z);
-                const float m_new = fmaxf(m_run, mx);
-                const float alpha = fast_exp2(m_run - m_new);  // m_run = -inf -> 0
-                const float p = fast_exp2(z - m_new);          // z = -inf -> 0
-                l_lane = l_lane * alpha + p;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) o[k] *= alpha;
-#pragma unroll
-                for (int s = 0; s < NS; ++s) {
-                    const float ps = __shfl_sync(FULL, p, g * G + s * LPS);
-                    const int kk = kb + s * KPW + g;
-                    if (kk < nk) {
-                        float f[8];
-                        lds8(sV + kk * D + sub * 8, f);
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) o[k] = fmaf(ps, f[k], o[k]);
-                    }
-                }
-                m_run = m_new;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-            if (++st == NSTAGE) { st = 0; ph ^= 1; }
+            // prefetch the next round's positions while this round's rows are in flight
+            pos_cur = pos_of(j0 + NCW * KR + (lane & (KR - 1)));
+            float v[NS];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                float f[8];
+                cvt(kr[s], f);
+                float acc = 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc = fmaf(q[k], f[k], acc);
+                v[s] = acc;
+            }
+            float z = group_transpose_reduce<NS, G>(v, lane);
+            if (myslot * KPW + g >= nk) z = -INFINITY;
+            const float mx = warp_max(z);
+            const float m_new = fmaxf(m_run, mx);
+            const float alpha = fast_exp2(m_run - m_new);  // m_run = -inf -> 0
+            const float p = fast_exp2(z - m_new);          // z = -inf -> 0
+            l_lane = l_lane * alpha + p;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] *= alpha;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                const float ps = __shfl_sync(FULL, p, g * G + s * LPS);
+                if (s * KPW + g < nk) {
+                    float f[8];
+                    cvt(vr[s], f);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) o[k] = fmaf(ps, f[k], o[k]);
+                }
+            }
+            m_run = m_new;
         }
-        // ---- segment epilogue: fold key groups, then the consumer warps ----
+        SQZ_TRACE_AT(g_trace_attn, 4);
+        // ---- segment epilogue: fold key groups, then the warps ----
 #pragma unroll
         for (int s2 = G; s2 < 32; s2 <<= 1)
 #pragma unroll
@@ -423,7 +395,7 @@ __global__ void __launch_bounds__(AT_NT) k_attend(AttnArgs a, int rows) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) s_o[warp * D + sub * 8 + k] = o[k];
         }
-        named_bar(1, NCT);
+        __syncthreads();
         if (tid < D) {
             float M = -INFINITY;
             for (int w = 0; w < NCW; ++w) M = fmaxf(M, s_m[w]);
@@ -439,18 +411,19 @@ __global__ void __launch_bounds__(AT_NT) k_attend(AttnArgs a, int rows) {
         }
         // the CTA that completes a row's last segment merges its partials
         __threadfence();
-        named_bar(1, NCT);
+        __syncthreads();
         if (tid == 0) {
             const int t = atomicAdd(a.row_cnt + sg.row, 1);
             s_last = (t == sg.nparts - 1);
             if (s_last) a.row_cnt[sg.row] = 0;
         }
-        named_bar(1, NCT);
+        __syncthreads();
         if (s_last) {
             __threadfence();
             merge_row<D>(a, sg.row, sg.nparts, s_w, s_red);
         }
     }
+    SQZ_TRACE_AT(g_trace_attn, 5);
 }
 
 template <typename T, int D>
@@ -458,34 +431,42 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     const int rows = a.B * a.H * a.n_q;
     if (rows == 0) return cudaSuccess;
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(AT_NT);
+    cfg.blockDim = dim3(NCT);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    const size_t ring = Ring<T, D>::BYTES + 2 * NSTAGE * sizeof(uint64_t);
+    // Host-side launch cost matters at decode sizes (a few microseconds per
+    // runtime query): attributes are set once and the persistent grid size is
+    // cached per row count (one device per process).
     if (a.n_q == 1 && rows <= 8192) {
-        const size_t dsm = ring + (size_t)(rows + 1) * sizeof(int);
+        const size_t dsm = (size_t)(2 * rows + 1) * sizeof(int);
         auto kern = k_attend<T, D, true>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-        if (e != cudaSuccess) return e;
-        int dev = 0, nsm = 0, occ = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, AT_NT, dsm);
-        if (occ < 1) occ = 1;
-        cfg.gridDim = dim3(std::min(nsm * occ, MAX_PERSIST_CTAS));
+        static size_t attr_bytes = 48 * 1024;
+        static int cached_rows = -1, cached_grid = 0;
+        if (dsm > attr_bytes) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)dsm);
+            if (e != cudaSuccess) return e;
+            attr_bytes = dsm;
+        }
+        if (rows != cached_rows) {
+            int dev = 0, nsm = 0, occ = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NCT, dsm);
+            cached_grid = std::min(nsm * std::max(occ, 1), MAX_PERSIST_CTAS);
+            cached_rows = rows;
+        }
+        cfg.gridDim = dim3(cached_grid);
         cfg.dynamicSmemBytes = dsm;
         return cudaLaunchKernelEx(&cfg, kern, a, rows);
     }
-    auto kern = k_attend<T, D, false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring);
-    if (e != cudaSuccess) return e;
     cfg.gridDim = dim3(rows, a.max_chunks);
-    cfg.dynamicSmemBytes = ring;
-    return cudaLaunchKernelEx(&cfg, kern, a, rows);
+    cfg.dynamicSmemBytes = 0;
+    return cudaLaunchKernelEx(&cfg, k_attend<T, D, false>, a, rows);
 }
 
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st) {
@@ -533,3 +514,5 @@ cudaError_t launch_merge(int P, const float *O_parts, const float *LSE_parts, in
 }
 
 }  // namespace sqz
+
+SQZ_TRACE_EXPORT(sqz::g_trace_attn, sqz_trace_attn)

@@ -77,3 +77,25 @@ __device__ __forceinline__ float fast_exp2(float x) {
 template <typename T> __device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
 
 }  // namespace sqz
+
+// ---- optional device-side timeline tracing (experiments only: -DSQZ_TRACE) ----
+#ifdef SQZ_TRACE
+#define SQZ_TRACE_DECL(name) __device__ unsigned long long name[2048 * 8];
+#define SQZ_TRACE_AT(name, slot)                                                          \
+    do {                                                                                  \
+        const unsigned lin_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+        if (threadIdx.x == 0 && lin_ < 2048) {                                            \
+            unsigned long long t_;                                                        \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                       \
+            name[lin_ * 8 + (slot)] = t_;                                                 \
+        }                                                                                 \
+    } while (0)
+#define SQZ_TRACE_EXPORT(name, fn)                                                        \
+    extern "C" int fn(void *host, size_t bytes) {                                         \
+        return (int)cudaMemcpyFromSymbol(host, name, bytes < sizeof(name) ? bytes : sizeof(name)); \
+    }
+#else
+#define SQZ_TRACE_DECL(name)
+#define SQZ_TRACE_AT(name, slot) do { } while (0)
+#define SQZ_TRACE_EXPORT(name, fn)
+#endif

@@ -59,7 +59,8 @@ struct AttnArgs {
     float *part_o;    // [rows, max_chunks, d]
     float *part_lse;  // [rows, max_chunks]
     int32_t *status;  // [1]
-    int32_t *row_cnt; // [rows] self-cleaning chunk tickets
+    int32_t *row_cnt; // [rows] self-cleaning tile tickets
+    int32_t *sched;   // [2] dynamic tile counter + finished-CTA counter (self-cleaning)
     void *O;
     float *LSE;
 };

@@ -26,6 +26,8 @@
 
 namespace sqz {
 
+SQZ_TRACE_DECL(g_trace_look)
+
 constexpr int CH = 128;     // centroid rows per CTA
 constexpr int NT = 256;     // threads per CTA
 constexpr int NW = NT / 32;
@@ -197,6 +199,10 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
                                                       LevelArgs lv, int rpc) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
+    // let the dependent attention grid launch now: its CTAs become resident and
+    // park at griddepcontrol.wait until this grid has completed
+    asm volatile("griddepcontrol.launch_dependents;");
+    SQZ_TRACE_AT(g_trace_look, 0);
     const int rank = (int)cluster.block_rank();
     const int h = blockIdx.y, g = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -277,6 +283,7 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
         if (ROWLIST && lane < U && rr0 + lane < nloc) s_row[rr0 + lane] = ldcg(rows + r0 + rr0 + lane);
     }
     __syncthreads();
+    SQZ_TRACE_AT(g_trace_look, 1);
     // (m, D) of the CTA's rows per query: block max, then one exp per row.
     for (int i = 0; i < nb; ++i) {
         float mx = -INFINITY;
@@ -302,6 +309,7 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
         }
     }
     cluster.sync();
+    SQZ_TRACE_AT(g_trace_look, 2);
     // ---- global (m, D) per query, ranks folded in order ----
     if (tid < nb) {
         float mm = -INFINITY, dd = 0.f;
@@ -345,6 +353,7 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
         if (tid == 0) { sh.cnt[i] = run; sh.keys[i] = runk; }
     }
     cluster.sync();
+    SQZ_TRACE_AT(g_trace_look, 3);
     // ---- cluster-wide offsets, then write the lists and expand the ranges ----
     for (int i = 0; i < nb; ++i) {
         const int bh = (b0 + i) * H + h;
@@ -369,8 +378,12 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
             lv.n_exp[bh] = tk;
         }
     }
+    SQZ_TRACE_AT(g_trace_look, 4);
     cluster.sync();  // keep this CTA's smem alive until every rank has read it
+    SQZ_TRACE_AT(g_trace_look, 5);
 }
+
+SQZ_TRACE_EXPORT(g_trace_look, sqz_trace_look)
 
 static size_t decode_smem_bytes(int NB, int rpc) { return (size_t)rpc * 4 * (NB + 1 + 4 * NB) + 16; }
 
@@ -429,6 +442,7 @@ template <typename T, int D, bool ROWLIST>
 __global__ void __launch_bounds__(NT) k_prefill_colsum(LookupShape s, const T *__restrict__ Q,
                                                        LevelArgs lv) {
     const int chunk = blockIdx.x, tile = blockIdx.y, bh = blockIdx.z;
+    asm volatile("griddepcontrol.launch_dependents;");
     const int h = bh % s.H;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = lv.c;
@@ -529,6 +543,15 @@ static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelAr
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+#ifdef SQZ_CARVEOUT_MAX
+    {
+        static bool done = false;
+        if (!done) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            done = true;
+        }
+    }
+#endif
     return cudaLaunchKernelEx(&cfg, kern, s, Q, lv, rpc);
 }
 
