@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
     int *s_st = s_sel + NB * rpc;                                  // [NB][rpc]
     int *s_n = s_st + NB * rpc;                                    // [NB][rpc]
     int *s_kp = s_n + NB * rpc;                                    // [NB][rpc]
+    float *s_Nw = reinterpret_cast<float *>(s_kp + NB * rpc);      // [rpc] N of the row
+    int *s_o0 = reinterpret_cast<int *>(s_Nw + rpc);               // [rpc] off[row]
+    int *s_o1 = s_o0 + rpc;                                        // [rpc] off[row + 1]
     __shared__ DecodeSmem<NB> sh;
     __shared__ float s_M[NB], s_lD[NB];
     __shared__ float s_wm[NW][NB], s_wd[NW][NB];
@@ -249,14 +252,23 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
     constexpr int U = 16;
     constexpr int RPT = 16 / NB;  // rows per 16-value transpose
     for (int rr0 = warp * U; rr0 < nloc; rr0 += NW * U) {
+        // lane l < U owns row rr0 + l: its id and its N / key-range metadata are
+        // fetched now, in the same memory round trip as the centroid rows
+        const int myrr = rr0 + lane;
+        int myrow = -1;
+        if (lane < U && myrr < nloc) {
+            myrow = ROWLIST ? ldcg(rows + r0 + myrr) : r0 + myrr;
+            s_row[myrr] = myrow;
+            s_Nw[myrr] = (float)__ldg(N + myrow);
+            s_o0[myrr] = __ldg(off + myrow);
+            s_o1[myrr] = __ldg(off + myrow + 1);
+        }
         float cf[U][D / 32];
         int rowid[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int rr = rr0 + u;
-            rowid[u] = -1;
-            if (rr < nloc) {
-                rowid[u] = ROWLIST ? ldcg(rows + r0 + rr) : r0 + rr;
+            rowid[u] = __shfl_sync(FULL, myrow, u);
+            if (rowid[u] >= 0) {
                 Lane<T, D>::load(C + (size_t)rowid[u] * D, lane, cf[u]);
             } else {
 #pragma unroll
@@ -280,7 +292,6 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
             const int rr = rr0 + gq * RPT + vi / NB;
             if ((lane & 1) == 0 && rr < nloc) s_log[(vi % NB) * rpc + rr] = sv;
         }
-        if (ROWLIST && lane < U && rr0 + lane < nloc) s_row[rr0 + lane] = ldcg(rows + r0 + rr0 + lane);
     }
     __syncthreads();
     SQZ_TRACE_AT(g_trace_look, 1);
@@ -295,10 +306,7 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
         for (int w = 0; w < NW; ++w) M = fmaxf(M, s_wm[w][i]);
         float e = 0.f;
         if (M != -INFINITY)
-            for (int rr = tid; rr < nloc; rr += NT) {
-                const int row = ROWLIST ? s_row[rr] : r0 + rr;
-                e += (float)__ldg(N + row) * expf(s_log[i * rpc + rr] - M);
-            }
+            for (int rr = tid; rr < nloc; rr += NT) e += s_Nw[rr] * expf(s_log[i * rpc + rr] - M);
         e = warp_sum(e);
         if (lane == 0) s_wd[warp][i] = e;
         __syncthreads();
@@ -310,16 +318,28 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
     }
     cluster.sync();
     SQZ_TRACE_AT(g_trace_look, 2);
-    // ---- global (m, D) per query, ranks folded in order ----
-    if (tid < nb) {
+    // ---- global (m, D) per query: warp i reads the NC ranks' partials in
+    // parallel (one DSMEM load per lane) and folds them with a butterfly, so
+    // every CTA of the cluster computes bit-identical values ----
+    if (warp < nb) {
+        const int i = warp;
         float mm = -INFINITY, dd = 0.f;
-        for (int r = 0; r < NC; ++r) {
-            const DecodeSmem<NB> *o = cluster.map_shared_rank(&sh, r);
-            md_combine(mm, dd, o->md[tid].x, o->md[tid].y);
+        if (lane < NC) {
+            const DecodeSmem<NB> *o = cluster.map_shared_rank(&sh, lane);
+            const float2 v = o->md[i];
+            mm = v.x;
+            dd = v.y;
         }
-        s_M[tid] = mm;
-        s_lD[tid] = logf(dd);
-        if (rank == 0 && lv.dbg_lse) lv.dbg_lse[(size_t)(b0 + tid) * H + h] = mm + logf(dd);
+#pragma unroll
+        for (int o = 1; o < NC; o <<= 1) {
+            const float m2 = __shfl_xor_sync(FULL, mm, o), d2 = __shfl_xor_sync(FULL, dd, o);
+            md_combine(mm, dd, m2, d2);
+        }
+        if (lane == 0) {
+            s_M[i] = mm;
+            s_lD[i] = logf(dd);
+            if (rank == 0 && lv.dbg_lse) lv.dbg_lse[(size_t)(b0 + i) * H + h] = mm + logf(dd);
+        }
     }
     __syncthreads();
     // ---- threshold + ordered compaction of the CTA's rows ----
@@ -338,7 +358,7 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
             if (valid && lv.dbg_S) lv.dbg_S[(size_t)bh * c + row] = expf(x - lD);
             if (valid && lv.bitmap) lv.bitmap[(size_t)bh * c + row] = sel ? 1 : 0;
             int st = 0, n = 0;
-            if (sel) { st = __ldg(off + row); n = __ldg(off + row + 1) - st; }
+            if (sel) { st = s_o0[rr]; n = s_o1[rr] - st; }
             int pos, kpre, tc, tk;
             tile_scan(sel, n, pos, kpre, tc, tk);
             if (sel) {
@@ -355,16 +375,37 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
     cluster.sync();
     SQZ_TRACE_AT(g_trace_look, 3);
     // ---- cluster-wide offsets, then write the lists and expand the ranges ----
+    __shared__ int s_oc[NB], s_ok[NB];
+    if (warp < nb) {  // warp i: lane r reads rank r's counts, prefix by shuffles
+        const int i = warp;
+        int cr = 0, kr = 0;
+        if (lane < NC) {
+            const DecodeSmem<NB> *o = cluster.map_shared_rank(&sh, lane);
+            cr = o->cnt[i];
+            kr = o->keys[i];
+        }
+        int ic = cr, ik = kr;
+#pragma unroll
+        for (int o = 1; o < NC; o <<= 1) {
+            const int tc_ = __shfl_up_sync(FULL, ic, o), tk_ = __shfl_up_sync(FULL, ik, o);
+            if (lane >= o) { ic += tc_; ik += tk_; }
+        }
+        const int exc = __shfl_sync(FULL, ic - cr, rank), exk = __shfl_sync(FULL, ik - kr, rank);
+        const int totc = __shfl_sync(FULL, ic, NC - 1), totk = __shfl_sync(FULL, ik, NC - 1);
+        if (lane == 0) {
+            s_oc[i] = exc;
+            s_ok[i] = exk;
+            if (rank == 0) {
+                const int bh = (b0 + i) * H + h;
+                lv.n_list[bh] = totc;
+                lv.n_exp[bh] = totk;
+            }
+        }
+    }
+    __syncthreads();
     for (int i = 0; i < nb; ++i) {
         const int bh = (b0 + i) * H + h;
-        int oc = 0, ok = 0, tc = 0, tk = 0;
-        for (int r = 0; r < NC; ++r) {
-            const DecodeSmem<NB> *o = cluster.map_shared_rank(&sh, r);
-            const int cr = o->cnt[i], kr = o->keys[i];
-            if (r < rank) { oc += cr; ok += kr; }
-            tc += cr;
-            tk += kr;
-        }
+        const int oc = s_oc[i], ok = s_ok[i];
         const int mine = sh.cnt[i];
         int32_t *list = lv.list + (size_t)bh * c + oc;
         int32_t *exp_list = lv.exp_list + (size_t)bh * lv.exp_stride + ok;
@@ -372,10 +413,6 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
         for (int j = warp; j < mine; j += NW) {
             const int st = s_st[i * rpc + j], n = s_n[i * rpc + j], kp = s_kp[i * rpc + j];
             for (int t = lane; t < n; t += 32) exp_list[kp + t] = st + t;
-        }
-        if (rank == 0 && tid == 0) {
-            lv.n_list[bh] = tc;
-            lv.n_exp[bh] = tk;
         }
     }
     SQZ_TRACE_AT(g_trace_look, 4);
@@ -385,7 +422,7 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
 
 SQZ_TRACE_EXPORT(g_trace_look, sqz_trace_look)
 
-static size_t decode_smem_bytes(int NB, int rpc) { return (size_t)rpc * 4 * (NB + 1 + 4 * NB) + 16; }
+static size_t decode_smem_bytes(int NB, int rpc) { return (size_t)rpc * 4 * (NB + 4 + 4 * NB) + 16; }
 
 // --------------------------------------------------------------------------
 // Prefill pass 1: LSE_t over the row space for every query row.
