@@ -430,7 +430,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 4),
                 "traffic": traffic_for(args.config, "sparse_attention"),
-                "kernel": "k_attend_persistent (split-KV chunks + fused last-chunk merge)",
+                "kernel": "k_attend (persistent split-KV over equal key ranges + fused merge)",
                 "peak_kind": f"{peak_kind} copy bandwidth",
                 "bytes_per_launch": int(bytes_attn)}
         step_bytes = bytes_lookup + bytes_attn
