@@ -470,6 +470,9 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
 }
 
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st) {
+    // bf16 prefill runs on the tensor cores (prefill_attn.cu); fp32 inputs stay
+    // on exact fp32 FFMA (tf32 tensor cores would break the fp32 tolerance)
+    if (a.n_q > 1 && a.dtype == SQZ_BF16) return launch_prefill_attention(a, st);
     if (a.dtype == SQZ_BF16) {
         if (a.d == 128) return launch_t<__nv_bfloat16, 128>(a, st);
         return launch_t<__nv_bfloat16, 64>(a, st);

@@ -65,6 +65,9 @@ struct AttnArgs {
     float *LSE;
 };
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st);
+// prefill_attn.cu: tcgen05 path for bf16 prefill (n_q > 1)
+cudaError_t launch_prefill_attention(const AttnArgs &a, cudaStream_t st);
+int prefill_split_keys();
 int attention_kch(int n_q);
 int attention_max_parts(int64_t L, int n_u, int n_q);
 cudaError_t launch_merge(int P, const float *O_parts, const float *LSE_parts, int64_t rows, int d,

@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "tcgen05.cuh"
 
 namespace sqz {
 
@@ -118,8 +119,8 @@ __device__ __forceinline__ void tile_scan(bool sel, int n, int &pos, int &kpre, 
     if (lane == 31) { s_wc[warp] = __popc(bal); s_wk[warp] = inc; }
     __syncthreads();
     int wb = 0, kb = 0, tc = 0, tk = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
+    const int nw = blockDim.x >> 5;  // 4 or 8 warps
+    for (int w = 0; w < nw; ++w) {
         if (w < warp) { wb += s_wc[w]; kb += s_wk[w]; }
         tc += s_wc[w];
         tk += s_wk[w];
@@ -141,11 +142,12 @@ __device__ void finalize_rows(const LevelArgs &lv, int bh, int h, int nrows, Sel
     int32_t *list = lv.list + (size_t)bh * lv.c;
     int32_t *exp_list = lv.exp_list + (size_t)bh * lv.exp_stride;
     const int32_t *rows = ROWLIST ? lv.rows + (size_t)bh * lv.row_stride : nullptr;
+    const int nt = blockDim.x, nwp = nt >> 5;  // works for 128- and 256-thread CTAs
     if (lv.dbg_S && ROWLIST)
-        for (int r = tid; r < lv.c; r += NT) lv.dbg_S[(size_t)bh * lv.c + r] = NAN;
+        for (int r = tid; r < lv.c; r += nt) lv.dbg_S[(size_t)bh * lv.c + r] = NAN;
     __syncthreads();
     int run = 0, runk = 0;
-    for (int base = 0; base < nrows; base += NT) {
+    for (int base = 0; base < nrows; base += nt) {
         const int r = base + tid;
         const bool valid = r < nrows;
         const int row = valid ? (ROWLIST ? ldcg(rows + r) : r) : 0;
@@ -164,7 +166,7 @@ __device__ void finalize_rows(const LevelArgs &lv, int bh, int h, int nrows, Sel
             s_kp[pos] = runk + kpre;
         }
         __syncthreads();
-        for (int j = warp; j < tc; j += NW) {
+        for (int j = warp; j < tc; j += nwp) {
             const int st_j = s_st[j], n_j = s_n[j], kp_j = s_kp[j];
             for (int t = lane; t < n_j; t += 32) exp_list[kp_j + t] = st_j + t;
         }
@@ -592,9 +594,244 @@ static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelAr
     return cudaLaunchKernelEx(&cfg, kern, s, Q, lv, rpc);
 }
 
+// --------------------------------------------------------------------------
+// Prefill lookup on the 5th-generation tensor cores (bf16): one CTA per
+// (128-query tile, b*h).  The centroid rows of the (candidate) row space are
+// streamed in 128-row tiles (cp.async gather into the 128B-swizzled operand
+// layout, double-buffered); S = Q C^T is one 128x128x(d) tcgen05.mma chain per
+// tile into TMEM (two S buffers, so the next tile's MMA overlaps this tile's
+// epilogue).  Pass 1 (tiles 0..n-1): thread = query row keeps the online
+// (m, D = sum N e^(s-m)) -> LSE_t.  Pass 2 (recomputes S, as the
+// paper's kernel does): p = e^(s - LSE_t), column sums over the tile's
+// 128 rows by a transposed butterfly (31 shuffles per 32 columns) and a
+// fixed-order sum over the 4 warps -- deterministic fp32, no float atomics.
+// The last CTA of each (b,h) averages the tiles and thresholds S-bar > T.
+// --------------------------------------------------------------------------
+constexpr int PL_T = 128;  // query rows per CTA = centroid rows per tile
+
+template <int D> struct PlSmem {
+    static constexpr int TILE = PL_T * D * 2;
+    static constexpr int Q = 0;
+    static constexpr int C0 = Q + TILE;           // 2 buffers
+    static constexpr int NW = C0 + 2 * TILE;      // float [2][128] N weights
+    static constexpr int RID = NW + 2 * PL_T * 4; // int [2][128] row ids
+    static constexpr int COLS = RID + 2 * PL_T * 4;  // float [4][128] warp column sums
+    static constexpr int MISC = COLS + 4 * PL_T * 4;
+    static constexpr int BYTES = MISC + 64 + 1024;
+};
+
+template <int D, bool ROWLIST>
+__global__ void __launch_bounds__(PL_T, 1) k_prefill_lookup_tc(LookupShape s,
+                                                                const __nv_bfloat16 *__restrict__ Q,
+                                                                LevelArgs lv) {
+    using SM = PlSmem<D>;
+    constexpr int CPR = D * 2 / 16;
+    constexpr int HB = PL_T * 128;
+    constexpr uint32_t IDESC = idesc_bf16(128, PL_T, false);
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const uint32_t sbase = smem_u32(sm);
+    float *s_nw = reinterpret_cast<float *>(sm + SM::NW);
+    int *s_rid = reinterpret_cast<int *>(sm + SM::RID);
+    float *s_cols = reinterpret_cast<float *>(sm + SM::COLS);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + SM::MISC);
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sm + SM::MISC + 16);
+    __shared__ int s_last;
+
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int qt = blockIdx.x, bh = blockIdx.y, h = bh % s.H;
+    const int t0 = qt * PL_T, c = lv.c;
+    const __nv_bfloat16 *C = reinterpret_cast<const __nv_bfloat16 *>(lv.C) + (size_t)h * c * D;
+    const int32_t *N = lv.N + (size_t)h * c;
+    const int nrows = ROWLIST ? ldcg(lv.n_rows + bh) : c;
+    const int32_t *rows = ROWLIST ? lv.rows + (size_t)bh * lv.row_stride : nullptr;
+    const int ntile = (nrows + PL_T - 1) / PL_T;
+
+    if (warp == 0) tmem_alloc(s_tmem, 256);
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        mbar_fence_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *s_tmem;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+
+    // Q tile (rows beyond n_q are zero)
+    const __nv_bfloat16 *Qb = Q + ((size_t)bh * s.n_q + t0) * D;
+    for (int e = tid; e < PL_T * CPR; e += PL_T) {
+        const int r = e / CPR, cc = e % CPR;
+        const bool valid = t0 + r < s.n_q;
+        cp_async16_zfill(sbase + SM::Q + (cc >> 3) * HB + sw128_off(r, cc & 7),
+                         Qb + (size_t)(valid ? r : 0) * D + cc * 8, valid);
+    }
+    // the row id / N weight of column `tid` of tile `tl`
+    auto col_meta = [&](int tl, int &rid, float &nw) {
+        const int j = tl * PL_T + tid;
+        rid = -1;
+        nw = 0.f;
+        if (j < nrows) {
+            rid = ROWLIST ? ldcg(rows + j) : j;
+            nw = (float)__ldg(N + rid);
+        }
+    };
+    auto issue_tile = [&](int buf) {
+        for (int e = tid; e < PL_T * CPR; e += PL_T) {
+            const int r = e / CPR, cc = e % CPR;
+            const int rid = s_rid[buf * PL_T + r];
+            cp_async16_zfill(sbase + SM::C0 + buf * SM::TILE + (cc >> 3) * HB + sw128_off(r, cc & 7),
+                             C + (size_t)(rid >= 0 ? rid : 0) * D + cc * 8, rid >= 0);
+        }
+    };
+    const int total = 2 * ntile;  // pass 1 then pass 2 over the same tiles
+    {
+        int rid;
+        float nw;
+        col_meta(0, rid, nw);
+        s_rid[tid] = rid;
+        s_nw[tid] = nw;
+    }
+    __syncthreads();
+    if (total > 0) issue_tile(0);
+    cp_async_commit_grp();
+
+    const bool row_ok = t0 + tid < s.n_q;
+    float m = -INFINITY, Dsum = 0.f, lse = INFINITY;
+    for (int it = 0; it < total; ++it) {
+        const int buf = it & 1, tl = it % ntile, pass = it / ntile;
+        int rid_n = -1;
+        float nw_n = 0.f;
+        if (it + 1 < total) col_meta((it + 1) % ntile, rid_n, nw_n);
+        cp_async_wait_all();
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+                const uint32_t off = (ks >> 2) * HB + (ks & 3) * 32;
+                umma_bf16(tmem + buf * 128, sdesc_sw128(sbase + SM::Q + off, 16, 1024),
+                          sdesc_sw128(sbase + SM::C0 + buf * SM::TILE + off, 16, 1024), IDESC, ks > 0);
+            }
+            umma_commit(&mbar[buf]);
+        }
+        // next tile into the other buffer (its MMA, it - 1, completed before the last epilogue)
+        if (it + 1 < total) {
+            s_rid[(buf ^ 1) * PL_T + tid] = rid_n;
+            s_nw[(buf ^ 1) * PL_T + tid] = nw_n;
+        }
+        __syncthreads();
+        if (it + 1 < total) issue_tile(buf ^ 1);
+        cp_async_commit_grp();
+
+        mbar_wait(&mbar[buf], (it >> 1) & 1);
+        tc_fence_after();
+        const float *nwb = s_nw + buf * PL_T;
+#pragma unroll 1
+        for (int ch = 0; ch < PL_T / 32; ++ch) {
+            float v[32];
+            tmem_ld32(tmem + buf * 128 + lane_off + ch * 32, v);
+            tmem_wait_ld();
+            if (pass == 0) {
+                float cmx = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const bool valid = tl * PL_T + ch * 32 + j < nrows;
+                    v[j] = valid ? v[j] * s.scale : -INFINITY;
+                    cmx = fmaxf(cmx, v[j]);
+                }
+                const float mn = fmaxf(m, cmx);
+                if (mn != -INFINITY) {
+                    float acc = Dsum * expf(m - mn);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc = fmaf(nwb[ch * 32 + j], expf(v[j] - mn), acc);
+                    Dsum = acc;
+                    m = mn;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const bool valid = row_ok && tl * PL_T + ch * 32 + j < nrows;
+                    v[j] = valid ? expf(v[j] * s.scale - lse) : 0.f;
+                }
+                const float colsum = transpose_reduce<32>(v, lane);  // lane = column
+                s_cols[warp * PL_T + ch * 32 + lane] = colsum;
+            }
+        }
+        if (pass == 0 && tl == ntile - 1) {  // LSE_t of this thread's query row
+            lse = row_ok ? m + logf(Dsum) : INFINITY;
+            if (row_ok) {
+                lv.rowlse[(size_t)bh * s.n_q + t0 + tid] = lse;
+                if (lv.dbg_lse) lv.dbg_lse[(size_t)bh * s.n_q + t0 + tid] = lse;
+            }
+            if (!(lse < INFINITY) || lse == -INFINITY) lse = INFINITY;  // no row: p = 0
+        }
+        if (pass == 1) {
+            __syncthreads();
+            const int rid = s_rid[buf * PL_T + tid];
+            if (rid >= 0) {
+                const float acc = s_cols[tid] + s_cols[PL_T + tid] + s_cols[2 * PL_T + tid] +
+                                  s_cols[3 * PL_T + tid];
+                lv.colpart[((size_t)qt * s.B * s.H + bh) * c + rid] = acc;
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 256);
+    // ---- the last CTA of this (b,h) averages the tiles and thresholds ----
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+        const int t = atomicAdd(lv.tick + bh, 1);
+        s_last = (t == (int)gridDim.x - 1);
+        if (s_last) lv.tick[bh] = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int nqt = gridDim.x;
+    const bool all = !(lv.T > 0.f);
+    const float inv_nq = 1.0f / (float)s.n_q;
+    finalize_rows<ROWLIST>(lv, bh, h, nrows, [&](int row, float &dbg) {
+        float acc = 0.f;
+        for (int t = 0; t < nqt; ++t) acc += ldcg(lv.colpart + ((size_t)t * s.B * s.H + bh) * c + row);
+        const float Sbar = acc * inv_nq;
+        dbg = Sbar;
+        return all || (Sbar > lv.T);
+    });
+}
+
+template <int D, bool RL>
+static cudaError_t launch_prefill_tc(const LookupShape &s, const __nv_bfloat16 *Q, const LevelArgs &lv,
+                                     cudaStream_t st) {
+    auto kern = k_prefill_lookup_tc<D, RL>;
+    static bool set = false;
+    if (!set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             PlSmem<D>::BYTES);
+        if (e != cudaSuccess) return e;
+        set = true;
+    }
+    dim3 grid((s.n_q + PL_T - 1) / PL_T, s.B * s.H);
+    kern<<<grid, PL_T, PlSmem<D>::BYTES, st>>>(s, Q, lv);
+    return cudaGetLastError();
+}
+
 template <typename T, int D>
 static cudaError_t launch_level_t(const LookupShape &s, const T *Q, const LevelArgs &lv,
                                   cudaStream_t st) {
+    if constexpr (sizeof(T) == 2) {
+        // bf16 prefill: tensor-core lookup (fp32 inputs keep the exact FFMA path)
+        if (s.n_q > 1) {
+            if (lv.rows) return launch_prefill_tc<D, true>(s, Q, lv, st);
+            return launch_prefill_tc<D, false>(s, Q, lv, st);
+        }
+    }
     const bool rl = lv.rows != nullptr;
     const int rowspace = rl ? lv.row_stride : lv.c;
     const int nch = (rowspace + CH - 1) / CH;
