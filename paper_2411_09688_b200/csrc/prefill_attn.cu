@@ -171,19 +171,33 @@ __global__ void __launch_bounds__(PF_NT, 1) k_prefill_attend(AttnArgs a, int qti
         // ---- softmax on this thread's row ----
         mbar_wait(&mbar[0], it & 1);
         tc_fence_after();
-        float v[32];
-        float mx = -INFINITY;
+        // the row's 128 logits stay in registers for both passes
+        float sv[PF_KT];
 #pragma unroll
-        for (int c = 0; c < PF_KT / 32; ++c) {
-            tmem_ld32(tS + lane_off + c * 32, v);
-            tmem_wait_ld();
+        for (int c = 0; c < PF_KT / 32; ++c)
+            tmem_ld32(tS + lane_off + c * 32, *reinterpret_cast<float(*)[32]>(sv + c * 32));
+        tmem_wait_ld();
+        // masks only where needed: ragged rows, the stream tail, the causal diagonal
+        const bool full = row_ok && k0 + PF_KT <= k_end &&
+                          (k0 + PF_KT <= nkf || k0 + PF_KT - 1 - nkf <= ulim);
+        if (!full) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const int k = k0 + c * 32 + j;
+            for (int j = 0; j < PF_KT; ++j) {
+                const int k = k0 + j;
                 const bool vis = row_ok && k < k_end && (k < nkf || k - nkf <= ulim);
-                mx = fmaxf(mx, vis ? v[j] * sl2 : -INFINITY);
+                if (!vis) sv[j] = -INFINITY;
             }
         }
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int j = 0; j < PF_KT; j += 4) {
+            mx4[0] = fmaxf(mx4[0], sv[j]);
+            mx4[1] = fmaxf(mx4[1], sv[j + 1]);
+            mx4[2] = fmaxf(mx4[2], sv[j + 2]);
+            mx4[3] = fmaxf(mx4[3], sv[j + 3]);
+        }
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
+        float v[32];
         // lazy rescale: only when a row's max grew by more than 2^8 (FA4); the
         // TMEM accesses are warp-collective, so the warp rescales together
         const bool need = mx > m_used + 8.f;
@@ -201,31 +215,26 @@ __global__ void __launch_bounds__(PF_NT, 1) k_prefill_attend(AttnArgs a, int qti
         }
         l *= alpha;
         if (need) m_used = mx;
+        // p = 2^(s*scale*log2e - m) (ex2.approx), bf16, into the swizzled P tile
+        const float moff = (m_used == -INFINITY) ? 0.f : m_used;  // masked row: all p = 0
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int c = 0; c < PF_KT / 32; ++c) {
-            tmem_ld32(tS + lane_off + c * 32, v);
-            tmem_wait_ld();
-            uint32_t pk[16];
+        for (int ch = 0; ch < PF_KT / 8; ++ch) {  // 16 chunks of 8 keys
+            uint32_t pk[4];
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-                const int k = k0 + c * 32 + j;
-                const bool v0 = row_ok && k < k_end && (k < nkf || k - nkf <= ulim);
-                const bool v1 = row_ok && k + 1 < k_end && (k + 1 < nkf || k + 1 - nkf <= ulim);
-                const float p0 = v0 ? fast_exp2(v[j] * sl2 - m_used) : 0.f;
-                const float p1 = v1 ? fast_exp2(v[j + 1] * sl2 - m_used) : 0.f;
-                l += p0 + p1;
+            for (int q = 0; q < 4; ++q) {
+                const float p0 = fast_exp2(fmaf(sv[ch * 8 + 2 * q], sl2, -moff));
+                const float p1 = fast_exp2(fmaf(sv[ch * 8 + 2 * q + 1], sl2, -moff));
+                ls[q] += p0 + p1;
                 const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-                pk[j >> 1] = *reinterpret_cast<const uint32_t *>(&b2);
+                pk[q] = *reinterpret_cast<const uint32_t *>(&b2);
             }
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {  // 4 chunks of 8 keys
-                const int ch = c * 4 + q4;    // chunk index 0..15 across the 128 keys
-                const uint32_t addr = sbase + S::P + (ch >> 3) * HB + sw128_off(tid, ch & 7);
-                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(pk[q4 * 4]),
-                             "r"(pk[q4 * 4 + 1]), "r"(pk[q4 * 4 + 2]), "r"(pk[q4 * 4 + 3])
-                             : "memory");
-            }
+            const uint32_t addr = sbase + S::P + (ch >> 3) * HB + sw128_off(tid, ch & 7);
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(pk[0]), "r"(pk[1]),
+                         "r"(pk[2]), "r"(pk[3])
+                         : "memory");
         }
+        l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
