@@ -23,6 +23,21 @@
 
 namespace sqz {
 
+#ifdef SQZ_TRACE
+__device__ unsigned long long g_trace_pf[64 * 8];
+#define PF_TRACE(it, slot)                                                                   \
+    do {                                                                                      \
+        if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&      \
+            (it) < 64) {                                                                      \
+            unsigned long long t_;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            g_trace_pf[(it) * 8 + (slot)] = t_;                                               \
+        }                                                                                     \
+    } while (0)
+#else
+#define PF_TRACE(it, slot) do { } while (0)
+#endif
+
 constexpr int PF_NT = 128;         // threads: 4 warps, thread = query row
 constexpr int PF_QT = 128;         // query rows per CTA
 constexpr int PF_KT = 128;         // keys per tile
@@ -145,11 +160,13 @@ __global__ void __launch_bounds__(PF_NT, 1) k_prefill_attend(AttnArgs a, int qti
         const int buf = it & 1;
         const int k0 = k_begin + it * PF_KT;
         const int k0n = k0 + PF_KT;
+        PF_TRACE(it, 0);
         const int pos_next = (it + 1 < ntile && k0n + tid < k_end) ? pos_of(k0n + tid) : 0;
         cp_async_wait_all();  // tile `it` (and Q) are in shared memory
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
+        PF_TRACE(it, 1);
         if (tid == 0) {  // S = Q K^T
             tc_fence_after();
 #pragma unroll
@@ -170,6 +187,7 @@ __global__ void __launch_bounds__(PF_NT, 1) k_prefill_attend(AttnArgs a, int qti
 
         // ---- softmax on this thread's row ----
         mbar_wait(&mbar[0], it & 1);
+        PF_TRACE(it, 2);
         tc_fence_after();
         // the row's 128 logits stay in registers for both passes
         float sv[PF_KT];
@@ -235,6 +253,7 @@ __global__ void __launch_bounds__(PF_NT, 1) k_prefill_attend(AttnArgs a, int qti
                          : "memory");
         }
         l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        PF_TRACE(it, 3);
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
@@ -247,6 +266,7 @@ __global__ void __launch_bounds__(PF_NT, 1) k_prefill_attend(AttnArgs a, int qti
                           (it > 0 || ks > 0) ? 1u : 0u);
             }
             umma_commit(&mbar[1]);
+            PF_TRACE(it, 4);
         }
     }
     // ---- split partial: O / l and lse for every row of the tile ----
@@ -352,3 +372,9 @@ cudaError_t launch_prefill_attention(const AttnArgs &a, cudaStream_t st) {
 }
 
 }  // namespace sqz
+
+#ifdef SQZ_TRACE
+extern "C" int sqz_trace_pf(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, sqz::g_trace_pf, bytes < sizeof(sqz::g_trace_pf) ? bytes : sizeof(sqz::g_trace_pf));
+}
+#endif
