@@ -67,6 +67,7 @@ struct AttnArgs {
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st);
 // prefill_attn.cu: tcgen05 path for bf16 prefill (n_q > 1)
 cudaError_t launch_prefill_attention(const AttnArgs &a, cudaStream_t st);
+cudaError_t launch_prefill_attention_ws(const AttnArgs &a, cudaStream_t st);  // d = 128
 int prefill_split_keys();
 int attention_kch(int n_q);
 int attention_max_parts(int64_t L, int n_u, int n_q);

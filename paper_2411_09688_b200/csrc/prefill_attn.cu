@@ -348,6 +348,8 @@ cudaError_t launch_prefill_attention(const AttnArgs &a, cudaStream_t st) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     if (a.d == 128) {
+        static const bool legacy = getenv("SQZ_PF_LEGACY") != nullptr;  // A/B switch
+        if (!legacy) return launch_prefill_attention_ws(a, st);
         static bool set = false;
         if (!set) {
             cudaError_t e = cudaFuncSetAttribute(k_prefill_attend<128>,
