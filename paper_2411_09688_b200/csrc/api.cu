@@ -122,8 +122,13 @@ AttnWs attn_carve(const sqz_index *idx, int B, int n_q, int n_u, char *base) {
     const size_t rows = (size_t)B * idx->H * n_q;
     w.status = cv.take<int32_t>(64);
     w.row_cnt = cv.take<int32_t>(rows);
-    w.part_lse = cv.take<float>(rows * w.max_chunks);
-    w.part_o = cv.take<float>(rows * w.max_chunks * idx->d);
+    // partial rows: [rows, max_chunks] for the split-KV kernels, one 256-row slot
+    // per piece for the persistent prefill kernel
+    const size_t prow = prefill_ws_applies(idx->d, idx->dtype, n_q)
+                            ? std::max(rows * w.max_chunks, prefill_ws_part_rows(B, idx->H, n_q))
+                            : rows * w.max_chunks;
+    w.part_lse = cv.take<float>(prow);
+    w.part_o = cv.take<float>(prow * idx->d);
     w.bytes = cv.used + 256;
     return w;
 }

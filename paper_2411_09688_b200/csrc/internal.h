@@ -68,6 +68,8 @@ cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st);
 // prefill_attn.cu: tcgen05 path for bf16 prefill (n_q > 1)
 cudaError_t launch_prefill_attention(const AttnArgs &a, cudaStream_t st);
 cudaError_t launch_prefill_attention_ws(const AttnArgs &a, cudaStream_t st);  // d = 128
+bool prefill_ws_applies(int d, int dtype, int n_q);       // routes to the persistent kernel
+size_t prefill_ws_part_rows(int B, int H, int n_q);       // its partial-buffer rows
 int prefill_split_keys();
 int attention_kch(int n_q);
 int attention_max_parts(int64_t L, int n_u, int n_q);

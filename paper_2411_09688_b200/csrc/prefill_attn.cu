@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(PF_NT, 1) k_prefill_attend(AttnArgs a, int qti
     const float sl2 = a.scale * LOG2E;
     const int trow = t0 + tid;                   // query index of this thread's row
     const bool row_ok = trow < a.n_q;
-    const int ulim = trow + a.n_u - a.n_q;       // causal: user key u visible iff u <= ulim
+    const int ulim = a.causal ? trow + a.n_u - a.n_q : a.n_u;  // user key u visible iff u <= ulim
     float m_used = -INFINITY, l = 0.f;
 
     for (int it = 0; it < ntile; ++it) {
@@ -348,8 +348,7 @@ cudaError_t launch_prefill_attention(const AttnArgs &a, cudaStream_t st) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     if (a.d == 128) {
-        static const bool legacy = getenv("SQZ_PF_LEGACY") != nullptr;  // A/B switch
-        if (!legacy) return launch_prefill_attention_ws(a, st);
+        if (prefill_ws_applies(a.d, a.dtype, a.n_q)) return launch_prefill_attention_ws(a, st);
         static bool set = false;
         if (!set) {
             cudaError_t e = cudaFuncSetAttribute(k_prefill_attend<128>,

@@ -1,23 +1,35 @@
-// prefill_attn_ws.cu -- warp-specialised prefill sparse attention on tcgen05
-// (section 4.2), d = 128, bf16.  FA4-style ping-pong:
+// prefill_attn_ws.cu -- warp-specialised, persistent prefill sparse attention on
+// tcgen05 (section 4.2), d = 128, bf16.
 //
-//   CTA = two 128-row query tiles (Q0, Q1) of one (b,h) x one 4096-key split of
-//   its key stream (selected fixed keys, then the visible user keys, R8).
-//   warps 0-3  softmax group 0 (rows of Q0)    warps 4-7  softmax group 1 (Q1)
-//   warp  8    MMA issuer (one lane)          warps 9-11 loaders (cp.async)
+// Work decomposition.  A "segment" is one (b,h) x one pair of 128-row query
+// tiles (256 rows) with its key stream: the selected fixed keys of (b,h), then
+// the user keys visible to the pair's last row (R8).  The segments' 128-key
+// tiles are laid end to end (segment s = bh * npairs + pair) and the grid --
+// one CTA per SM -- cuts that list into equal contiguous ranges, so every CTA
+// does the same number of tiles whatever the per-head selection sizes are (the
+// decode kernel's equal-key-range idea).  A CTA walks the
+// "pieces" (segment x its range) in order; a segment cut by a CTA boundary
+// writes (O/l, lse) partials per piece, and the CTA that completes its last
+// piece merges them at its end.  Unsplit segments are written
+// directly.
+//
+// Inside a CTA (FA4-style):
+//   warps 0-3  softmax group 0 (query tile 0)   warps 4-7  softmax group 1 (tile 1)
+//   warp  8    MMA issuer (one lane)            warps 12-13 K loaders, 14-15 V loaders
+//   (setmaxnreg moves registers from warpgroups 2-3 to the softmax groups)
 //   TMEM: S0 | S1 | O0 | O1 (4 x 128 columns); P_g (bf16) is written by the
 //   softmax group into the first 64 columns of S_g and consumed from TMEM by the
-//   PV MMA (A operand in tensor memory), so shared memory holds only Q0, Q1 and
-//   a 2-stage K/V ring (192 KB).
-//   Order on the tensor core per key tile t: PV0(t), S0(t+1), PV1(t), S1(t+1):
-//   while group 0 runs the softmax of tile t+1, the tensor core computes
-//   group 1's PV(t) and S(t+1), and vice versa.
+//   PV MMA (A operand in tensor memory), so shared memory holds Q0, Q1, a
+//   3-stage K ring and a 2-stage V ring (224 KB).  K(t) is released as soon as
+//   S1(t) completes, V(t) after PV1(t), Q after the piece's last S.
+//   Tensor-core order per key tile t: PV0(t), S0(t+1), PV1(t), S1(t+1).
 //   Loaders gather the K/V rows by key position with 16-byte cp.async into the
 //   128B-swizzled operand layout; cp.async.mbarrier.arrive signals a stage.
 // Softmax: thread = query row, logits in registers, lazy O rescale (only when
-// the row max grows by > 2^8, FA4), ex2.approx, masks only on ragged / causal
-// diagonal tiles.  Each split writes (O/l, lse) partials; the CTA that
-// completes a pair's last split merges them.
+// the row max grows by > 2^8, FA4), FFMA2/FADD2 packed arithmetic, ex2.approx,
+// masks only on ragged / causal-diagonal tiles.
+#include <cuda.h>
+
 #include "common.cuh"
 #include "internal.h"
 #include "tcgen05.cuh"
@@ -26,24 +38,100 @@ namespace sqz {
 
 namespace ws {
 constexpr int D = 128;
-constexpr int MMAW = 8;               // MMA warp index
-constexpr int LD0 = 9, NLDW = 3;      // loader warps
-constexpr int NLD = NLDW * 32;        // loader threads
-constexpr int NT = 32 * (LD0 + NLDW); // 384
+constexpr int MMAW = 8;               // MMA warp index (warps 9-11 idle in the main loop)
+constexpr int KLW = 12, VLW = 14;     // K loader warps 12-13, V loader warps 14-15
+constexpr int NT = 512;               // 16 warps = 4 warpgroups
 constexpr int QT = 128;               // rows per query tile
+constexpr int PR = 2 * QT;            // rows per segment (query-tile pair)
 constexpr int KT = 128;               // keys per key tile
-constexpr int NST = 2;                // K/V stages
-constexpr int SPLIT = 4096;           // keys per CTA
+constexpr int NKS = 3, NVS = 2;       // K / V ring stages
 constexpr int HB = 128 * 128;         // bytes of one 64-element half of a 128-row tile
-constexpr int TILE = 2 * HB;          // 128 rows x 128 bf16
+constexpr int TILE = 2 * HB;          // 128 rows x 128 bf16 = 32 KB
 constexpr int OFF_Q = 0;              // Q0, Q1
-constexpr int OFF_KV = 2 * TILE;      // stage s: K at OFF_KV + s*2*TILE, V right after
-constexpr int OFF_POS = OFF_KV + NST * 2 * TILE;  // int [NST][128]
-constexpr int OFF_BAR = OFF_POS + NST * KT * 4;    // mbarriers
-constexpr int NBAR = 2 * NST + 2 + 2 + 2 + 1;
-constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
-constexpr int BYTES = OFF_TMEM + 16 + 1024;
+constexpr int OFF_K = 2 * TILE;
+constexpr int OFF_V = OFF_K + NKS * TILE;
+constexpr int OFF_BAR = OFF_V + NVS * TILE;
+constexpr int NBAR = 2 * NKS + 2 * NVS + 2 + 2 + 2 + 2;
+constexpr int OFF_MISC = OFF_BAR + NBAR * 8;  // tmem addr, first segment, merges
+constexpr int BYTES = OFF_MISC + 64 + 1024;   // + alignment slack
+static_assert(BYTES <= 232448, "shared memory budget");
+constexpr int INVALID = (int)0x80000000;      // key position of a masked (past-the-end) slot
 }  // namespace ws
+
+#ifdef SQZ_TRACE
+#ifndef SQZ_TRACE_CTA
+#define SQZ_TRACE_CTA 0
+#endif
+__device__ unsigned long long g_trace_ws[128 * 24];
+__device__ unsigned long long g_cta_ws[1024 * 4];  // per CTA: entry, loop end, exit (globaltimer)
+#define WS_CTA_T(slot)                                                                        \
+    do {                                                                                      \
+        if (threadIdx.x == 0 && blockIdx.x < 1024) {                                          \
+            unsigned long long t_;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            g_cta_ws[blockIdx.x * 4 + (slot)] = t_;                                           \
+        }                                                                                     \
+    } while (0)
+#define WS_TRACE(cond, it, slot)                                                              \
+    do {                                                                                      \
+        if ((cond) && blockIdx.x == SQZ_TRACE_CTA && (it) < 128) {                                       \
+            unsigned long long t_;                                                            \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));                                \
+            g_trace_ws[(it) * 24 + (slot)] = t_;                                              \
+        }                                                                                     \
+    } while (0)
+#else
+#define WS_TRACE(cond, it, slot) do { } while (0)
+#define WS_CTA_T(slot) do { } while (0)
+#endif
+
+// ---- packed fp32x2 arithmetic (FFMA2 / FADD2, sm_100) and the FMA-pipe exp2 ----
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const uint64_t *>(&a)), "l"(*reinterpret_cast<const uint64_t *>(&b)),
+          "l"(*reinterpret_cast<const uint64_t *>(&c)));
+    return *reinterpret_cast<float2 *>(&d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const uint64_t *>(&a)), "l"(*reinterpret_cast<const uint64_t *>(&b)));
+    return *reinterpret_cast<float2 *>(&d);
+}
+// 2^x for a pair without the MUFU: x = j + f (j = rint(x) by the 1.5*2^23 trick,
+// f in [-1/2, 1/2]), 2^f by a degree-3 polynomial (max relative error 7.5e-5,
+// far below the bf16 rounding of P), 2^j added into the exponent field.
+// x is clamped at -125 so 2^j stays a normal number (smaller p are irrelevant
+// next to the row maximum's p >= 2^-8).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+    constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
+    x.x = fmaxf(x.x, -125.f);
+    x.y = fmaxf(x.y, -125.f);
+    const float2 t = fadd2(x, make_float2(MAGIC, MAGIC));
+    const float2 jf = fadd2(t, make_float2(-MAGIC, -MAGIC));
+    const float2 f = ffma2(jf, make_float2(-1.f, -1.f), x);
+    float2 p = ffma2(f, make_float2(0.05517121f, 0.05517121f), make_float2(0.24261023f, 0.24261023f));
+    p = ffma2(p, f, make_float2(0.69326103f, 0.69326103f));
+    p = ffma2(p, f, make_float2(0.99992818f, 0.99992818f));
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
+// which key pairs of a 128-key tile take the polynomial (the rest use MUFU.EX2);
+// measured on cfg3: every step towards the polynomial was slower, so 0.
+#ifndef SQZ_PF_EMU_MASK
+#define SQZ_PF_EMU_MASK 0x00u
+#endif
+
+// bits j of a 32-bit word (slots base + j) that fall in [lo, hi)
+__device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
+    const int l = min(max(lo - base, 0), 32), h = min(max(hi - base, 0), 32);
+    const uint32_t below_h = h >= 32 ? 0xffffffffu : (1u << h) - 1u;
+    const uint32_t below_l = l >= 32 ? 0xffffffffu : (1u << l) - 1u;
+    return below_h & ~below_l;
+}
 
 __device__ __forceinline__ void tmem_st32f(uint32_t taddr, const float *v) {
     uint32_t u[32];
@@ -52,301 +140,630 @@ __device__ __forceinline__ void tmem_st32f(uint32_t taddr, const float *v) {
     tmem_st32u(taddr, u);
 }
 
-__global__ void __launch_bounds__(ws::NT, 1) k_prefill_attend_ws(AttnArgs a, int npairs) {
+// 64 threads gather a 128-row tile into the SW128 layout.  Thread lt (0..63):
+// warp w = lt/32 copies rows 2(w + 2j) + (lane/16), j = 0..31, chunk lane%16;
+// the row's key position is held by lane 2(j%16) + (lane/16) of the same warp
+// (posA for j < 16, posB for j >= 16) and broadcast by shuffle.
+__device__ __forceinline__ void gather_rows(uint32_t dst, const __nv_bfloat16 *fixed,
+                                            const __nv_bfloat16 *user, int posA, int posB, int lt) {
+    using namespace ws;
+    const int w = lt >> 5, lane = lt & 31, hh = lane >> 4, c = lane & 15;
+    const uint32_t coff = (uint32_t)((c >> 3) * HB);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const int pos = __shfl_sync(FULL, j < 16 ? posA : posB, 2 * (j & 15) + hh);
+        const int row = 2 * (w + 2 * j) + hh;
+        const bool valid = pos != INVALID;
+        const __nv_bfloat16 *src = pos >= 0 ? fixed + (size_t)pos * D : user + (size_t)(-1 - pos) * D;
+        cp_async16_zfill(dst + coff + sw128_off(row, c & 7), valid ? src + c * 8 : fixed, valid);
+    }
+}
+
+// TMA descriptor of Q (2-D [B*H*n_q, 128] bf16, box {64, 128}, 128B swizzle)
+struct TmaMaps {
+    CUtensorMap q;
+};
+
+// ---- the segment list ----
+// key stream of a segment: selected fixed keys [0, nkf), padding [nkf, nkf4)
+// (masked; nkf4 = nkf rounded up to 4 when user keys follow, so that every TMA
+// gather4 group of 4 stream slots reads from one tensor), user keys
+// [nkf4, nkf4 + nuv)
+struct Seg {
+    int bh, pair, nkf, nkf4, len, tiles;
+};
+__device__ __forceinline__ Seg seg_of(const AttnArgs &a, int npairs, int s) {
+    Seg g;
+    g.bh = s / npairs;
+    g.pair = s - g.bh * npairs;
+    g.nkf = ldcg(a.n_keys + g.bh);
+    const int last_row = min(g.pair * ws::PR + ws::PR, a.n_q) - 1;
+    int nuv = a.causal ? last_row + a.n_u - a.n_q + 1 : a.n_u;
+    nuv = max(0, min(nuv, a.n_u));
+    g.nkf4 = nuv > 0 ? (g.nkf + 3) & ~3 : g.nkf;
+    g.len = g.nkf4 + nuv;
+    g.tiles = (g.len + ws::KT - 1) / ws::KT;
+    return g;
+}
+// CTA owning global tile x when T tiles are cut into G equal ranges
+// [floor(T c / G), floor(T (c+1) / G))
+__device__ __forceinline__ int owner_of(long long x, long long T, int G) {
+    const long long c = ((x + 1) * G + T - 1) / T - 1;
+    return (int)(c < 0 ? 0 : (c > G - 1 ? G - 1 : c));
+}
+
+// Iterates the pieces of CTA c: all roles walk the identical sequence.
+struct PieceWalk {
+    int s, nseg, npairs, c, G;
+    long long st, lo, hi, T;
+    long long seg_st;  // start tile of the segment last returned
+    // next piece; false when done.  Fills seg, [pb, pe) tile range within the segment.
+    __device__ __forceinline__ bool next(const AttnArgs &a, Seg &g, int &pb, int &pe, int &seg_id) {
+        while (s < nseg) {
+            const bool last_cta = c == G - 1;
+            if (st > hi || (st == hi && !last_cta)) return false;
+            g = seg_of(a, npairs, s);
+            const long long st0 = st, en = st + g.tiles;
+            const long long b = max(st0, lo), e = min(en, hi);
+            seg_id = s;
+            seg_st = st0;
+            ++s;
+            st = en;
+            if (g.tiles == 0) {
+                if (st0 >= lo && (st0 < hi || last_cta)) {
+                    pb = pe = 0;
+                    return true;
+                }
+                continue;
+            }
+            if (e > b) {
+                pb = (int)(b - st0);
+                pe = (int)(e - st0);
+                return true;
+            }
+        }
+        return false;
+    }
+};
+
+__global__ void __launch_bounds__(ws::NT, 1)
+    k_prefill_attend_ws(AttnArgs a, int npairs, const __grid_constant__ TmaMaps maps) {
     using namespace ws;
     constexpr uint32_t IDESC_S = idesc_bf16(128, KT, false);
     constexpr uint32_t IDESC_O = idesc_bf16(128, D, true);
     extern __shared__ unsigned char smem_raw[];
     unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t sbase = smem_u32(sm);
-    int *s_pos = reinterpret_cast<int *>(sm + OFF_POS);
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
-    uint64_t *kv_full = bar, *kv_empty = bar + NST, *s_full = bar + 2 * NST,
-             *p_full = bar + 2 * NST + 2, *o_done = bar + 2 * NST + 4, *q_full = bar + 2 * NST + 6;
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sm + OFF_TMEM);
-    __shared__ int s_flag;
+    uint64_t *k_full = bar, *k_empty = bar + NKS, *v_full = bar + 2 * NKS,
+             *v_empty = bar + 2 * NKS + NVS, *s_full = bar + 2 * NKS + 2 * NVS,
+             *p_full = s_full + 2, *o_done = s_full + 4, *q_full = s_full + 6, *q_empty = s_full + 7;
+    // misc ints: [0] tmem addr, [1] first segment, [6..7] segments to merge,
+    // [8..9] merge flags, [10..13] their CTA ranges; misc64[0] (bytes 48..55) start
+    // tile of the first segment
+    int *misc = reinterpret_cast<int *>(sm + OFF_MISC);
+    long long *misc64 = reinterpret_cast<long long *>(sm + OFF_MISC + 56);
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int pair = blockIdx.x, split = blockIdx.y, bh = blockIdx.z;
-    const int h = bh % a.H;
-    const int t0 = pair * 2 * QT;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int nseg = a.B * a.H * npairs;
 
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int nkf = ldcg(a.n_keys + bh);
-    int nuv = a.causal ? (t0 + 2 * QT - 1) + a.n_u - a.n_q + 1 : a.n_u;
-    nuv = max(0, min(nuv, a.n_u));
-    const int len = nkf + nuv;
-    const int nsplit = (len + SPLIT - 1) / SPLIT;
-    const size_t row0 = (size_t)bh * a.n_q + t0;
-    if (nsplit == 0) {  // no key at all: identity outputs (an error when final)
-        if (split == 0 && tid < 2 * QT && t0 + tid < a.n_q) {
-            for (int k = 0; k < D; ++k) {
-                if (a.out_dtype == SQZ_BF16)
-                    reinterpret_cast<__nv_bfloat16 *>(a.O)[(row0 + tid) * D + k] = __float2bfloat16_rn(0.f);
-                else
-                    reinterpret_cast<float *>(a.O)[(row0 + tid) * D + k] = 0.f;
-            }
-            a.LSE[row0 + tid] = -INFINITY;
-            if (!a.partial) atomicOr(a.status, 1);
-        }
-        return;
-    }
-    if (split >= nsplit) return;
-    const int k_begin = split * SPLIT, k_end = min(len, k_begin + SPLIT);
-    const int ntile = (k_end - k_begin + KT - 1) / KT;
+    WS_TRACE(tid == 0, 0, 19);
+    WS_CTA_T(0);
 
-    if (warp == 0) tmem_alloc(s_tmem, 512);
+    // ---- segment prefix (in tiles): per-thread runs + block scan in the K ring ----
+    long long *scan = reinterpret_cast<long long *>(sm + OFF_K);
+    const int R = (nseg + NT - 1) / NT;
+    const int sb = min(nseg, tid * R), se = min(nseg, sb + R);
+    long long run = 0;
+    for (int s = sb; s < se; ++s) run += seg_of(a, npairs, s).tiles;
+    scan[tid] = run;
     if (tid == 0) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(&kv_full[s], NLD);
-            mbar_init(&kv_empty[s], 1);
+        misc[1] = nseg;
+        misc64[0] = 0;
+    }
+    __syncthreads();
+    for (int off = 1; off < NT; off <<= 1) {  // Hillis-Steele inclusive scan
+        const long long v = tid >= off ? scan[tid - off] : 0;
+        __syncthreads();
+        scan[tid] += v;
+        __syncthreads();
+    }
+    const long long T = scan[NT - 1];
+    // at most one CTA per tile, so every CTA range is non-empty and the owners of
+    // a segment's tiles are consecutive CTAs each holding one piece of it
+    const int G = (int)(T < 1 ? 1 : (T < (long long)gridDim.x ? T : (long long)gridDim.x));
+    if (c >= G) return;
+    const long long lo = T * c / G, hi = T * (c + 1) / G;
+    {
+        // first segment of this CTA: the first s that is not (entirely before lo)
+        long long st = scan[tid] - run;
+        for (int s = sb; s < se; ++s) {
+            const long long en = st + seg_of(a, npairs, s).tiles;
+            if (!(en <= lo && st < lo)) {
+                atomicMin(&misc[1], s);
+                break;
+            }
+            st = en;
+        }
+    }
+    __syncthreads();
+    {
+        const int s0 = misc[1];
+        if (s0 >= sb && s0 < se) {
+            long long st = scan[tid] - run;
+            for (int s = sb; s < s0; ++s) st += seg_of(a, npairs, s).tiles;
+            misc64[0] = st;
+        }
+    }
+    if (warp == 0) tmem_alloc(reinterpret_cast<uint32_t *>(&misc[0]), 512);
+    if (tid == 0) {
+        for (int s = 0; s < NKS; ++s) {
+            mbar_init(&k_full[s], 64);
+            mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < NVS; ++s) {
+            mbar_init(&v_full[s], 64);
+            mbar_init(&v_empty[s], 1);
         }
         for (int g = 0; g < 2; ++g) {
             mbar_init(&s_full[g], 1);
             mbar_init(&p_full[g], 128);
             mbar_init(&o_done[g], 1);
         }
-        mbar_init(q_full, NLD);
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        misc[6] = misc[7] = -1;
         mbar_fence_init();
     }
     tc_fence_before();
-    __syncthreads();
+    __syncthreads();  // also: the scan scratch in the K ring is dead before any cp.async
     tc_fence_after();
-    const uint32_t tmem = *s_tmem;
+    const uint32_t tmem = static_cast<uint32_t>(misc[0]);
+    PieceWalk walk{misc[1], nseg, npairs, c, G, misc64[0], lo, hi, T, 0};
+    WS_TRACE(tid == 0, 0, 20);
 
-    if (warp >= LD0) {
+    if (warp >= KLW) {
         // ======================= loaders =======================
-        const int li = tid - LD0 * 32;
-        const __nv_bfloat16 *Qb = reinterpret_cast<const __nv_bfloat16 *>(a.Q) + row0 * D;
-        for (int e = li; e < 2 * QT * 16; e += NLD) {
-            const int r = e >> 4, c = e & 15, g = r >> 7, rr = r & 127;
-            const bool valid = t0 + r < a.n_q;
-            cp_async16_zfill(sbase + OFF_Q + g * TILE + (c >> 3) * HB + sw128_off(rr, c & 7),
-                             Qb + (size_t)(valid ? r : 0) * D + c * 8, valid);
-        }
-        cp_async_mbar_arrive(q_full);
-        const __nv_bfloat16 *Kf = reinterpret_cast<const __nv_bfloat16 *>(a.Kp) + (size_t)h * a.L * D;
-        const __nv_bfloat16 *Vf = reinterpret_cast<const __nv_bfloat16 *>(a.Vp) + (size_t)h * a.L * D;
-        const __nv_bfloat16 *Ku = reinterpret_cast<const __nv_bfloat16 *>(a.Ku) + (size_t)bh * a.n_u * D;
-        const __nv_bfloat16 *Vu = reinterpret_cast<const __nv_bfloat16 *>(a.Vu) + (size_t)bh * a.n_u * D;
-        const int32_t *kidx = a.key_idx + (size_t)bh * a.L;
-        auto pos_of = [&](int k) -> int {
-            if (k >= k_end) return 0;
-            return k < nkf ? ldcg(kidx + k) : -1 - (k - nkf);
-        };
-        for (int t = 0; t < ntile; ++t) {
-            const int st = t % NST, k0 = k_begin + t * KT;
-            const int p0 = pos_of(k0 + li);
-            const int p1 = li + NLD < KT ? pos_of(k0 + li + NLD) : 0;
-            if (t >= NST) mbar_wait(&kv_empty[st], ((t / NST) - 1) & 1);
-            s_pos[st * KT + li] = p0;
-            if (li + NLD < KT) s_pos[st * KT + li + NLD] = p1;
-            named_bar(2, NLD);
-            const uint32_t kb = sbase + OFF_KV + st * 2 * TILE, vb = kb + TILE;
-            for (int e = li; e < KT * 16; e += NLD) {
-                const int key = e >> 4, c = e & 15;
-                const bool valid = k0 + key < k_end;
-                const int pos = s_pos[st * KT + key];
-                const __nv_bfloat16 *ks = pos >= 0 ? Kf + (size_t)pos * D : Ku + (size_t)(-1 - pos) * D;
-                const __nv_bfloat16 *vs = pos >= 0 ? Vf + (size_t)pos * D : Vu + (size_t)(-1 - pos) * D;
-                const uint32_t off = (c >> 3) * HB + sw128_off(key, c & 7);
-                cp_async16_zfill(kb + off, valid ? ks + c * 8 : Kf, valid);
-                cp_async16_zfill(vb + off, valid ? vs + c * 8 : Vf, valid);
+        // K/V rows gathered by key position with 16-byte cp.async (a TMA gather4
+        // moves only 512 B per instruction and measured ~3x slower here); the Q
+        // pair is two contiguous 128-row tiles and comes by TMA
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+        const int lane = tid & 31;
+        const bool isK = warp < VLW;
+        const int lt = tid - (isK ? KLW : VLW) * 32;  // 0..63
+        const int w = lt >> 5;
+        const int rA = 2 * (w + 2 * (lane >> 1)) + (lane & 1);  // this lane's rows rA, rA + 64
+        const int nst = isK ? NKS : NVS;
+        uint64_t *full = isK ? k_full : v_full, *empty = isK ? k_empty : v_empty;
+        const uint32_t ring = sbase + (isK ? OFF_K : OFF_V);
+        Seg g;
+        int pb, pe, s_id, tau = 0, piece = 0;
+        while (walk.next(a, g, pb, pe, s_id)) {
+            if (pe == pb) continue;
+            const int h = g.bh % a.H;
+            const __nv_bfloat16 *Fx = reinterpret_cast<const __nv_bfloat16 *>(isK ? a.Kp : a.Vp) + (size_t)h * a.L * D;
+            const __nv_bfloat16 *Us = reinterpret_cast<const __nv_bfloat16 *>(isK ? a.Ku : a.Vu) + (size_t)g.bh * a.n_u * D;
+            const int32_t *kidx = a.key_idx + (size_t)g.bh * a.L;
+            // stream slot -> key position (>= 0 fixed, < 0 user), INVALID when masked
+            auto pos_of = [&](int k) -> int {
+                if (k >= g.len || (k >= g.nkf && k < g.nkf4)) return INVALID;
+                return k < g.nkf ? ldcg(kidx + k) : -1 - (k - g.nkf4);
+            };
+            for (int tt = pb; tt < pe; ++tt, ++tau) {
+                const int st = tau % nst, k0 = tt * KT;
+                const int pA = pos_of(k0 + rA), pB = pos_of(k0 + rA + 64);
+                if (tau >= nst) mbar_wait(&empty[st], ((tau / nst) - 1) & 1);
+                WS_TRACE(lt == 0, tau, isK ? 10 : 11);
+                gather_rows(ring + st * TILE, Fx, Us, pA, pB, lt);
+                cp_async_mbar_arrive(&full[st]);
+                WS_TRACE(lt == 0, tau, isK ? 8 : 9);
+                if (isK && tt == pb && lt == 0) {
+                    // the piece's Q pair once the previous piece's S are done (after the
+                    // first K tile is in flight, so a piece switch costs one Q latency)
+                    if (piece > 0) mbar_wait(q_empty, (piece - 1) & 1);
+                    mbar_arrive_expect_tx(q_full, 2 * TILE);
+                    WS_TRACE(true, tau, 23);
+                    const int y0 = g.bh * a.n_q + g.pair * PR;
+#pragma unroll
+                    for (int qg = 0; qg < 2; ++qg)
+#pragma unroll
+                        for (int hf = 0; hf < 2; ++hf)
+                            tma_load_2d(sbase + OFF_Q + qg * TILE + hf * HB, &maps.q, hf * 64, y0 + qg * QT, q_full);
+                }
             }
-            cp_async_mbar_arrive(&kv_full[st]);
-            // s_pos[st] may be rewritten only after every loader has issued from it
-            named_bar(2, NLD);
+            ++piece;
         }
     } else if (warp == MMAW) {
         // ======================= MMA issuer =======================
-        if (lane == 0) {
-            auto wait_kv = [&](int t) {
-                mbar_wait(&kv_full[t % NST], (t / NST) & 1);
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+        if ((tid & 31) == 0) {
+            auto wait_full = [&](uint64_t *b, int t, int nst) {
+                mbar_wait(&b[t % nst], (t / nst) & 1);
                 fence_async_smem();
                 tc_fence_after();
             };
+            // descriptors: base + (byte offset >> 4) (the start-address field is the low bits)
+            const uint64_t dQ = sdesc_sw128(sbase + OFF_Q, 16, 1024);
+            const uint64_t dK = sdesc_sw128(sbase + OFF_K, 16, 1024);
+            const uint64_t dV = sdesc_sw128(sbase + OFF_V, HB, 1024);
             auto issue_S = [&](int g, int t) {
-                const uint32_t qb = sbase + OFF_Q + g * TILE;
-                const uint32_t kb = sbase + OFF_KV + (t % NST) * 2 * TILE;
+                const uint64_t qd = dQ + (uint64_t)((g * TILE) >> 4);
+                const uint64_t kd = dK + (uint64_t)(((t % NKS) * TILE) >> 4);
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
-                    const uint32_t off = (ks >> 2) * HB + (ks & 3) * 32;
-                    umma_bf16(tmem + g * 128, sdesc_sw128(qb + off, 16, 1024),
-                              sdesc_sw128(kb + off, 16, 1024), IDESC_S, ks > 0);
+                    const uint32_t off = ((ks >> 2) * HB + (ks & 3) * 32) >> 4;
+                    umma_bf16(tmem + g * 128, qd + off, kd + off, IDESC_S, ks > 0);
                 }
                 umma_commit(&s_full[g]);
             };
-            auto issue_PV = [&](int g, int t) {
-                const uint32_t vb = sbase + OFF_KV + (t % NST) * 2 * TILE + TILE;
+            auto issue_PV = [&](int g, int t, bool first) {
+                const uint64_t vd = dV + (uint64_t)(((t % NVS) * TILE) >> 4);
 #pragma unroll
                 for (int ks = 0; ks < KT / 16; ++ks)
-                    umma_bf16_ts(tmem + 256 + g * 128, tmem + g * 128 + ks * 8,
-                                 sdesc_sw128(vb + ks * 2048, HB, 1024), IDESC_O, (t > 0 || ks > 0));
+                    umma_bf16_ts(tmem + 256 + g * 128, tmem + g * 128 + ks * 8, vd + (ks * 2048 >> 4),
+                                 IDESC_O, (!first || ks > 0));
                 umma_commit(&o_done[g]);
             };
-            mbar_wait(q_full, 0);
-            wait_kv(0);
-            issue_S(0, 0);
-            issue_S(1, 0);
-            for (int t = 0; t < ntile; ++t) {
-                mbar_wait(&p_full[0], t & 1);
-                tc_fence_after();
-                issue_PV(0, t);
-                if (t + 1 < ntile) {
-                    wait_kv(t + 1);
-                    issue_S(0, t + 1);
+            Seg g;
+            int pb, pe, s_id, tau = 0, piece = 0;
+            while (walk.next(a, g, pb, pe, s_id)) {
+                const int n = pe - pb;
+                if (n == 0) continue;
+                mbar_wait(q_full, piece & 1);
+                WS_TRACE(true, tau, 15);
+                wait_full(k_full, tau, NKS);
+                issue_S(0, tau);
+                issue_S(1, tau);
+                umma_commit(&k_empty[tau % NKS]);
+                if (n == 1) umma_commit(q_empty);
+                for (int i = 0; i < n; ++i, ++tau) {
+                    mbar_wait(&p_full[0], tau & 1);
+                    tc_fence_after();
+                    WS_TRACE(true, tau, 4);
+                    wait_full(v_full, tau, NVS);
+                    WS_TRACE(true, tau, 5);
+                    issue_PV(0, tau, i == 0);
+                    WS_TRACE(true, tau, 12);
+                    if (i + 1 < n) {
+                        wait_full(k_full, tau + 1, NKS);
+                        WS_TRACE(true, tau, 6);
+                        issue_S(0, tau + 1);
+                        WS_TRACE(true, tau, 13);
+                    }
+                    mbar_wait(&p_full[1], tau & 1);
+                    tc_fence_after();
+                    WS_TRACE(true, tau, 7);
+                    issue_PV(1, tau, i == 0);
+                    umma_commit(&v_empty[tau % NVS]);
+                    if (i + 1 < n) {
+                        issue_S(1, tau + 1);
+                        umma_commit(&k_empty[(tau + 1) % NKS]);
+                        if (i + 2 == n) umma_commit(q_empty);
+                    }
                 }
-                mbar_wait(&p_full[1], t & 1);
-                tc_fence_after();
-                issue_PV(1, t);
-                umma_commit(&kv_empty[t % NST]);  // stage t free once its MMAs complete
-                if (t + 1 < ntile) issue_S(1, t + 1);
+                ++piece;
             }
         }
         __syncwarp();
+    } else if (warp > MMAW) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");  // idle warps 9-11
     } else {
         // ======================= softmax groups =======================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
         const int g = warp >> 2, r = tid & 127;  // TMEM lane = r
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t tS = tmem + g * 128 + lane_off, tO = tmem + 256 + g * 128 + lane_off;
-        const int trow = t0 + g * QT + r;
-        const bool row_ok = trow < a.n_q;
-        const int ulim = trow + a.n_u - a.n_q;
         const float sl2 = a.scale * LOG2E;
-        float m_used = -INFINITY, l = 0.f;
-        for (int t = 0; t < ntile; ++t) {
-            const int k0 = k_begin + t * KT;
-            mbar_wait(&s_full[g], t & 1);
-            tc_fence_after();
-            float sv[KT];
-#pragma unroll
-            for (int c = 0; c < KT / 32; ++c)
-                tmem_ld32(tS + c * 32, *reinterpret_cast<float(*)[32]>(sv + c * 32));
-            tmem_wait_ld();
-            const bool full = row_ok && k0 + KT <= k_end && (k0 + KT <= nkf || k0 + KT - 1 - nkf <= ulim);
-            if (!full) {
-#pragma unroll
-                for (int j = 0; j < KT; ++j) {
-                    const int k = k0 + j;
-                    const bool vis = row_ok && k < k_end && (k < nkf || k - nkf <= ulim);
-                    if (!vis) sv[j] = -INFINITY;
+        Seg sg;
+        int pb, pe, s_id, tau = 0;
+        while (walk.next(a, sg, pb, pe, s_id)) {
+            const int trow = sg.pair * PR + g * QT + r;
+            const bool row_ok = trow < a.n_q;
+            const size_t orow = (size_t)sg.bh * a.n_q + trow;
+            if (pe == pb) {  // no key at all: identity outputs (an error when final)
+                if (row_ok) {
+                    for (int k = 0; k < D; ++k) {
+                        if (a.out_dtype == SQZ_BF16)
+                            reinterpret_cast<__nv_bfloat16 *>(a.O)[orow * D + k] = __float2bfloat16_rn(0.f);
+                        else
+                            reinterpret_cast<float *>(a.O)[orow * D + k] = 0.f;
+                    }
+                    a.LSE[orow] = -INFINITY;
+                    if (!a.partial) atomicOr(a.status, 1);
                 }
+                continue;
             }
-            float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-            for (int j = 0; j < KT; j += 4) {
-                mx4[0] = fmaxf(mx4[0], sv[j]);
-                mx4[1] = fmaxf(mx4[1], sv[j + 1]);
-                mx4[2] = fmaxf(mx4[2], sv[j + 2]);
-                mx4[3] = fmaxf(mx4[3], sv[j + 3]);
-            }
-            const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
-            const bool need = mx > m_used + 8.f;
-            const float alpha = need ? ((m_used == -INFINITY) ? 0.f : exp2f(m_used - mx)) : 1.f;
-            if (t > 0 && __any_sync(FULL, need)) {
-                // O_g must be stable: PV_g(t-1) has completed
-                mbar_wait(&o_done[g], (t - 1) & 1);
+            // visible keys of the row form a prefix of the segment's stream: all fixed
+            // keys, then user keys u <= trow + n_u - n_q (causal, R8) or all of them
+            // visible stream slots: [0, a_end) fixed keys and [nkf4, b_end) user keys
+            // u <= trow + n_u - n_q (causal, R8) or all of them
+            const int uvis = a.causal ? max(0, trow + a.n_u - a.n_q + 1) : a.n_u;
+            const int a_end = row_ok ? sg.nkf : 0;
+            const int b_end = row_ok ? min(sg.len, sg.nkf4 + uvis) : 0;
+            float m_used = -INFINITY, l = 0.f;
+            for (int tt = pb; tt < pe; ++tt, ++tau) {
+                const int k0 = tt * KT;
+                mbar_wait(&s_full[g], tau & 1);
                 tc_fence_after();
-#pragma unroll 1
-                for (int c = 0; c < D / 32; ++c) {
-                    float v[32];
-                    tmem_ld32(tO + c * 32, v);
-                    tmem_wait_ld();
+                WS_TRACE(r == 0, tau, 2 * g);
+                float sv[KT];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] *= alpha;
-                    tmem_st32(tO + c * 32, v);
+                for (int cc = 0; cc < KT / 32; ++cc)
+                    tmem_ld32(tS + cc * 32, *reinterpret_cast<float(*)[32]>(sv + cc * 32));
+                tmem_wait_ld();
+                WS_TRACE(r == 0 && g == 0, tau, 16);
+                const int na = a_end - k0, nb0 = sg.nkf4 - k0, nb1 = b_end - k0;
+                if (na < KT && (nb0 > 0 || nb1 < KT)) {
+                    // visible slots [0, na) u [nb0, nb1) as a 128-bit mask, then one
+                    // bit test + select per logit
+#pragma unroll
+                    for (int w = 0; w < KT / 32; ++w) {
+                        const uint32_t vm = range_bits(0, na, 32 * w) | range_bits(nb0, nb1, 32 * w);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            sv[32 * w + j] = (vm >> j) & 1u ? sv[32 * w + j] : -INFINITY;
+                    }
                 }
-                tmem_wait_st();
-            }
-            l *= alpha;
-            if (need) m_used = mx;
-            const float moff = (m_used == -INFINITY) ? 0.f : m_used;
-            float ls[4] = {0.f, 0.f, 0.f, 0.f};
-            // p packed in place: bf16x2 of keys (2j, 2j+1) into sv[j] (slot j <= 2j is consumed)
+                float mx8[8];
 #pragma unroll
-            for (int j = 0; j < KT / 2; ++j) {
-                const float p0 = fast_exp2(fmaf(sv[2 * j], sl2, -moff));
-                const float p1 = fast_exp2(fmaf(sv[2 * j + 1], sl2, -moff));
-                ls[j & 3] += p0 + p1;
-                const __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-                sv[j] = __uint_as_float(*reinterpret_cast<const uint32_t *>(&b2));
-            }
-            l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-            tmem_st32f(tS, sv);        // P columns 0..31
-            tmem_st32f(tS + 32, sv + 32);  // P columns 32..63
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&p_full[g]);
-        }
-        // ---- this split's partial for the row ----
-        mbar_wait(&o_done[g], (ntile - 1) & 1);
-        tc_fence_after();
-        const size_t slot = ((size_t)row0 + g * QT + r) * a.max_chunks + split;
-        const bool have = row_ok && l > 0.f;
-        const float inv_l = have ? 1.0f / l : 0.f;
+                for (int j = 0; j < 8; ++j) mx8[j] = sv[j];
+#pragma unroll
+                for (int j = 8; j < KT; j += 8) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) mx8[q] = fmaxf(mx8[q], sv[j + q]);
+                }
+                const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+                const bool need = mx > m_used + 8.f;
+                const float alpha = need ? ((m_used == -INFINITY) ? 0.f : exp2f(m_used - mx)) : 1.f;
+                if (tt > pb && __any_sync(FULL, need)) {
+                    // O_g must be stable: PV_g(tau-1) has completed
+                    mbar_wait(&o_done[g], (tau - 1) & 1);
+                    tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-            float v[32];
-            tmem_ld32(tO + c * 32, v);
-            tmem_wait_ld();
-            if (row_ok) {
-                float4 *dst = reinterpret_cast<float4 *>(a.part_o + slot * D + c * 32);
+                    for (int cc = 0; cc < D / 32; ++cc) {
+                        float v[32];
+                        tmem_ld32(tO + cc * 32, v);
+                        tmem_wait_ld();
 #pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                    dst[j / 4] = make_float4(v[j] * inv_l, v[j + 1] * inv_l, v[j + 2] * inv_l, v[j + 3] * inv_l);
+                        for (int j = 0; j < 32; ++j) v[j] *= alpha;
+                        tmem_st32(tO + cc * 32, v);
+                    }
+                    tmem_wait_st();
+                }
+                l *= alpha;
+                if (need) m_used = mx;
+                const float moff = (m_used == -INFINITY) ? 0.f : m_used;
+                WS_TRACE(r == 0 && g == 0, tau, 14);
+                // p = 2^(s*scale*log2e - m): FFMA2 for the pair, MUFU.EX2 (or the
+                // FMA-pipe polynomial), bf16x2 packed in place into sv[j] (slot j <= 2j
+                // is already consumed), row sum by FADD2
+                const float2 sc2 = make_float2(sl2, sl2), mo2 = make_float2(-moff, -moff);
+                float2 acc2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                for (int j = 0; j < KT / 2; ++j) {
+                    const float2 x = ffma2(make_float2(sv[2 * j], sv[2 * j + 1]), sc2, mo2);
+                    float2 p;
+                    if ((SQZ_PF_EMU_MASK >> (j & 7)) & 1u) {
+                        p = exp2_poly2(x);
+                    } else {
+                        p.x = fast_exp2(x.x);
+                        p.y = fast_exp2(x.y);
+                    }
+                    acc2[j & 1] = fadd2(acc2[j & 1], p);
+                    const __nv_bfloat162 b2 = __floats2bfloat162_rn(p.x, p.y);
+                    sv[j] = __uint_as_float(*reinterpret_cast<const uint32_t *>(&b2));
+                }
+                const float2 accs = fadd2(acc2[0], acc2[1]);
+                l += accs.x + accs.y;
+                WS_TRACE(r == 0 && g == 0, tau, 17);
+                tmem_st32f(tS, sv);            // P columns 0..31
+                tmem_st32f(tS + 32, sv + 32);  // P columns 32..63
+                tmem_wait_st();
+                WS_TRACE(r == 0 && g == 0, tau, 18);
+                tc_fence_before();
+                mbar_arrive(&p_full[g]);
+                WS_TRACE(r == 0, tau, 2 * g + 1);
+            }
+            // ---- the piece's result for the row: final, or a partial to merge ----
+            mbar_wait(&o_done[g], (tau - 1) & 1);
+            tc_fence_after();
+            const int c0 = owner_of(walk.seg_st, T, G), c1 = owner_of(walk.seg_st + sg.tiles - 1, T, G);
+            const bool have = row_ok && l > 0.f;
+            const float inv_l = have ? 1.0f / l : 0.f;
+            const float lse = have ? (m_used + log2f(l)) * LN2 : -INFINITY;
+            if (c0 == c1) {
+#pragma unroll 1
+                for (int cc = 0; cc < D / 32; ++cc) {
+                    float v[32];
+                    tmem_ld32(tO + cc * 32, v);
+                    tmem_wait_ld();
+                    if (row_ok) {
+                        if (a.out_dtype == SQZ_BF16) {
+                            uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(a.O) + orow * D + cc * 32);
+#pragma unroll
+                            for (int j = 0; j < 32; j += 8) {
+                                uint32_t u[4];
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    const __nv_bfloat162 b = __floats2bfloat162_rn(v[j + 2 * q] * inv_l, v[j + 2 * q + 1] * inv_l);
+                                    u[q] = *reinterpret_cast<const uint32_t *>(&b);
+                                }
+                                dst[j / 8] = make_uint4(u[0], u[1], u[2], u[3]);
+                            }
+                        } else {
+                            float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.O) + orow * D + cc * 32);
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4)
+                                dst[j / 4] = make_float4(v[j] * inv_l, v[j + 1] * inv_l, v[j + 2] * inv_l, v[j + 3] * inv_l);
+                        }
+                    }
+                }
+                if (row_ok) {
+                    a.LSE[orow] = lse;
+                    if (!have && !a.partial) atomicOr(a.status, 1);
+                }
+            } else {
+                const size_t slot = (size_t)(s_id + c) * PR + g * QT + r;  // piece id = segment + CTA
+#pragma unroll 1
+                for (int cc = 0; cc < D / 32; ++cc) {
+                    float v[32];
+                    tmem_ld32(tO + cc * 32, v);
+                    tmem_wait_ld();
+                    if (row_ok) {
+                        float4 *dst = reinterpret_cast<float4 *>(a.part_o + slot * D + cc * 32);
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            dst[j / 4] = make_float4(v[j] * inv_l, v[j + 1] * inv_l, v[j + 2] * inv_l, v[j + 3] * inv_l);
+                    }
+                }
+                if (row_ok) a.part_lse[slot] = lse;
+                WS_TRACE(r == 0 && g == 0, tau - 1, 19);
+                // only a CTA's first and last pieces can be cut
+                if (tid == 0) {
+                    if (misc[6] < 0) misc[6] = s_id;
+                    else if (misc[6] != s_id) misc[7] = s_id;
+                    misc[10 + 2 * (misc[7] == s_id ? 1 : 0)] = c0;
+                    misc[11 + 2 * (misc[7] == s_id ? 1 : 0)] = c1;
+                }
             }
         }
-        if (row_ok) a.part_lse[slot] = have ? (m_used + log2f(l)) * LN2 : -INFINITY;
         tc_fence_before();
     }
     __threadfence();
     __syncthreads();
+    WS_TRACE(tid == 0, 0, 21);
+    WS_CTA_T(1);
     if (warp == 0) tmem_dealloc(tmem, 512);
-    // ---- the CTA completing the pair's last split merges ----
+    // ---- tickets: the CTA completing a cut segment's last piece merges it ----
     if (tid == 0) {
-        int *cnt = a.row_cnt + (size_t)bh * npairs + pair;
-        const int t = atomicAdd(cnt, 1);
-        s_flag = (t == nsplit - 1);
-        if (s_flag) *cnt = 0;
-    }
-    __syncthreads();
-    if (!s_flag) return;
-    __threadfence();
-    for (int r = warp; r < 2 * QT; r += NT / 32) {
-        if (t0 + r >= a.n_q) break;
-        const size_t row = row0 + r;
-        float M = -INFINITY;
-        for (int p = 0; p < nsplit; ++p) M = fmaxf(M, ldcg(a.part_lse + row * a.max_chunks + p));
-        float L = 0.f, acc[D / 32];
-#pragma unroll
-        for (int k = 0; k < D / 32; ++k) acc[k] = 0.f;
-        if (M != -INFINITY) {
-            for (int p = 0; p < nsplit; ++p) {
-                const float w = expf(ldcg(a.part_lse + row * a.max_chunks + p) - M);
-                L += w;
-                const float *op = a.part_o + (row * a.max_chunks + p) * D;
-#pragma unroll
-                for (int k = 0; k < D / 32; ++k) acc[k] = fmaf(w, ldcg(op + lane + 32 * k), acc[k]);
+        for (int k = 0; k < 2; ++k) {
+            misc[8 + k] = 0;
+            const int s = misc[6 + k];
+            if (s < 0) continue;
+            const int c0 = misc[10 + 2 * k], c1 = misc[11 + 2 * k];
+            int *cnt = a.row_cnt + s;
+            const int t = atomicAdd(cnt, 1);
+            if (t == c1 - c0) {
+                *cnt = 0;
+                misc[8 + k] = 1;
             }
         }
-#pragma unroll
-        for (int k = 0; k < D / 32; ++k) {
-            const float o = M == -INFINITY ? 0.f : acc[k] / L;
-            if (a.out_dtype == SQZ_BF16)
-                reinterpret_cast<__nv_bfloat16 *>(a.O)[row * D + lane + 32 * k] = __float2bfloat16_rn(o);
-            else
-                reinterpret_cast<float *>(a.O)[row * D + lane + 32 * k] = o;
-        }
-        if (lane == 0) {
-            a.LSE[row] = M == -INFINITY ? -INFINITY : M + logf(L);
+    }
+    __syncthreads();
+    float *wgt = reinterpret_cast<float *>(sm + OFF_K);  // [parts][256] merge weights (rings are dead)
+    for (int k = 0; k < 2; ++k) {
+        if (!misc[8 + k]) continue;
+        __threadfence();
+        const int s = misc[6 + k], c0 = misc[10 + 2 * k], c1 = misc[11 + 2 * k];
+        const int np = c1 - c0 + 1;
+        const int bh = s / npairs, pair = s - bh * npairs;
+        const int nrow = min(PR, a.n_q - pair * PR);
+        const float *lse_p = a.part_lse + (size_t)(s + c0) * PR;  // part p, row rr: lse_p[p * PR + rr]
+        const float *o_p = a.part_o + (size_t)(s + c0) * PR * D;
+        for (int rr = tid; rr < nrow; rr += NT) {
+            float M = -INFINITY;
+            for (int p = 0; p < np; ++p) M = fmaxf(M, ldcg(lse_p + (size_t)p * PR + rr));
+            float L = 0.f;
+            for (int p = 0; p < np; ++p) {
+                const float w = M == -INFINITY ? 0.f : expf(ldcg(lse_p + (size_t)p * PR + rr) - M);
+                wgt[p * PR + rr] = w;
+                L += w;
+            }
+            const float inv = M == -INFINITY ? 0.f : 1.f / L;
+            for (int p = 0; p < np; ++p) wgt[p * PR + rr] *= inv;
+            const size_t orow = (size_t)bh * a.n_q + pair * PR + rr;
+            a.LSE[orow] = M == -INFINITY ? -INFINITY : M + logf(L);
             if (M == -INFINITY && !a.partial) atomicOr(a.status, 1);
         }
+        __syncthreads();
+        // item = (row, 4-dim chunk); loads independent across parts and items
+        for (int it = tid; it < nrow * (D / 4); it += NT) {
+            const int rr = it / (D / 4), ch = it % (D / 4);
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            int p = 0;
+            for (; p + 4 <= np; p += 4) {
+                float4 o[4];
+                float w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    o[q] = __ldcg(reinterpret_cast<const float4 *>(o_p + ((size_t)(p + q) * PR + rr) * D) + ch);
+                    w[q] = wgt[(p + q) * PR + rr];
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc.x = fmaf(w[q], o[q].x, acc.x);
+                    acc.y = fmaf(w[q], o[q].y, acc.y);
+                    acc.z = fmaf(w[q], o[q].z, acc.z);
+                    acc.w = fmaf(w[q], o[q].w, acc.w);
+                }
+            }
+            for (; p < np; ++p) {
+                const float4 o = __ldcg(reinterpret_cast<const float4 *>(o_p + ((size_t)p * PR + rr) * D) + ch);
+                const float w = wgt[p * PR + rr];
+                acc.x = fmaf(w, o.x, acc.x);
+                acc.y = fmaf(w, o.y, acc.y);
+                acc.z = fmaf(w, o.z, acc.z);
+                acc.w = fmaf(w, o.w, acc.w);
+            }
+            const size_t orow = (size_t)bh * a.n_q + pair * PR + rr;
+            if (a.out_dtype == SQZ_BF16) {
+                __nv_bfloat162 *dst = reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<__nv_bfloat16 *>(a.O) + orow * D + ch * 4);
+                dst[0] = __floats2bfloat162_rn(acc.x, acc.y);
+                dst[1] = __floats2bfloat162_rn(acc.z, acc.w);
+            } else {
+                reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.O) + orow * D)[ch] = acc;
+            }
+        }
+        __syncthreads();
     }
+    WS_TRACE(tid == 0, 0, 22);
+    WS_CTA_T(2);
 }
 
+namespace {
+int ws_grid() {
+    static int g = 0;
+    if (!g) {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        g = n > 0 ? n : 148;
+    }
+    return g;
+}
+}  // namespace
+
+bool prefill_ws_applies(int d, int dtype, int n_q) {
+    static const bool legacy = getenv("SQZ_PF_LEGACY") != nullptr;  // A/B switch
+    return !legacy && n_q > 1 && d == 128 && dtype == SQZ_BF16;
+}
+// rows of the partial buffers: one 256-row slot per piece, piece id = segment + CTA
+size_t prefill_ws_part_rows(int B, int H, int n_q) {
+    const size_t npairs = (size_t)(n_q + ws::PR - 1) / ws::PR;
+    return ((size_t)B * H * npairs + ws_grid()) * ws::PR;
+}
+
+namespace {
+CUresult encode_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows) {
+    cuuint64_t dims[2] = {(cuuint64_t)ws::D, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ws::D * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims,
+                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+}  // namespace
+
 cudaError_t launch_prefill_attention_ws(const AttnArgs &a, cudaStream_t st) {
-    const int npairs = (a.n_q + 2 * ws::QT - 1) / (2 * ws::QT);
-    const int nsplit_max = (int)((a.L + a.n_u + ws::SPLIT - 1) / ws::SPLIT);
+    const int npairs = (a.n_q + ws::PR - 1) / ws::PR;
+    TmaMaps maps;
+    if (encode_map(&maps.q, a.Q, (uint64_t)a.B * a.H * a.n_q, 128) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
     static bool set = false;
     if (!set) {
         cudaError_t e = cudaFuncSetAttribute(k_prefill_attend_ws,
@@ -355,7 +772,7 @@ cudaError_t launch_prefill_attention_ws(const AttnArgs &a, cudaStream_t st) {
         set = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(npairs, nsplit_max, a.B * a.H);
+    cfg.gridDim = dim3(ws_grid());
     cfg.blockDim = dim3(ws::NT);
     cfg.dynamicSmemBytes = ws::BYTES;
     cfg.stream = st;
@@ -364,7 +781,16 @@ cudaError_t launch_prefill_attention_ws(const AttnArgs &a, cudaStream_t st) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_prefill_attend_ws, a, npairs);
+    return cudaLaunchKernelEx(&cfg, k_prefill_attend_ws, a, npairs, maps);
 }
 
 }  // namespace sqz
+
+#ifdef SQZ_TRACE
+extern "C" int sqz_trace_ws_cta(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, sqz::g_cta_ws, bytes < sizeof(sqz::g_cta_ws) ? bytes : sizeof(sqz::g_cta_ws));
+}
+extern "C" int sqz_trace_ws(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, sqz::g_trace_ws, bytes < sizeof(sqz::g_trace_ws) ? bytes : sizeof(sqz::g_trace_ws));
+}
+#endif

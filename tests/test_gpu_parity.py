@@ -146,16 +146,23 @@ def test_decode_lookup_and_attention(case):
 
 
 PREFILL_CASES = [
-    ("bf16_single", 2, 2048, 128, 100, 0, synth.BF16, 1, 200, 200, 0.3),
-    ("fp32_d64", 1, 1500, 64, 40, 0, synth.F32, 2, 70, 90, 0.3),
-    ("hier_bf16", 2, 3000, 128, 150, 30, synth.BF16, 1, 130, 130, 0.15),
+    # id, H, L, d, c2, c1, dtype, B, n_q, n_u, retention, causal
+    ("bf16_single", 2, 2048, 128, 100, 0, synth.BF16, 1, 200, 200, 0.3, True),
+    ("fp32_d64", 1, 1500, 64, 40, 0, synth.F32, 2, 70, 90, 0.3, True),
+    ("hier_bf16", 2, 3000, 128, 150, 30, synth.BF16, 1, 130, 130, 0.15, True),
+    # non-causal: every user key visible to every query row
+    ("bf16_noncausal_B2", 2, 2048, 128, 100, 0, synth.BF16, 2, 300, 150, 0.3, False),
+    ("fp32_d64_noncausal", 1, 1500, 64, 40, 0, synth.F32, 1, 50, 20, 0.3, False),
+    # more 128-key tiles than SMs: segments cut across CTAs, multi-part merges,
+    # several pieces per CTA, ragged last query pair
+    ("bf16_multiseg", 4, 6000, 128, 150, 0, synth.BF16, 1, 600, 600, 0.4, True),
 ]
 
 
 @pytest.mark.parametrize("case", PREFILL_CASES, ids=lambda c: c[0])
 def test_prefill_lookup_and_attention(case):
     sqz = _sqz()
-    _, H, L, d, c2, c1, dt, B, n_q, n_u, ret = case
+    _, H, L, d, c2, c1, dt, B, n_q, n_u, ret, causal = case
     P = oracle_problem(H, L, d, c2, c1, dt, seed=zlib.crc32(case[0].encode()) % 1000 + 7, B=B, n_u=n_u, n_q=n_q,
                        prefill=True)
     scale = 1.0 / np.sqrt(d)
@@ -165,10 +172,10 @@ def test_prefill_lookup_and_attention(case):
     torch.cuda.synchronize()
     _check_lookup(P, sel, scale, T, T1, B)
     O, LSE = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, t["Ku"], t["Vu"], scale,
-                                  causal=True)
+                                  causal=causal)
     torch.cuda.synchronize()
     fp32 = dt == synth.F32
-    _check_attention(P, sel, O, LSE, scale, True, B, 1e-4 if fp32 else 2e-2,
+    _check_attention(P, sel, O, LSE, scale, causal, B, 1e-4 if fp32 else 2e-2,
                      None if fp32 else 5e-3)
 
 
