@@ -43,15 +43,17 @@ constexpr int KLW = 12, VLW = 14;     // K loader warps 12-13, V loader warps 14
 constexpr int NT = 512;               // 16 warps = 4 warpgroups
 constexpr int QT = 128;               // rows per query tile
 constexpr int PR = 2 * QT;            // rows per segment (query-tile pair)
-constexpr int KT = 128;               // keys per key tile
-constexpr int NKS = 3, NVS = 2;       // K / V ring stages
-constexpr int HB = 128 * 128;         // bytes of one 64-element half of a 128-row tile
-constexpr int TILE = 2 * HB;          // 128 rows x 128 bf16 = 32 KB
+constexpr int KT = 64;                // keys per key tile
+constexpr int NKS = 6, NVS = 4;       // K / V ring stages
+constexpr int HBQ = 128 * 128;        // bytes of one 64-element half of a 128-row Q tile
+constexpr int QTILE = 2 * HBQ;        // 128 rows x 128 bf16 = 32 KB
+constexpr int HBK = KT * 128;         // half of a K/V tile (64 rows x 128 B)
+constexpr int KTILE = 2 * HBK;        // 64 keys x 128 bf16 = 16 KB
 constexpr int OFF_Q = 0;              // Q0, Q1
-constexpr int OFF_K = 2 * TILE;
-constexpr int OFF_V = OFF_K + NKS * TILE;
-constexpr int OFF_BAR = OFF_V + NVS * TILE;
-constexpr int NBAR = 2 * NKS + 2 * NVS + 2 + 2 + 2 + 2;
+constexpr int OFF_K = 2 * QTILE;
+constexpr int OFF_V = OFF_K + NKS * KTILE;
+constexpr int OFF_BAR = OFF_V + NVS * KTILE;
+constexpr int NBAR = 2 * NKS + 2 * NVS + 4 + 4 + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + NBAR * 8;  // tmem addr, first segment, merges
 constexpr int BYTES = OFF_MISC + 64 + 1024;   // + alignment slack
 static_assert(BYTES <= 232448, "shared memory budget");
@@ -140,18 +142,18 @@ __device__ __forceinline__ void tmem_st32f(uint32_t taddr, const float *v) {
     tmem_st32u(taddr, u);
 }
 
-// 64 threads gather a 128-row tile into the SW128 layout.  Thread lt (0..63):
-// warp w = lt/32 copies rows 2(w + 2j) + (lane/16), j = 0..31, chunk lane%16;
-// the row's key position is held by lane 2(j%16) + (lane/16) of the same warp
-// (posA for j < 16, posB for j >= 16) and broadcast by shuffle.
+// 64 threads gather a 64-row K/V tile into the SW128 layout.  Thread lt (0..63):
+// warp w = lt/32 copies rows 2(w + 2j) + (lane/16), j = 0..15, chunk lane%16;
+// the row's key position is held by lane 2j + (lane/16) of the same warp and
+// broadcast by shuffle.
 __device__ __forceinline__ void gather_rows(uint32_t dst, const __nv_bfloat16 *fixed,
-                                            const __nv_bfloat16 *user, int posA, int posB, int lt) {
+                                            const __nv_bfloat16 *user, int pos_mine, int lt) {
     using namespace ws;
     const int w = lt >> 5, lane = lt & 31, hh = lane >> 4, c = lane & 15;
-    const uint32_t coff = (uint32_t)((c >> 3) * HB);
+    const uint32_t coff = (uint32_t)((c >> 3) * HBK);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        const int pos = __shfl_sync(FULL, j < 16 ? posA : posB, 2 * (j & 15) + hh);
+    for (int j = 0; j < KT / 4; ++j) {
+        const int pos = __shfl_sync(FULL, pos_mine, 2 * j + hh);
         const int row = 2 * (w + 2 * j) + hh;
         const bool valid = pos != INVALID;
         const __nv_bfloat16 *src = pos >= 0 ? fixed + (size_t)pos * D : user + (size_t)(-1 - pos) * D;
@@ -235,9 +237,13 @@ __global__ void __launch_bounds__(ws::NT, 1)
     unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t sbase = smem_u32(sm);
     uint64_t *bar = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
+    // s_full / p_full[2 * g + b]: S / P of group g in TMEM buffer b (tiles with
+    // tau & 1 == b).  Per buffer, so no waiter is ever two phases behind (a
+    // softmax group may finish P(t+1) before the MMA warp consumed P(t)).
     uint64_t *k_full = bar, *k_empty = bar + NKS, *v_full = bar + 2 * NKS,
              *v_empty = bar + 2 * NKS + NVS, *s_full = bar + 2 * NKS + 2 * NVS,
-             *p_full = s_full + 2, *o_done = s_full + 4, *q_full = s_full + 6, *q_empty = s_full + 7;
+             *p_full = s_full + 4, *o_done = s_full + 8, *q_full = s_full + 10, *q_empty = s_full + 11,
+             *o_fin = s_full + 12;  // o_fin[g]: the piece's last PV_g is complete (one phase per piece)
     // misc ints: [0] tmem addr, [1] first segment, [6..7] segments to merge,
     // [8..9] merge flags, [10..13] their CTA ranges; misc64[0] (bytes 48..55) start
     // tile of the first segment
@@ -307,10 +313,13 @@ __global__ void __launch_bounds__(ws::NT, 1)
             mbar_init(&v_full[s], 64);
             mbar_init(&v_empty[s], 1);
         }
-        for (int g = 0; g < 2; ++g) {
+        for (int g = 0; g < 4; ++g) {
             mbar_init(&s_full[g], 1);
             mbar_init(&p_full[g], 128);
+        }
+        for (int g = 0; g < 2; ++g) {
             mbar_init(&o_done[g], 1);
+            mbar_init(&o_fin[g], 1);
         }
         mbar_init(q_full, 1);
         mbar_init(q_empty, 1);
@@ -334,7 +343,7 @@ __global__ void __launch_bounds__(ws::NT, 1)
         const bool isK = warp < VLW;
         const int lt = tid - (isK ? KLW : VLW) * 32;  // 0..63
         const int w = lt >> 5;
-        const int rA = 2 * (w + 2 * (lane >> 1)) + (lane & 1);  // this lane's rows rA, rA + 64
+        const int rA = 2 * (w + 2 * (lane >> 1)) + (lane & 1);  // the row whose position this lane holds
         const int nst = isK ? NKS : NVS;
         uint64_t *full = isK ? k_full : v_full, *empty = isK ? k_empty : v_empty;
         const uint32_t ring = sbase + (isK ? OFF_K : OFF_V);
@@ -353,24 +362,24 @@ __global__ void __launch_bounds__(ws::NT, 1)
             };
             for (int tt = pb; tt < pe; ++tt, ++tau) {
                 const int st = tau % nst, k0 = tt * KT;
-                const int pA = pos_of(k0 + rA), pB = pos_of(k0 + rA + 64);
+                const int pA = pos_of(k0 + rA);
                 if (tau >= nst) mbar_wait(&empty[st], ((tau / nst) - 1) & 1);
                 WS_TRACE(lt == 0, tau, isK ? 10 : 11);
-                gather_rows(ring + st * TILE, Fx, Us, pA, pB, lt);
+                gather_rows(ring + st * KTILE, Fx, Us, pA, lt);
                 cp_async_mbar_arrive(&full[st]);
                 WS_TRACE(lt == 0, tau, isK ? 8 : 9);
                 if (isK && tt == pb && lt == 0) {
                     // the piece's Q pair once the previous piece's S are done (after the
                     // first K tile is in flight, so a piece switch costs one Q latency)
                     if (piece > 0) mbar_wait(q_empty, (piece - 1) & 1);
-                    mbar_arrive_expect_tx(q_full, 2 * TILE);
+                    mbar_arrive_expect_tx(q_full, 2 * QTILE);
                     WS_TRACE(true, tau, 23);
                     const int y0 = g.bh * a.n_q + g.pair * PR;
 #pragma unroll
                     for (int qg = 0; qg < 2; ++qg)
 #pragma unroll
                         for (int hf = 0; hf < 2; ++hf)
-                            tma_load_2d(sbase + OFF_Q + qg * TILE + hf * HB, &maps.q, hf * 64, y0 + qg * QT, q_full);
+                            tma_load_2d(sbase + OFF_Q + qg * QTILE + hf * HBQ, &maps.q, hf * 64, y0 + qg * QT, q_full);
                 }
             }
             ++piece;
@@ -378,7 +387,7 @@ __global__ void __launch_bounds__(ws::NT, 1)
     } else if (warp == MMAW) {
         // ======================= MMA issuer =======================
         asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
-        if ((tid & 31) == 0) {
+        {  // whole warp, converged; one elected lane issues
             auto wait_full = [&](uint64_t *b, int t, int nst) {
                 mbar_wait(&b[t % nst], (t / nst) & 1);
                 fence_async_smem();
@@ -387,24 +396,27 @@ __global__ void __launch_bounds__(ws::NT, 1)
             // descriptors: base + (byte offset >> 4) (the start-address field is the low bits)
             const uint64_t dQ = sdesc_sw128(sbase + OFF_Q, 16, 1024);
             const uint64_t dK = sdesc_sw128(sbase + OFF_K, 16, 1024);
-            const uint64_t dV = sdesc_sw128(sbase + OFF_V, HB, 1024);
+            const uint64_t dV = sdesc_sw128(sbase + OFF_V, HBK, 1024);
+            // S_g(t) -> TMEM buffer t & 1 of group g (columns g*128 + (t&1)*64)
             auto issue_S = [&](int g, int t) {
-                const uint64_t qd = dQ + (uint64_t)((g * TILE) >> 4);
-                const uint64_t kd = dK + (uint64_t)(((t % NKS) * TILE) >> 4);
+                const uint64_t qd = dQ + (uint64_t)((g * QTILE) >> 4);
+                const uint64_t kd = dK + (uint64_t)(((t % NKS) * KTILE) >> 4);
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
-                    const uint32_t off = ((ks >> 2) * HB + (ks & 3) * 32) >> 4;
-                    umma_bf16(tmem + g * 128, qd + off, kd + off, IDESC_S, ks > 0);
+                    const uint32_t qo = ((ks >> 2) * HBQ + (ks & 3) * 32) >> 4;
+                    const uint32_t ko = ((ks >> 2) * HBK + (ks & 3) * 32) >> 4;
+                    umma_bf16_w(tmem + g * 128 + (t & 1) * 64, qd + qo, kd + ko, IDESC_S, ks > 0);
                 }
-                umma_commit(&s_full[g]);
+                umma_commit_w(&s_full[2 * g + (t & 1)]);
             };
+            // O_g += P_g(t) V(t), P_g(t) bf16 in the first 32 columns of S buffer t & 1
             auto issue_PV = [&](int g, int t, bool first) {
-                const uint64_t vd = dV + (uint64_t)(((t % NVS) * TILE) >> 4);
+                const uint64_t vd = dV + (uint64_t)(((t % NVS) * KTILE) >> 4);
 #pragma unroll
                 for (int ks = 0; ks < KT / 16; ++ks)
-                    umma_bf16_ts(tmem + 256 + g * 128, tmem + g * 128 + ks * 8, vd + (ks * 2048 >> 4),
-                                 IDESC_O, (!first || ks > 0));
-                umma_commit(&o_done[g]);
+                    umma_bf16_ts_w(tmem + 256 + g * 128, tmem + g * 128 + (t & 1) * 64 + ks * 8,
+                                 vd + (ks * 2048 >> 4), IDESC_O, (!first || ks > 0));
+                umma_commit_w(&o_done[g]);
             };
             Seg g;
             int pb, pe, s_id, tau = 0, piece = 0;
@@ -412,35 +424,42 @@ __global__ void __launch_bounds__(ws::NT, 1)
                 const int n = pe - pb;
                 if (n == 0) continue;
                 mbar_wait(q_full, piece & 1);
-                WS_TRACE(true, tau, 15);
-                wait_full(k_full, tau, NKS);
-                issue_S(0, tau);
-                issue_S(1, tau);
-                umma_commit(&k_empty[tau % NKS]);
-                if (n == 1) umma_commit(q_empty);
+                WS_TRACE((tid & 31) == 0, tau, 15);
+                // S of the piece's first two tiles; afterwards S(t + 2) follows PV(t),
+                // which frees its buffer, so each softmax group always has the next S
+                // ready when it finishes a tile
+                for (int j2 = 0; j2 < 2 && j2 < n; ++j2) {
+                    wait_full(k_full, tau + j2, NKS);
+                    issue_S(0, tau + j2);
+                    issue_S(1, tau + j2);
+                    umma_commit_w(&k_empty[(tau + j2) % NKS]);
+                }
+                if (n <= 2) umma_commit_w(q_empty);
                 for (int i = 0; i < n; ++i, ++tau) {
-                    mbar_wait(&p_full[0], tau & 1);
+                    mbar_wait(&p_full[tau & 1], (tau >> 1) & 1);
                     tc_fence_after();
-                    WS_TRACE(true, tau, 4);
+                    WS_TRACE((tid & 31) == 0, tau, 4);
                     wait_full(v_full, tau, NVS);
-                    WS_TRACE(true, tau, 5);
+                    WS_TRACE((tid & 31) == 0, tau, 5);
                     issue_PV(0, tau, i == 0);
-                    WS_TRACE(true, tau, 12);
-                    if (i + 1 < n) {
-                        wait_full(k_full, tau + 1, NKS);
-                        WS_TRACE(true, tau, 6);
-                        issue_S(0, tau + 1);
-                        WS_TRACE(true, tau, 13);
+                    if (i + 1 == n) umma_commit_w(&o_fin[0]);
+                    WS_TRACE((tid & 31) == 0, tau, 12);
+                    if (i + 2 < n) {
+                        wait_full(k_full, tau + 2, NKS);
+                        WS_TRACE((tid & 31) == 0, tau, 6);
+                        issue_S(0, tau + 2);
+                        WS_TRACE((tid & 31) == 0, tau, 13);
                     }
-                    mbar_wait(&p_full[1], tau & 1);
+                    mbar_wait(&p_full[2 + (tau & 1)], (tau >> 1) & 1);
                     tc_fence_after();
-                    WS_TRACE(true, tau, 7);
+                    WS_TRACE((tid & 31) == 0, tau, 7);
                     issue_PV(1, tau, i == 0);
-                    umma_commit(&v_empty[tau % NVS]);
-                    if (i + 1 < n) {
-                        issue_S(1, tau + 1);
-                        umma_commit(&k_empty[(tau + 1) % NKS]);
-                        if (i + 2 == n) umma_commit(q_empty);
+                    if (i + 1 == n) umma_commit_w(&o_fin[1]);
+                    umma_commit_w(&v_empty[tau % NVS]);
+                    if (i + 2 < n) {
+                        issue_S(1, tau + 2);
+                        umma_commit_w(&k_empty[(tau + 2) % NKS]);
+                        if (i + 3 == n) umma_commit_w(q_empty);
                     }
                 }
                 ++piece;
@@ -454,10 +473,10 @@ __global__ void __launch_bounds__(ws::NT, 1)
         asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
         const int g = warp >> 2, r = tid & 127;  // TMEM lane = r
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t tS = tmem + g * 128 + lane_off, tO = tmem + 256 + g * 128 + lane_off;
+        const uint32_t tS0 = tmem + g * 128 + lane_off, tO = tmem + 256 + g * 128 + lane_off;
         const float sl2 = a.scale * LOG2E;
         Seg sg;
-        int pb, pe, s_id, tau = 0;
+        int pb, pe, s_id, tau = 0, piece = 0;
         while (walk.next(a, sg, pb, pe, s_id)) {
             const int trow = sg.pair * PR + g * QT + r;
             const bool row_ok = trow < a.n_q;
@@ -485,9 +504,10 @@ __global__ void __launch_bounds__(ws::NT, 1)
             float m_used = -INFINITY, l = 0.f;
             for (int tt = pb; tt < pe; ++tt, ++tau) {
                 const int k0 = tt * KT;
-                mbar_wait(&s_full[g], tau & 1);
+                mbar_wait(&s_full[2 * g + (tau & 1)], (tau >> 1) & 1);
                 tc_fence_after();
                 WS_TRACE(r == 0, tau, 2 * g);
+                const uint32_t tS = tS0 + (tau & 1) * 64;
                 float sv[KT];
 #pragma unroll
                 for (int cc = 0; cc < KT / 32; ++cc)
@@ -559,16 +579,18 @@ __global__ void __launch_bounds__(ws::NT, 1)
                 const float2 accs = fadd2(acc2[0], acc2[1]);
                 l += accs.x + accs.y;
                 WS_TRACE(r == 0 && g == 0, tau, 17);
-                tmem_st32f(tS, sv);            // P columns 0..31
-                tmem_st32f(tS + 32, sv + 32);  // P columns 32..63
+                tmem_st32f(tS, sv);            // P: columns 0..31 of the S buffer
                 tmem_wait_st();
                 WS_TRACE(r == 0 && g == 0, tau, 18);
                 tc_fence_before();
-                mbar_arrive(&p_full[g]);
+                mbar_arrive(&p_full[2 * g + (tau & 1)]);
                 WS_TRACE(r == 0, tau, 2 * g + 1);
             }
             // ---- the piece's result for the row: final, or a partial to merge ----
-            mbar_wait(&o_done[g], (tau - 1) & 1);
+            // (o_done alone is ambiguous here: with S issued two tiles ahead, PV(last-1)
+            // may still be pending, two phases behind)
+            mbar_wait(&o_fin[g], piece & 1);
+            ++piece;
             tc_fence_after();
             const int c0 = owner_of(walk.seg_st, T, G), c1 = owner_of(walk.seg_st + sg.tiles - 1, T, G);
             const bool have = row_ok && l > 0.f;
