@@ -39,7 +39,7 @@ namespace sqz {
 namespace ws {
 constexpr int D = 128;
 constexpr int MMAW = 8;               // MMA warp index (warps 9-11 idle in the main loop)
-constexpr int KLW = 12, VLW = 14;     // K loader warps 12-13, V loader warps 14-15
+constexpr int NWK = 4, NWV = 2;       // K loader warps 9, 10, 12, 13; V loader warps 14, 15
 constexpr int NT = 512;               // 16 warps = 4 warpgroups
 constexpr int QT = 128;               // rows per query tile
 constexpr int PR = 2 * QT;            // rows per segment (query-tile pair)
@@ -142,19 +142,20 @@ __device__ __forceinline__ void tmem_st32f(uint32_t taddr, const float *v) {
     tmem_st32u(taddr, u);
 }
 
-// 64 threads gather a 64-row K/V tile into the SW128 layout.  Thread lt (0..63):
-// warp w = lt/32 copies rows 2(w + 2j) + (lane/16), j = 0..15, chunk lane%16;
-// the row's key position is held by lane 2j + (lane/16) of the same warp and
+// NW warps gather a 64-row K/V tile into the SW128 layout.  Warp w (0..NW-1)
+// copies rows 2(w + NW j) + (lane/16), j < 32/NW, 16-byte chunk lane%16; the
+// row's key position is held by lane 2j + (lane/16) of the same warp and
 // broadcast by shuffle.
+template <int NW>
 __device__ __forceinline__ void gather_rows(uint32_t dst, const __nv_bfloat16 *fixed,
-                                            const __nv_bfloat16 *user, int pos_mine, int lt) {
+                                            const __nv_bfloat16 *user, int pos_mine, int w, int lane) {
     using namespace ws;
-    const int w = lt >> 5, lane = lt & 31, hh = lane >> 4, c = lane & 15;
+    const int hh = lane >> 4, c = lane & 15;
     const uint32_t coff = (uint32_t)((c >> 3) * HBK);
 #pragma unroll
-    for (int j = 0; j < KT / 4; ++j) {
+    for (int j = 0; j < KT / (2 * NW); ++j) {
         const int pos = __shfl_sync(FULL, pos_mine, 2 * j + hh);
-        const int row = 2 * (w + 2 * j) + hh;
+        const int row = 2 * (w + NW * j) + hh;
         const bool valid = pos != INVALID;
         const __nv_bfloat16 *src = pos >= 0 ? fixed + (size_t)pos * D : user + (size_t)(-1 - pos) * D;
         cp_async16_zfill(dst + coff + sw128_off(row, c & 7), valid ? src + c * 8 : fixed, valid);
@@ -306,11 +307,11 @@ __global__ void __launch_bounds__(ws::NT, 1)
     if (warp == 0) tmem_alloc(reinterpret_cast<uint32_t *>(&misc[0]), 512);
     if (tid == 0) {
         for (int s = 0; s < NKS; ++s) {
-            mbar_init(&k_full[s], 64);
+            mbar_init(&k_full[s], 32 * NWK);
             mbar_init(&k_empty[s], 1);
         }
         for (int s = 0; s < NVS; ++s) {
-            mbar_init(&v_full[s], 64);
+            mbar_init(&v_full[s], 32 * NWV);
             mbar_init(&v_empty[s], 1);
         }
         for (int g = 0; g < 4; ++g) {
@@ -333,17 +334,19 @@ __global__ void __launch_bounds__(ws::NT, 1)
     PieceWalk walk{misc[1], nseg, npairs, c, G, misc64[0], lo, hi, T, 0};
     WS_TRACE(tid == 0, 0, 20);
 
-    if (warp >= KLW) {
+    const int kw = warp == 9 ? 0 : warp == 10 ? 1 : (warp == 12 || warp == 13) ? warp - 10 : -1;
+    const int vw = warp >= 14 ? warp - 14 : -1;
+    if (kw >= 0 || vw >= 0) {
         // ======================= loaders =======================
         // K/V rows gathered by key position with 16-byte cp.async (a TMA gather4
-        // moves only 512 B per instruction and measured ~3x slower here); the Q
-        // pair is two contiguous 128-row tiles and comes by TMA
+        // moves only 512 B per instruction and measured ~3x slower here; LDGSTS
+        // issue is per-warp latency bound, hence 4 K warps); the Q pair is two
+        // contiguous 128-row tiles and comes by TMA
         asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
         const int lane = tid & 31;
-        const bool isK = warp < VLW;
-        const int lt = tid - (isK ? KLW : VLW) * 32;  // 0..63
-        const int w = lt >> 5;
-        const int rA = 2 * (w + 2 * (lane >> 1)) + (lane & 1);  // the row whose position this lane holds
+        const bool isK = kw >= 0;
+        const int w = isK ? kw : vw, nwl = isK ? NWK : NWV;
+        const int rA = 2 * (w + nwl * (lane >> 1)) + (lane & 1);  // the row whose position this lane holds
         const int nst = isK ? NKS : NVS;
         uint64_t *full = isK ? k_full : v_full, *empty = isK ? k_empty : v_empty;
         const uint32_t ring = sbase + (isK ? OFF_K : OFF_V);
@@ -364,11 +367,14 @@ __global__ void __launch_bounds__(ws::NT, 1)
                 const int st = tau % nst, k0 = tt * KT;
                 const int pA = pos_of(k0 + rA);
                 if (tau >= nst) mbar_wait(&empty[st], ((tau / nst) - 1) & 1);
-                WS_TRACE(lt == 0, tau, isK ? 10 : 11);
-                gather_rows(ring + st * KTILE, Fx, Us, pA, lt);
+                WS_TRACE(w == 0 && lane == 0, tau, isK ? 10 : 11);
+                if (isK)
+                    gather_rows<NWK>(ring + st * KTILE, Fx, Us, pA, w, lane);
+                else
+                    gather_rows<NWV>(ring + st * KTILE, Fx, Us, pA, w, lane);
                 cp_async_mbar_arrive(&full[st]);
-                WS_TRACE(lt == 0, tau, isK ? 8 : 9);
-                if (isK && tt == pb && lt == 0) {
+                WS_TRACE(w == 0 && lane == 0, tau, isK ? 8 : 9);
+                if (isK && tt == pb && w == 0 && lane == 0) {
                     // the piece's Q pair once the previous piece's S are done (after the
                     // first K tile is in flight, so a piece switch costs one Q latency)
                     if (piece > 0) mbar_wait(q_empty, (piece - 1) & 1);
@@ -401,21 +407,14 @@ __global__ void __launch_bounds__(ws::NT, 1)
             auto issue_S = [&](int g, int t) {
                 const uint64_t qd = dQ + (uint64_t)((g * QTILE) >> 4);
                 const uint64_t kd = dK + (uint64_t)(((t % NKS) * KTILE) >> 4);
-#pragma unroll
-                for (int ks = 0; ks < D / 16; ++ks) {
-                    const uint32_t qo = ((ks >> 2) * HBQ + (ks & 3) * 32) >> 4;
-                    const uint32_t ko = ((ks >> 2) * HBK + (ks & 3) * 32) >> 4;
-                    umma_bf16_w(tmem + g * 128 + (t & 1) * 64, qd + qo, kd + ko, IDESC_S, ks > 0);
-                }
+                umma_S8_w<(HBQ >> 4), (HBK >> 4)>(tmem + g * 128 + (t & 1) * 64, qd, kd, IDESC_S);
                 umma_commit_w(&s_full[2 * g + (t & 1)]);
             };
             // O_g += P_g(t) V(t), P_g(t) bf16 in the first 32 columns of S buffer t & 1
+            static_assert(KT == 64, "umma_PV4_w covers 4 K16 steps");
             auto issue_PV = [&](int g, int t, bool first) {
                 const uint64_t vd = dV + (uint64_t)(((t % NVS) * KTILE) >> 4);
-#pragma unroll
-                for (int ks = 0; ks < KT / 16; ++ks)
-                    umma_bf16_ts_w(tmem + 256 + g * 128, tmem + g * 128 + (t & 1) * 64 + ks * 8,
-                                 vd + (ks * 2048 >> 4), IDESC_O, (!first || ks > 0));
+                umma_PV4_w(tmem + 256 + g * 128, tmem + g * 128 + (t & 1) * 64, vd, IDESC_O, !first);
                 umma_commit_w(&o_done[g]);
             };
             Seg g;
@@ -467,7 +466,7 @@ __global__ void __launch_bounds__(ws::NT, 1)
         }
         __syncwarp();
     } else if (warp > MMAW) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");  // idle warps 9-11
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");  // idle warp 11
     } else {
         // ======================= softmax groups =======================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");

@@ -102,6 +102,51 @@ __device__ __forceinline__ void umma_commit_w(uint64_t *bar) {
             smem_u32(bar))
         : "memory");
 }
+// One S tile: 8 K16-steps of SS MMA (K = 128) in a single elect-predicated block.
+// a/b K-step offsets in descriptor units (bytes >> 4): steps 0-3 +0,2,4,6 within a
+// 64-element half, steps 4-7 the same plus the half stride (A_HALF / B_HALF).
+template <int A_HALF, int B_HALF>
+__device__ __forceinline__ void umma_S8_w(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred e, f, t;\n\t.reg .b64 a, b;\n\t"
+        "setp.ne.b32 f, 0, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n\t"
+        "add.s64 a, %1, 2;\n\tadd.s64 b, %2, 2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, 4;\n\tadd.s64 b, %2, 4;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, 6;\n\tadd.s64 b, %2, 6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, %4;\n\tadd.s64 b, %2, %5;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, %4 + 2;\n\tadd.s64 b, %2, %5 + 2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, %4 + 4;\n\tadd.s64 b, %2, %5 + 4;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, %1, %4 + 6;\n\tadd.s64 b, %2, %5 + 6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t}" ::"r"(d_tmem),
+        "l"(a0), "l"(b0), "r"(idesc), "n"(A_HALF), "n"(B_HALF)
+        : "memory");
+}
+// One PV tile of 64 keys: 4 K16-steps, A (P, bf16x2) from TMEM columns +0,8,16,24,
+// B (V, MN-major) descriptor +0,128,256,384 (2048-byte steps); accumulate unless first
+__device__ __forceinline__ void umma_PV4_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b0, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+        "add.s32 a, %1, 8;\n\tadd.s64 b, %2, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.s32 a, %1, 16;\n\tadd.s64 b, %2, 256;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.s32 a, %1, 24;\n\tadd.s64 b, %2, 384;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b0), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 // arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
     asm volatile(
