@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
     if verbose:
         for o in objs:
             sys.stdout.write(open(o + ".log").read())
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcuda"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", OUT, *objs])
     return OUT
 
 
