@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQZ_ABI_VERSION 1
+#define SQZ_ABI_VERSION 2
 
 enum {
     SQZ_OK = 0,
@@ -48,6 +48,7 @@ enum {
     SQZ_ERR_FORMAT = 3,      /* malformed index tables                                   */
     SQZ_ERR_INVARIANT = 4,   /* tables violate sum N = L, perm not a permutation, ...    */
     SQZ_ERR_CUDA = 5,        /* a CUDA runtime call failed (message has the CUDA error)  */
+    SQZ_ERR_NCCL = 6,        /* NCCL missing or a collective failed (message has why)     */
     SQZ_ERR_EMPTY = 7,       /* a final (non-partial) output row attended no key         */
     SQZ_ERR_UNSUPPORTED = 8  /* valid but not supported by this build (e.g. d not 64/128) */
 };
@@ -74,7 +75,15 @@ typedef enum { SQZ_F32 = 0, SQZ_BF16 = 1 } sqz_dtype;
  *   C1         [H, c1, d]   dtype             Level-1 centroids (levels == 2)
  *   N1         [H, c1]      int32             descendant keys of each Level-1 cluster (R4)
  *   child_off  [H, c1 + 1]  int32             Level-2 children ranges (levels == 2)
- * Single level: levels = 1, c1 = 0, C1/N1/child_off = NULL. */
+ * Single level: levels = 1, c1 = 0, C1/N1/child_off = NULL.
+ *
+ * Fixed-context shards (cluster sharding across GPUs): a shard
+ * index (sqz_shard_plan + sqz_index_shard) holds a subset of the clusters of
+ * every head.  Then L_total = the global keys per head (perm values index the
+ * ORIGINAL key space [0, L_total)), L = the shard's row capacity of Kp/Vp/perm
+ * (>= its keys in every head), and sum_i N2[h][i] = key_off[h][c2] <= L; rows
+ * past key_off[h][c2] are padding that no call reads.  L_total = 0 means an
+ * unsharded index (L_total == L, sum N2 = L). */
 typedef struct {
     int32_t H;       /* heads                                  */
     int32_t d;       /* head dimension: 64 or 128              */
@@ -90,6 +99,7 @@ typedef struct {
     int32_t *N2;
     int32_t *key_off;
     int32_t *perm;
+    int64_t L_total; /* 0: unsharded; else global keys per head (see above) */
 } sqz_index;
 
 /* ---------------------------------------------------------------------- */
@@ -140,6 +150,13 @@ typedef struct {
     float scale; /* logit scale s_i = scale * q.C_i; 1/sqrt(d) default (R1)          */
     float T;     /* global threshold (finest level), T >= 0; T == 0 selects all (R6)  */
     float T1;    /* Level-1 threshold (levels == 2), T1 >= 0                         */
+    void *comm;  /* NULL: idx is the whole fixed context.  Else an sqz_comm (see    */
+                 /* "Multi-GPU") whose ranks each hold one shard of it: the lookup  */
+                 /* exchanges the per-query (m, D) statistics of every level with   */
+                 /* an all-gather so each rank thresholds against the GLOBAL Eq. 1  */
+                 /* / Eq. 3 denominator and selects exactly the clusters the        */
+                 /* unsharded lookup selects among its own (the workspace must then */
+                 /* be sized by sqz_lookup_workspace_comm).                         */
 } sqz_lookup_params;
 
 /* Outputs of the lookup, caller-allocated device memory.
@@ -182,6 +199,28 @@ int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t 
                         const sqz_lookup_params *p, const sqz_selection *out, void *ws,
                         size_t ws_bytes, void *stream);
 
+/* Staged form of the lookup, for fixed-context shards with a caller-driven
+ * exchange (what sqz_centroid_lookup runs internally when p->comm is set).
+ * A level's statistics are, per query row (b, h, t), the pair (m, D) with
+ * m = max_i s_i and D = sum_i N_i exp(s_i - m) over the rows this shard scans
+ * at that level (m = -inf, D = 0 if none); the global denominator of Eq. 1 /
+ * Eq. 3 is the fold of the shards' pairs, LSE_w = log sum_r D_r e^{m_r}.
+ *   stage 0:        scan the first level (Level 1, or the single level),
+ *                   write its statistics to stats_out [B, H, n_q, 2] fp32.
+ *   stage k >= 1:   stats_in [P, B, H, n_q, 2] = the statistics of level k
+ *                   from all P shards in rank order (P = 1: this shard only,
+ *                   equal to the unsharded lookup); fold them in rank order,
+ *                   threshold level k (writing `out` when k == levels), and if
+ *                   k < levels scan level k + 1 over the children of the
+ *                   surviving clusters, writing its statistics to stats_out.
+ * Stages 0 .. levels must run in order on one workspace (p->comm ignored);
+ * the exchange between them is the caller's (sqz_comm_allgather_stats, NCCL,
+ * or, in tests, a device copy). */
+int sqz_centroid_lookup_stage(const sqz_index *idx, const void *Q, int32_t B, int32_t n_q,
+                              const sqz_lookup_params *p, int32_t stage, int32_t P,
+                              const float *stats_in, float *stats_out, const sqz_selection *out,
+                              void *ws, size_t ws_bytes, void *stream);
+
 /* ---------------------------------------------------------------------- */
 /* Online step 2: sparse attention (section 4.2)                  */
 /* ---------------------------------------------------------------------- */
@@ -221,6 +260,75 @@ int sqz_attention_status(void *ws, size_t ws_bytes, void *stream);
  *   LSE = log sum_p exp(LSE_p), O = sum_p exp(LSE_p - LSE) O_p. */
 int sqz_merge_partials(int32_t P, const float *O_parts, const float *LSE_parts, int64_t rows,
                        int32_t d, void *O, float *LSE, int32_t out_dtype, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Multi-GPU: fixed-context sharding by cluster (the paper is    */
+/* single-GPU, so this is this build's addition)                     */
+/* ---------------------------------------------------------------------- */
+/* Plan of one rank's shard, computed on the HOST from host copies of the
+ * index's integer tables (no GPU needed).  Ownership: Level-1 cluster p (or,
+ * single level, cluster i) belongs to rank p mod world ("interleaved", so
+ * jointly selected neighbouring clusters spread over the ranks); a Level-1
+ * cluster's children and every cluster's keys stay with it.  Local ids keep
+ * the global order.
+ *   key_off   [H, c2 + 1] host int32 of the full index; child_off [H, c1 + 1]
+ *             host int32 (levels == 2) else NULL.
+ *   plan->c1, c2, L   out: local table rows / key row capacity (max over
+ *             heads; padding rows have N = 0 and empty ranges)
+ *   The array fields are optional HOST outputs (NULL = skip; call once with
+ *   all NULL to size them):
+ *   c1_src [H, c1] global Level-1 id of local row      N1 [H, c1], child_off [H, c1 + 1]
+ *   c2_src [H, c2] global Level-2 id, -1 = padding     N2 [H, c2], key_off [H, c2 + 1]
+ *   key_src [H, L] global cluster-major position of local key row, -1 = padding
+ * Errors: SQZ_ERR_INVALID_ARG (world < 1, rank out of range, fewer clusters
+ * than ranks at the sharded level, inconsistent tables). */
+typedef struct {
+    int32_t c1, c2;
+    int64_t L;
+    int32_t *c1_src, *c2_src, *key_src;
+    int32_t *N1, *child_off, *N2, *key_off;
+} sqz_shard_plan;
+
+int sqz_shard_plan_compute(int32_t H, int32_t levels, int32_t c1, int32_t c2, int64_t L,
+                           const int32_t *key_off, const int32_t *child_off, int32_t rank,
+                           int32_t world, sqz_shard_plan *plan);
+
+/* Builds the shard index on the device from the full one:
+ *   full, Kp, Vp: the full index and its cluster-major K/V (device)
+ *   c1_src, c2_src, key_src: the plan's arrays copied to the DEVICE
+ *   local: geometry (H, d, levels, dtype, c1, c2, L = plan's, L_total =
+ *          full->L) and device tables; the caller uploads N1, child_off, N2,
+ *          key_off from the plan; this call writes C1, C2 (rows gathered,
+ *          padding = 0), perm (gathered, padding = -1), Kp_local, Vp_local
+ *          [H, L, d] (padding rows = 0).  Asynchronous on `stream`. */
+int sqz_index_shard(const sqz_index *full, const void *Kp, const void *Vp, const int32_t *c1_src,
+                    const int32_t *c2_src, const int32_t *key_src, const sqz_index *local,
+                    void *Kp_local, void *Vp_local, void *stream);
+
+/* Communicator over the ranks holding the shards (one process per GPU).  The
+ * library resolves NCCL at run time (the copy already loaded in the process,
+ * e.g. torch's, else libnccl.so.2); without it these calls return
+ * SQZ_ERR_NCCL.  Rank 0 creates the id and the caller broadcasts its 128
+ * bytes (e.g. with torch.distributed); every rank then calls sqz_comm_init
+ * with the CUDA device it will use current.  Blocking (collective). */
+int sqz_comm_unique_id(uint8_t id[128]);
+int sqz_comm_init(const uint8_t id[128], int32_t rank, int32_t world, void **comm);
+int sqz_comm_destroy(void *comm);
+
+/* Workspace of sqz_centroid_lookup with p->comm set (world ranks). */
+int sqz_lookup_workspace_comm(const sqz_index *idx, int32_t B, int32_t n_q, int32_t world,
+                              size_t *ws_bytes);
+
+/* Output exchange (P:361-363 across GPUs): every rank passes its partial
+ * (O_part [rows, d] fp32, LSE_part [rows] fp32; -inf = identity) from
+ * sqz_sparse_attention(partial = 1, out_dtype = SQZ_F32); the partials are
+ * all-gathered over NVLink (NCCL) into ws and merged in rank order, so every
+ * rank ends with the same O [rows, d] out_dtype and LSE [rows].  ws:
+ * sqz_comm_merge_workspace bytes.  Asynchronous on `stream`. */
+int sqz_comm_merge_workspace(int32_t world, int64_t rows, int32_t d, size_t *ws_bytes);
+int sqz_comm_allgather_merge(void *comm, const float *O_part, const float *LSE_part, int64_t rows,
+                             int32_t d, void *O, float *LSE, int32_t out_dtype, void *ws,
+                             size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Misc                                                                      */

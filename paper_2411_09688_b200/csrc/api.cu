@@ -23,6 +23,17 @@ int fail(int code, const char *fmt, ...) {
     va_end(ap);
     return code;
 }
+}  // namespace
+
+int sqz::set_error(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+namespace {
 int cuda_fail(cudaError_t e, const char *what) {
     return fail(SQZ_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
@@ -55,6 +66,9 @@ int check_index(const sqz_index *idx, bool need_tables) {
                     (long long)idx->L);
     if (idx->levels == 2 && (idx->c1 < 1 || idx->c1 > idx->c2))
         return fail(SQZ_ERR_INVALID_ARG, "idx->c1 = %d must be in [1, c2=%d]", idx->c1, idx->c2);
+    if (idx->L_total < 0 || idx->L_total > 0x7fffffffLL)
+        return fail(SQZ_ERR_INVALID_ARG, "idx->L_total = %lld out of range [0, 2^31)",
+                    (long long)idx->L_total);
     if (need_tables) {
         if (!idx->C2 || !idx->N2 || !idx->key_off)
             return fail(SQZ_ERR_INVALID_ARG, "idx->C2 / N2 / key_off must be non-NULL");
@@ -71,10 +85,11 @@ int check_index(const sqz_index *idx, bool need_tables) {
 // ---------------- lookup workspace ----------------
 struct LookupWs {
     LevelArgs l1, l2;
+    float2 *send, *recv;  // comm mode: this rank's statistics, the gathered [world] ones
     size_t bytes;
 };
 
-LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base) {
+LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base, int world = 0) {
     Carve cv{base};
     const int64_t BH = (int64_t)B * idx->H;
     const int CHR = lookup_chunk_rows();
@@ -87,6 +102,7 @@ LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base) {
         const int nch = (c + CHR - 1) / CHR;
         lv.tick = cv.take<int32_t>(BH);
         lv.sel_pref = cv.take<int32_t>(BH * c);
+        lv.gstat = cv.take<float2>(BH * n_q);
         if (prefill) {
             lv.rowlse = cv.take<float>(BH * n_q);
             lv.colpart = cv.take<float>((size_t)nqt * BH * c);
@@ -102,6 +118,11 @@ LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base) {
         w.l1.n_list = cv.take<int32_t>(BH);
         w.l1.exp_list = cv.take<int32_t>(BH * idx->c2);
         w.l1.n_exp = cv.take<int32_t>(BH);
+    }
+    w.send = w.recv = nullptr;
+    if (world > 0) {
+        w.send = cv.take<float2>(BH * n_q);
+        w.recv = cv.take<float2>((size_t)world * BH * n_q);
     }
     w.bytes = cv.used + 256;
     return w;
@@ -176,6 +197,8 @@ int sqz_cluster_keys(const void *K, const void *V, const int64_t *init2, const i
     if (!K || !V || !Kp || !Vp) return fail(SQZ_ERR_INVALID_ARG, "K, V, Kp, Vp must be non-NULL");
     if (!aligned16(K) || !aligned16(V) || !aligned16(Kp) || !aligned16(Vp))
         return fail(SQZ_ERR_INVALID_ARG, "K, V, Kp, Vp must be 16-byte aligned");
+    if (idx->L_total != 0)
+        return fail(SQZ_ERR_INVALID_ARG, "sqz_cluster_keys builds a full index: L_total must be 0");
     if (!init2) return fail(SQZ_ERR_INVALID_ARG, "init2 is NULL");
     if (idx->levels == 2 && !init1) return fail(SQZ_ERR_INVALID_ARG, "init1 is NULL (levels=2)");
     if (!idx->perm) return fail(SQZ_ERR_INVALID_ARG, "idx->perm is NULL");
@@ -217,9 +240,8 @@ int sqz_lookup_workspace(const sqz_index *idx, int32_t B, int32_t n_q, size_t *w
     return SQZ_OK;
 }
 
-int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t n_q,
-                        const sqz_lookup_params *p, const sqz_selection *out, void *ws,
-                        size_t ws_bytes, void *stream) {
+static int lookup_check(const sqz_index *idx, const void *Q, int32_t B, int32_t n_q,
+                        const sqz_lookup_params *p, const sqz_selection *out, const void *ws) {
     int rc = check_index(idx, true);
     if (rc) return rc;
     if (!Q) return fail(SQZ_ERR_INVALID_ARG, "Q is NULL");
@@ -234,12 +256,12 @@ int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t 
     if (!out || !out->clusters || !out->n_clusters || !out->n_keys || !out->key_idx)
         return fail(SQZ_ERR_INVALID_ARG, "selection outputs clusters/n_clusters/n_keys/key_idx required");
     if (!ws) return fail(SQZ_ERR_INVALID_ARG, "ws is NULL");
-    LookupWs w = lookup_carve(idx, B, n_q, align_ws(ws));
-    if (ws_bytes < w.bytes + 256)
-        return fail(SQZ_ERR_INVALID_ARG, "ws_bytes = %zu < required %zu", ws_bytes, w.bytes + 256);
+    return SQZ_OK;
+}
 
-    LookupShape s{B, idx->H, n_q, idx->d, idx->dtype, p->scale};
-    cudaStream_t st = (cudaStream_t)stream;
+// wires the level arguments of the carved workspace to the index and outputs
+static void lookup_levels(const sqz_index *idx, const sqz_lookup_params *p, const sqz_selection *out,
+                          LookupWs &w) {
     LevelArgs &l2 = w.l2;
     l2.C = idx->C2;
     l2.N = idx->N2;
@@ -263,15 +285,109 @@ int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t 
         l1.exp_stride = idx->c2;
         l1.bitmap = out->l1_surv;
         l1.dbg_S = out->dbg_S1;
-        cudaError_t e = launch_lookup_level(s, Q, l1, st);
-        if (e != cudaSuccess) return cuda_fail(e, "lookup level 1");
         l2.rows = l1.exp_list;
         l2.n_rows = l1.n_exp;
         l2.row_stride = idx->c2;
     }
-    cudaError_t e = launch_lookup_level(s, Q, l2, st);
+}
+
+// one stage of the staged lookup (see sqz_centroid_lookup_stage)
+static int run_stage(const sqz_index *idx, const LookupShape &s, const void *Q, LookupWs &w, int stage,
+                     int P, const float2 *stats_in, float2 *stats_out, cudaStream_t st) {
+    const int levels = idx->levels;
+    const int64_t n = (int64_t)s.B * s.H * s.n_q;
+    const bool prefill = s.n_q > 1;
+    auto level = [&](int k) -> LevelArgs & { return (levels == 2 && k == 1) ? w.l1 : w.l2; };
+    cudaError_t e;
+    if (stage > 0) {
+        LevelArgs &lv = level(stage);
+        e = launch_fold_stats(P, stats_in, n, const_cast<float2 *>(lv.gstat),
+                              prefill ? lv.rowlse : nullptr, st);
+        if (e != cudaSuccess) return cuda_fail(e, "stats fold");
+        if (prefill && lv.dbg_lse) {
+            e = cudaMemcpyAsync(lv.dbg_lse, lv.rowlse, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_fail(e, "dbg_lse copy");
+        }
+        lv.phase = 2;
+        e = launch_lookup_level(s, Q, lv, st);
+        if (e != cudaSuccess) return cuda_fail(e, "lookup select");
+    }
+    if (stage < levels) {
+        LevelArgs &nx = level(stage + 1);
+        nx.phase = 1;
+        nx.stats_out = stats_out;
+        e = launch_lookup_level(s, Q, nx, st);
+        if (e != cudaSuccess) return cuda_fail(e, "lookup statistics");
+    }
+    return SQZ_OK;
+}
+
+int sqz_lookup_workspace_comm(const sqz_index *idx, int32_t B, int32_t n_q, int32_t world,
+                              size_t *ws_bytes) {
+    int rc = check_index(idx, false);
+    if (rc) return rc;
+    if (B < 1 || n_q < 1 || world < 1)
+        return fail(SQZ_ERR_INVALID_ARG, "B = %d, n_q = %d, world = %d must be >= 1", B, n_q, world);
+    if (!ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes is NULL");
+    *ws_bytes = lookup_carve(idx, B, n_q, nullptr, world).bytes + 256;
+    return SQZ_OK;
+}
+
+int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t n_q,
+                        const sqz_lookup_params *p, const sqz_selection *out, void *ws,
+                        size_t ws_bytes, void *stream) {
+    int rc = lookup_check(idx, Q, B, n_q, p, out, ws);
+    if (rc) return rc;
+    const int world = p->comm ? comm_world(p->comm) : 0;
+    LookupWs w = lookup_carve(idx, B, n_q, align_ws(ws), world);
+    if (ws_bytes < w.bytes + 256)
+        return fail(SQZ_ERR_INVALID_ARG, "ws_bytes = %zu < required %zu%s", ws_bytes, w.bytes + 256,
+                    world ? " (size it with sqz_lookup_workspace_comm)" : "");
+    LookupShape s{B, idx->H, n_q, idx->d, idx->dtype, p->scale};
+    cudaStream_t st = (cudaStream_t)stream;
+    lookup_levels(idx, p, out, w);
+    if (world) {
+        // sharded: stats -> all-gather -> fold + select, once per level
+        const size_t cnt = (size_t)B * idx->H * n_q * 2;
+        for (int stage = 0; stage <= idx->levels; ++stage) {
+            rc = run_stage(idx, s, Q, w, stage, world, w.recv, w.send, st);
+            if (rc) return rc;
+            if (stage < idx->levels) {
+                rc = comm_allgather_f32(p->comm, reinterpret_cast<const float *>(w.send),
+                                        reinterpret_cast<float *>(w.recv), cnt, st);
+                if (rc) return rc;
+            }
+        }
+        return SQZ_OK;
+    }
+    if (idx->levels == 2) {
+        cudaError_t e = launch_lookup_level(s, Q, w.l1, st);
+        if (e != cudaSuccess) return cuda_fail(e, "lookup level 1");
+    }
+    cudaError_t e = launch_lookup_level(s, Q, w.l2, st);
     if (e != cudaSuccess) return cuda_fail(e, "lookup level 2");
     return SQZ_OK;
+}
+
+int sqz_centroid_lookup_stage(const sqz_index *idx, const void *Q, int32_t B, int32_t n_q,
+                              const sqz_lookup_params *p, int32_t stage, int32_t P,
+                              const float *stats_in, float *stats_out, const sqz_selection *out,
+                              void *ws, size_t ws_bytes, void *stream) {
+    int rc = lookup_check(idx, Q, B, n_q, p, out, ws);
+    if (rc) return rc;
+    if (stage < 0 || stage > idx->levels)
+        return fail(SQZ_ERR_INVALID_ARG, "stage = %d must be in [0, levels=%d]", stage, idx->levels);
+    if (stage > 0 && (P < 1 || !stats_in))
+        return fail(SQZ_ERR_INVALID_ARG, "stage %d needs P >= 1 and stats_in", stage);
+    if (stage < idx->levels && !stats_out)
+        return fail(SQZ_ERR_INVALID_ARG, "stage %d needs stats_out", stage);
+    LookupWs w = lookup_carve(idx, B, n_q, align_ws(ws));
+    if (ws_bytes < w.bytes + 256)
+        return fail(SQZ_ERR_INVALID_ARG, "ws_bytes = %zu < required %zu", ws_bytes, w.bytes + 256);
+    LookupShape s{B, idx->H, n_q, idx->d, idx->dtype, p->scale};
+    lookup_levels(idx, p, out, w);
+    return run_stage(idx, s, Q, w, stage, P, reinterpret_cast<const float2 *>(stats_in),
+                     reinterpret_cast<float2 *>(stats_out), (cudaStream_t)stream);
 }
 
 // ------------------------------------------------------------------ attention

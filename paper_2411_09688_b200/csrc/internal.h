@@ -8,6 +8,12 @@
 
 namespace sqz {
 
+// api.cu: records the thread-local sqz_last_error() message; returns `code`
+int set_error(int code, const char *fmt, ...);
+// dist.cu: communicator helpers (comm = sqz_comm_init handle)
+int comm_world(void *comm);
+int comm_allgather_f32(void *comm, const float *send, float *recv, size_t count, cudaStream_t st);
+
 // One lookup level (Eq. 1 single level, or Eq. 2 / Eq. 3 of the hierarchy).
 struct LevelArgs {
     const void *C;        // [H, c, d] centroid table of this level
@@ -35,6 +41,12 @@ struct LevelArgs {
     uint8_t *bitmap;      // optional [B,H,c]
     float *dbg_S;         // optional [B,H,c]
     float *dbg_lse;       // optional [B,H,n_q]
+    // staged lookup over fixed-context shards (sqz_centroid_lookup_stage)
+    int32_t phase;        // 0: scan + threshold; 1: scan -> stats_out only; 2: threshold
+                          //    with the folded global statistics gstat (decode reuses the
+                          //    logits phase 1 stored, prefill recomputes them)
+    float2 *stats_out;    // [B,H,n_q] (m, D) of this shard's rows        (phase 1)
+    const float2 *gstat;  // [B,H,n_q] (M, log D) folded over the shards  (phase 2)
 };
 
 struct LookupShape {
@@ -45,6 +57,10 @@ struct LookupShape {
 // lookup.cu
 cudaError_t launch_lookup_level(const LookupShape &s, const void *Q, const LevelArgs &lv,
                                 cudaStream_t st);
+// fold of P shards' (m, D) statistics in rank order -> (M, log D); also
+// M + log D into rowlse when non-null (prefill)
+cudaError_t launch_fold_stats(int P, const float2 *stats_in, int64_t n, float2 *gstat,
+                              float *rowlse, cudaStream_t st);
 int lookup_chunk_rows();
 int lookup_qtile();
 
@@ -85,5 +101,11 @@ int cluster_keys(const void *K, const void *V, const int64_t *init2, const int64
 size_t validate_workspace_bytes(const sqz_index &idx);
 int index_validate(const sqz_index &idx, void *ws, size_t ws_bytes, cudaStream_t st, char *err,
                    size_t errlen);
+
+// shard.cu: gathers of the shard index rows
+cudaError_t launch_shard_gather(const sqz_index &full, const void *Kp, const void *Vp,
+                                const int32_t *c1_src, const int32_t *c2_src,
+                                const int32_t *key_src, const sqz_index &local, void *Kp_loc,
+                                void *Vp_loc, cudaStream_t st);
 
 }  // namespace sqz

@@ -642,18 +642,21 @@ __global__ void k_validate(sqz_index idx, int32_t *__restrict__ hist, int *__res
     const int h = blockIdx.y;
     const int c2 = idx.c2;
     const int64_t L = idx.L;
+    // a shard (L_total > 0) holds key_off[c2] <= L keys of the L_total original ones
+    const int64_t Lt = idx.L_total > 0 ? idx.L_total : L;
     const int32_t *N2 = idx.N2 + (size_t)h * c2;
     const int32_t *ko = idx.key_off + (size_t)h * (c2 + 1);
+    const int64_t nkeys = min((int64_t)ko[c2], L);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c2; i += gridDim.x * blockDim.x) {
         if (N2[i] < 0 || ko[i + 1] - ko[i] != N2[i]) atomicOr(bad, 1);
         if (i == 0 && ko[0] != 0) atomicOr(bad, 1);
-        if (i == c2 - 1 && ko[c2] != L) atomicOr(bad, 1);
+        if (i == c2 - 1 && (idx.L_total > 0 ? ko[c2] > L : ko[c2] != L)) atomicOr(bad, 1);
     }
     const int32_t *pm = idx.perm + (size_t)h * L;
-    for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < L; j += gridDim.x * blockDim.x) {
+    for (int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nkeys; j += gridDim.x * blockDim.x) {
         const int32_t v = pm[j];
-        if (v < 0 || v >= L) atomicOr(bad, 2);
-        else atomicAdd(hist + (size_t)h * L + v, 1);
+        if (v < 0 || v >= Lt) atomicOr(bad, 2);
+        else atomicAdd(hist + (size_t)h * Lt + v, 1);
     }
     if (idx.levels == 2) {
         const int c1 = idx.c1;
@@ -662,20 +665,22 @@ __global__ void k_validate(sqz_index idx, int32_t *__restrict__ hist, int *__res
         for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < c1; p += gridDim.x * blockDim.x) {
             if (co[p + 1] < co[p] || co[p] < 0 || co[p + 1] > c2) { atomicOr(bad, 4); continue; }
             if (p == 0 && co[0] != 0) atomicOr(bad, 4);
-            if (p == c1 - 1 && co[c1] != c2) atomicOr(bad, 4);
+            if (p == c1 - 1 && (idx.L_total > 0 ? co[c1] > c2 : co[c1] != c2)) atomicOr(bad, 4);
             long long s = 0;
             for (int l = co[p]; l < co[p + 1]; ++l) s += N2[l];
             if (s != N1[p]) atomicOr(bad, 8);
         }
     }
 }
-__global__ void k_validate_hist(const int32_t *__restrict__ hist, int64_t n, int *__restrict__ bad) {
+// every original key exactly once (a shard: at most once)
+__global__ void k_validate_hist(const int32_t *__restrict__ hist, int64_t n, int shard,
+                                int *__restrict__ bad) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-        if (hist[j] != 1) atomicOr(bad, 2);
+        if (shard ? hist[j] > 1 : hist[j] != 1) atomicOr(bad, 2);
 }
 
 size_t validate_workspace_bytes(const sqz_index &idx) {
-    return sizeof(int32_t) * ((size_t)idx.H * idx.L + 64);
+    return sizeof(int32_t) * ((size_t)idx.H * (idx.L_total > 0 ? idx.L_total : idx.L) + 64);
 }
 
 int index_validate(const sqz_index &idx, void *ws, size_t ws_bytes, cudaStream_t st, char *err,
@@ -689,7 +694,8 @@ int index_validate(const sqz_index &idx, void *ws, size_t ws_bytes, cudaStream_t
     CK(cudaMemsetAsync(ws, 0, validate_workspace_bytes(idx), st));
     dim3 g(std::max(1, (int)std::min<int64_t>(1024, (idx.L + 255) / 256)), idx.H);
     k_validate<<<g, 256, 0, st>>>(idx, hist, bad);
-    k_validate_hist<<<1024, 256, 0, st>>>(hist, (int64_t)idx.H * idx.L, bad);
+    k_validate_hist<<<1024, 256, 0, st>>>(hist, (int64_t)idx.H * (idx.L_total > 0 ? idx.L_total : idx.L),
+                                          idx.L_total > 0, bad);
     CK(cudaGetLastError());
     int hb = 0;
     CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -239,6 +239,26 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
             lv.dbg_S[((size_t)b0 * H + h) * c + r] = NAN;
     }
 
+    const int phase = lv.phase;
+    if (phase == 2) {
+        // ---- staged select: the logits and row metadata phase 1 stored, and the
+        // (M, log D) folded over every shard ----
+        for (int rr = tid; rr < nloc; rr += NT) {
+            const int row = ROWLIST ? ldcg(rows + r0 + rr) : r0 + rr;
+            s_row[rr] = row;
+            s_Nw[rr] = (float)__ldg(N + row);
+            s_o0[rr] = __ldg(off + row);
+            s_o1[rr] = __ldg(off + row + 1);
+            for (int i = 0; i < nb; ++i)
+                s_log[i * rpc + rr] = ldcg(lv.logits + ((size_t)(b0 + i) * H + h) * c + r0 + rr);
+        }
+        if (tid < nb) {
+            const float2 g2 = ldcg(lv.gstat + (size_t)(b0 + tid) * H + h);
+            s_M[tid] = g2.x;
+            s_lD[tid] = g2.y;
+            if (rank == 0 && lv.dbg_lse) lv.dbg_lse[(size_t)(b0 + tid) * H + h] = g2.x + g2.y;
+        }
+    } else {
     // ---- scan: logits of the CTA's rows for the NB queries ----
     float q[NB][D / 32];
 #pragma unroll
@@ -296,6 +316,10 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
         }
     }
     __syncthreads();
+    if (phase == 1)  // keep the logits for the phase-2 threshold
+        for (int i = 0; i < nb; ++i)
+            for (int rr = tid; rr < nloc; rr += NT)
+                lv.logits[((size_t)(b0 + i) * H + h) * c + r0 + rr] = s_log[i * rpc + rr];
     SQZ_TRACE_AT(g_trace_look, 1);
     // (m, D) of the CTA's rows per query: block max, then one exp per row.
     for (int i = 0; i < nb; ++i) {
@@ -340,9 +364,18 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
         if (lane == 0) {
             s_M[i] = mm;
             s_lD[i] = logf(dd);
-            if (rank == 0 && lv.dbg_lse) lv.dbg_lse[(size_t)(b0 + i) * H + h] = mm + logf(dd);
+            if (phase == 1) {
+                if (rank == 0) lv.stats_out[(size_t)(b0 + i) * H + h] = make_float2(mm, dd);
+            } else if (rank == 0 && lv.dbg_lse) {
+                lv.dbg_lse[(size_t)(b0 + i) * H + h] = mm + logf(dd);
+            }
         }
     }
+    if (phase == 1) {  // statistics only; keep smem alive for the other ranks' reads
+        cluster.sync();
+        return;
+    }
+    }  // phase != 2
     __syncthreads();
     // ---- threshold + ordered compaction of the CTA's rows ----
     const bool all = !(lv.T > 0.f);
@@ -424,6 +457,32 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
 
 SQZ_TRACE_EXPORT(g_trace_look, sqz_trace_look)
 
+// --------------------------------------------------------------------------
+// Fold of the shards' (m, D) statistics, sequentially in rank order (every
+// rank folds the same gathered array, so all ranks get identical bits).
+// --------------------------------------------------------------------------
+__global__ void k_fold_stats(int P, const float2 *__restrict__ in, int64_t n, float2 *__restrict__ g,
+                             float *__restrict__ rowlse) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        float m = -INFINITY, D = 0.f;
+        for (int p = 0; p < P; ++p) {
+            const float2 v = in[(size_t)p * n + j];
+            md_combine(m, D, v.x, v.y);
+        }
+        const float lD = logf(D);  // -inf when no shard scanned a row
+        g[j] = make_float2(m, lD);
+        if (rowlse) rowlse[j] = m + lD;
+    }
+}
+
+cudaError_t launch_fold_stats(int P, const float2 *stats_in, int64_t n, float2 *gstat, float *rowlse,
+                              cudaStream_t st) {
+    const int blocks = (int)std::min<int64_t>(1024, (n + 255) / 256);
+    k_fold_stats<<<std::max(blocks, 1), 256, 0, st>>>(P, stats_in, n, gstat, rowlse);
+    return cudaGetLastError();
+}
+
 static size_t decode_smem_bytes(int NB, int rpc) { return (size_t)rpc * 4 * (NB + 4 + 4 * NB) + 16; }
 
 // --------------------------------------------------------------------------
@@ -466,7 +525,9 @@ __global__ void __launch_bounds__(NT) k_prefill_rowlse(LookupShape s, const T *_
         md_combine(m, Dsum, sv, (float)N[row]);
     }
     const int t = t0 + myq;
-    if ((lane & 3) == 0 && t < s.n_q) {
+    if ((lane & 3) == 0 && t < s.n_q && lv.phase == 1) {
+        lv.stats_out[(size_t)bh * s.n_q + t] = make_float2(m, Dsum);
+    } else if ((lane & 3) == 0 && t < s.n_q) {
         const float lse = m + logf(Dsum);  // -inf when no row
         lv.rowlse[(size_t)bh * s.n_q + t] = lse;
         if (lv.dbg_lse) lv.dbg_lse[(size_t)bh * s.n_q + t] = lse;
@@ -595,35 +656,40 @@ static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelAr
 }
 
 // --------------------------------------------------------------------------
-// Prefill lookup on the 5th-generation tensor cores (bf16): one CTA per
-// (128-query tile, b*h).  The centroid rows of the (candidate) row space are
-// streamed in 128-row tiles (cp.async gather into the 128B-swizzled operand
-// layout, double-buffered); S = Q C^T is one 128x128x(d) tcgen05.mma chain per
-// tile into TMEM (two S buffers, so the next tile's MMA overlaps this tile's
-// epilogue).  Pass 1 (tiles 0..n-1): thread = query row keeps the online
-// (m, D = sum N e^(s-m)) -> LSE_t.  Pass 2 (recomputes S, as the
-// paper's kernel does): p = e^(s - LSE_t), column sums over the tile's
-// 128 rows by a transposed butterfly (31 shuffles per 32 columns) and a
-// fixed-order sum over the 4 warps -- deterministic fp32, no float atomics.
-// The last CTA of each (b,h) averages the tiles and thresholds S-bar > T.
+// Prefill lookup on the 5th-generation tensor cores (bf16): one CTA of 8 warps
+// per (128-query tile, b*h).  The centroid rows of the (candidate) row space
+// are streamed in 128-row tiles (cp.async gather into the 128B-swizzled
+// operand layout, double-buffered), and every tile is multiplied twice
+// (the paper's kernel also recomputes the scores):
+//   pass 1: S = Q C^T (M = queries): thread = query row, the online
+//           (m, D = sum N e^(s-m)) over its half of the columns, the two halves
+//           folded in fixed order -> LSE_t;
+//   pass 2: S^T = C Q^T (M = centroids): thread = centroid row, so the column
+//           sum S-bar_i = sum_t e^(s_ti - LSE_t) is a per-thread sum over its
+//           half of the queries (4 interleaved fp32 accumulators, fixed order)
+//           -- no shuffles, no float atomics, deterministic (numerics rule 4).
+// Both MMAs read the same two K-major smem tiles; only the operand roles swap.
+// The last CTA of each (b,h) averages the q-tile partials and thresholds.
 // --------------------------------------------------------------------------
-constexpr int PL_T = 128;  // query rows per CTA = centroid rows per tile
+constexpr int PL_T = 128;   // query rows per CTA = centroid rows per tile
+constexpr int PL_NT = 256;  // 8 warps: (TMEM lane quarter) x (column half)
 
 template <int D> struct PlSmem {
     static constexpr int TILE = PL_T * D * 2;
     static constexpr int Q = 0;
-    static constexpr int C0 = Q + TILE;           // 2 buffers
-    static constexpr int NW = C0 + 2 * TILE;      // float [2][128] N weights
-    static constexpr int RID = NW + 2 * PL_T * 4; // int [2][128] row ids
-    static constexpr int COLS = RID + 2 * PL_T * 4;  // float [4][128] warp column sums
-    static constexpr int MISC = COLS + 4 * PL_T * 4;
+    static constexpr int C0 = Q + TILE;              // 2 buffers
+    static constexpr int NW = C0 + 2 * TILE;         // float [2][128] N weights
+    static constexpr int RID = NW + 2 * PL_T * 4;    // int [2][128] row ids
+    static constexpr int LSE = RID + 2 * PL_T * 4;   // float [128] LSE_t of the q tile
+    static constexpr int HALF = LSE + PL_T * 4;      // float2 [2][128] per-half partials
+    static constexpr int MISC = HALF + 2 * PL_T * 8;
     static constexpr int BYTES = MISC + 64 + 1024;
 };
 
 template <int D, bool ROWLIST>
-__global__ void __launch_bounds__(PL_T, 1) k_prefill_lookup_tc(LookupShape s,
-                                                                const __nv_bfloat16 *__restrict__ Q,
-                                                                LevelArgs lv) {
+__global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
+                                                                 const __nv_bfloat16 *__restrict__ Q,
+                                                                 LevelArgs lv) {
     using SM = PlSmem<D>;
     constexpr int CPR = D * 2 / 16;
     constexpr int HB = PL_T * 128;
@@ -633,13 +699,16 @@ __global__ void __launch_bounds__(PL_T, 1) k_prefill_lookup_tc(LookupShape s,
     const uint32_t sbase = smem_u32(sm);
     float *s_nw = reinterpret_cast<float *>(sm + SM::NW);
     int *s_rid = reinterpret_cast<int *>(sm + SM::RID);
-    float *s_cols = reinterpret_cast<float *>(sm + SM::COLS);
+    float *s_lse = reinterpret_cast<float *>(sm + SM::LSE);
+    float2 *s_half = reinterpret_cast<float2 *>(sm + SM::HALF);
     uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + SM::MISC);
     uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sm + SM::MISC + 16);
     __shared__ int s_last;
 
     asm volatile("griddepcontrol.launch_dependents;");
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int quarter = warp & 3, hf = warp >> 2;  // TMEM lanes [32q, +32), columns [64hf, +64)
+    const int r = quarter * 32 + lane;              // TMEM lane = M row of this thread
     const int qt = blockIdx.x, bh = blockIdx.y, h = bh % s.H;
     const int t0 = qt * PL_T, c = lv.c;
     const __nv_bfloat16 *C = reinterpret_cast<const __nv_bfloat16 *>(lv.C) + (size_t)h * c * D;
@@ -658,69 +727,85 @@ __global__ void __launch_bounds__(PL_T, 1) k_prefill_lookup_tc(LookupShape s,
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *s_tmem;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
 
     // Q tile (rows beyond n_q are zero)
     const __nv_bfloat16 *Qb = Q + ((size_t)bh * s.n_q + t0) * D;
-    for (int e = tid; e < PL_T * CPR; e += PL_T) {
-        const int r = e / CPR, cc = e % CPR;
-        const bool valid = t0 + r < s.n_q;
-        cp_async16_zfill(sbase + SM::Q + (cc >> 3) * HB + sw128_off(r, cc & 7),
-                         Qb + (size_t)(valid ? r : 0) * D + cc * 8, valid);
+    for (int e = tid; e < PL_T * CPR; e += PL_NT) {
+        const int rr = e / CPR, cc = e % CPR;
+        const bool valid = t0 + rr < s.n_q;
+        cp_async16_zfill(sbase + SM::Q + (cc >> 3) * HB + sw128_off(rr, cc & 7),
+                         Qb + (size_t)(valid ? rr : 0) * D + cc * 8, valid);
     }
-    // the row id / N weight of column `tid` of tile `tl`
-    auto col_meta = [&](int tl, int &rid, float &nw) {
-        const int j = tl * PL_T + tid;
+    // row id / N weight of column j of tile tl (threads 0..127)
+    auto col_meta = [&](int tl, int j, int &rid, float &nw) {
+        const int jj = tl * PL_T + j;
         rid = -1;
         nw = 0.f;
-        if (j < nrows) {
-            rid = ROWLIST ? ldcg(rows + j) : j;
+        if (jj < nrows) {
+            rid = ROWLIST ? ldcg(rows + jj) : jj;
             nw = (float)__ldg(N + rid);
         }
     };
     auto issue_tile = [&](int buf) {
-        for (int e = tid; e < PL_T * CPR; e += PL_T) {
-            const int r = e / CPR, cc = e % CPR;
-            const int rid = s_rid[buf * PL_T + r];
-            cp_async16_zfill(sbase + SM::C0 + buf * SM::TILE + (cc >> 3) * HB + sw128_off(r, cc & 7),
+        for (int e = tid; e < PL_T * CPR; e += PL_NT) {
+            const int rr = e / CPR, cc = e % CPR;
+            const int rid = s_rid[buf * PL_T + rr];
+            cp_async16_zfill(sbase + SM::C0 + buf * SM::TILE + (cc >> 3) * HB + sw128_off(rr, cc & 7),
                              C + (size_t)(rid >= 0 ? rid : 0) * D + cc * 8, rid >= 0);
         }
     };
-    const int total = 2 * ntile;  // pass 1 then pass 2 over the same tiles
-    {
+    // pass 1 then pass 2 over the same tiles; the staged lookup runs them as
+    // separate launches (phase 1: pass 1 only; phase 2: pass 2 only, with the
+    // LSE folded over the shards)
+    const int first = lv.phase == 2 ? ntile : 0;
+    const int total = lv.phase == 1 ? ntile : 2 * ntile;
+    if (tid < PL_T) {
         int rid;
         float nw;
-        col_meta(0, rid, nw);
+        col_meta(0, tid, rid, nw);
         s_rid[tid] = rid;
         s_nw[tid] = nw;
     }
+    const bool row_ok = t0 + r < s.n_q;  // pass 1: this thread's query row
+    if (tid < PL_T) {
+        float lse = INFINITY;
+        if (lv.phase == 2 && t0 + tid < s.n_q) {
+            const float2 g2 = ldcg(lv.gstat + (size_t)bh * s.n_q + t0 + tid);
+            lse = g2.x + g2.y;
+            if (lv.dbg_lse) lv.dbg_lse[(size_t)bh * s.n_q + t0 + tid] = lse;
+            if (!(lse < INFINITY) || lse == -INFINITY) lse = INFINITY;  // no row: p = 0
+        }
+        s_lse[tid] = lse;
+    }
     __syncthreads();
-    if (total > 0) issue_tile(0);
+    if (total > first) issue_tile(0);
     cp_async_commit_grp();
 
-    const bool row_ok = t0 + tid < s.n_q;
-    float m = -INFINITY, Dsum = 0.f, lse = INFINITY;
-    for (int it = 0; it < total; ++it) {
-        const int buf = it & 1, tl = it % ntile, pass = it / ntile;
+    float m = -INFINITY, Dsum = 0.f;
+    for (int it = first; it < total; ++it) {
+        const int buf = (it - first) & 1, tl = it % ntile, pass = it / ntile;
         int rid_n = -1;
         float nw_n = 0.f;
-        if (it + 1 < total) col_meta((it + 1) % ntile, rid_n, nw_n);
+        if (it + 1 < total && tid < PL_T) col_meta((it + 1) % ntile, tid, rid_n, nw_n);
         cp_async_wait_all();
         fence_async_smem();
         tc_fence_before();
         __syncthreads();
         if (tid == 0) {
             tc_fence_after();
+            const uint32_t qa = sbase + SM::Q, ca = sbase + SM::C0 + buf * SM::TILE;
+            const uint32_t a_base = pass == 0 ? qa : ca, b_base = pass == 0 ? ca : qa;
 #pragma unroll
             for (int ks = 0; ks < D / 16; ++ks) {
                 const uint32_t off = (ks >> 2) * HB + (ks & 3) * 32;
-                umma_bf16(tmem + buf * 128, sdesc_sw128(sbase + SM::Q + off, 16, 1024),
-                          sdesc_sw128(sbase + SM::C0 + buf * SM::TILE + off, 16, 1024), IDESC, ks > 0);
+                umma_bf16(tmem + buf * 128, sdesc_sw128(a_base + off, 16, 1024),
+                          sdesc_sw128(b_base + off, 16, 1024), IDESC, ks > 0);
             }
             umma_commit(&mbar[buf]);
         }
         // next tile into the other buffer (its MMA, it - 1, completed before the last epilogue)
-        if (it + 1 < total) {
+        if (it + 1 < total && tid < PL_T) {
             s_rid[(buf ^ 1) * PL_T + tid] = rid_n;
             s_nw[(buf ^ 1) * PL_T + tid] = nw_n;
         }
@@ -728,61 +813,94 @@ __global__ void __launch_bounds__(PL_T, 1) k_prefill_lookup_tc(LookupShape s,
         if (it + 1 < total) issue_tile(buf ^ 1);
         cp_async_commit_grp();
 
-        mbar_wait(&mbar[buf], (it >> 1) & 1);
+        mbar_wait(&mbar[buf], ((it - first) >> 1) & 1);
         tc_fence_after();
         const float *nwb = s_nw + buf * PL_T;
+        if (pass == 0) {
+            // thread = query row r; columns = centroids hf*64 + [0, 64) of tile tl
 #pragma unroll 1
-        for (int ch = 0; ch < PL_T / 32; ++ch) {
-            float v[32];
-            tmem_ld32(tmem + buf * 128 + lane_off + ch * 32, v);
-            tmem_wait_ld();
-            if (pass == 0) {
+            for (int ch = 0; ch < 2; ++ch) {
+                const int col0 = hf * 64 + ch * 32;
+                float v[32];
+                tmem_ld32(tmem + buf * 128 + lane_off + col0, v);
+                tmem_wait_ld();
                 float cmx = -INFINITY;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    const bool valid = tl * PL_T + ch * 32 + j < nrows;
+                    const bool valid = tl * PL_T + col0 + j < nrows;
                     v[j] = valid ? v[j] * s.scale : -INFINITY;
                     cmx = fmaxf(cmx, v[j]);
                 }
                 const float mn = fmaxf(m, cmx);
                 if (mn != -INFINITY) {
-                    float acc = Dsum * expf(m - mn);
+                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) acc = fmaf(nwb[ch * 32 + j], expf(v[j] - mn), acc);
-                    Dsum = acc;
+                    for (int j = 0; j < 32; j += 4) {
+                        a0 = fmaf(nwb[col0 + j], expf(v[j] - mn), a0);
+                        a1 = fmaf(nwb[col0 + j + 1], expf(v[j + 1] - mn), a1);
+                        a2 = fmaf(nwb[col0 + j + 2], expf(v[j + 2] - mn), a2);
+                        a3 = fmaf(nwb[col0 + j + 3], expf(v[j + 3] - mn), a3);
+                    }
+                    Dsum = Dsum * expf(m - mn) + ((a0 + a1) + (a2 + a3));
                     m = mn;
                 }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const bool valid = row_ok && tl * PL_T + ch * 32 + j < nrows;
-                    v[j] = valid ? expf(v[j] * s.scale - lse) : 0.f;
+            }
+            if (tl == ntile - 1) {  // fold the two column halves of each query row
+                s_half[hf * PL_T + r] = make_float2(m, Dsum);
+                __syncthreads();
+                if (tid < PL_T) {
+                    const float2 h0 = s_half[tid], h1 = s_half[PL_T + tid];
+                    float mm = h0.x, dd = h0.y;
+                    md_combine(mm, dd, h1.x, h1.y);
+                    const bool ok = t0 + tid < s.n_q;
+                    if (lv.phase == 1) {
+                        if (ok) lv.stats_out[(size_t)bh * s.n_q + t0 + tid] = make_float2(mm, dd);
+                    } else {
+                        float lse = mm + logf(dd);  // -inf when no row
+                        if (ok) {
+                            lv.rowlse[(size_t)bh * s.n_q + t0 + tid] = lse;
+                            if (lv.dbg_lse) lv.dbg_lse[(size_t)bh * s.n_q + t0 + tid] = lse;
+                        }
+                        if (!ok || !(lse < INFINITY) || lse == -INFINITY) lse = INFINITY;
+                        s_lse[tid] = lse;
+                    }
                 }
-                const float colsum = transpose_reduce<32>(v, lane);  // lane = column
-                s_cols[warp * PL_T + ch * 32 + lane] = colsum;
+                // s_lse is read after the next iteration's __syncthreads
             }
-        }
-        if (pass == 0 && tl == ntile - 1) {  // LSE_t of this thread's query row
-            lse = row_ok ? m + logf(Dsum) : INFINITY;
-            if (row_ok) {
-                lv.rowlse[(size_t)bh * s.n_q + t0 + tid] = lse;
-                if (lv.dbg_lse) lv.dbg_lse[(size_t)bh * s.n_q + t0 + tid] = lse;
+        } else {
+            // S^T: thread = centroid row r of tile tl; columns = queries hf*64 + [0, 64)
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 1
+            for (int ch = 0; ch < 2; ++ch) {
+                const int col0 = hf * 64 + ch * 32;
+                float v[32];
+                tmem_ld32(tmem + buf * 128 + lane_off + col0, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    a0 += expf(fmaf(v[j], s.scale, -s_lse[col0 + j]));
+                    a1 += expf(fmaf(v[j + 1], s.scale, -s_lse[col0 + j + 1]));
+                    a2 += expf(fmaf(v[j + 2], s.scale, -s_lse[col0 + j + 2]));
+                    a3 += expf(fmaf(v[j + 3], s.scale, -s_lse[col0 + j + 3]));
+                }
             }
-            if (!(lse < INFINITY) || lse == -INFINITY) lse = INFINITY;  // no row: p = 0
-        }
-        if (pass == 1) {
+            s_half[hf * PL_T + r].x = (a0 + a1) + (a2 + a3);
             __syncthreads();
-            const int rid = s_rid[buf * PL_T + tid];
-            if (rid >= 0) {
-                const float acc = s_cols[tid] + s_cols[PL_T + tid] + s_cols[2 * PL_T + tid] +
-                                  s_cols[3 * PL_T + tid];
-                lv.colpart[((size_t)qt * s.B * s.H + bh) * c + rid] = acc;
+            if (tid < PL_T) {
+                const int rid = s_rid[buf * PL_T + tid];
+                if (rid >= 0)
+                    lv.colpart[((size_t)qt * s.B * s.H + bh) * c + rid] = s_half[tid].x + s_half[PL_T + tid].x;
             }
         }
         tc_fence_before();
     }
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, 256);
+    if (lv.phase == 1) {
+        if (ntile == 0 && tid < PL_T && t0 + tid < s.n_q)  // no rows: the identity statistics
+            lv.stats_out[(size_t)bh * s.n_q + t0 + tid] = make_float2(-INFINITY, 0.f);
+        return;
+    }
     // ---- the last CTA of this (b,h) averages the tiles and thresholds ----
     __threadfence();
     __syncthreads();
@@ -799,7 +917,18 @@ __global__ void __launch_bounds__(PL_T, 1) k_prefill_lookup_tc(LookupShape s,
     const float inv_nq = 1.0f / (float)s.n_q;
     finalize_rows<ROWLIST>(lv, bh, h, nrows, [&](int row, float &dbg) {
         float acc = 0.f;
-        for (int t = 0; t < nqt; ++t) acc += ldcg(lv.colpart + ((size_t)t * s.B * s.H + bh) * c + row);
+        const float *cp = lv.colpart + (size_t)bh * c + row;
+        const size_t stride = (size_t)s.B * s.H * c;
+        int t = 0;
+        for (; t + 4 <= nqt; t += 4) {  // independent loads, summed in tile order
+            const float x0 = ldcg(cp + t * stride), x1 = ldcg(cp + (t + 1) * stride);
+            const float x2 = ldcg(cp + (t + 2) * stride), x3 = ldcg(cp + (t + 3) * stride);
+            acc += x0;
+            acc += x1;
+            acc += x2;
+            acc += x3;
+        }
+        for (; t < nqt; ++t) acc += ldcg(cp + t * stride);
         const float Sbar = acc * inv_nq;
         dbg = Sbar;
         return all || (Sbar > lv.T);
@@ -818,7 +947,7 @@ static cudaError_t launch_prefill_tc(const LookupShape &s, const __nv_bfloat16 *
         set = true;
     }
     dim3 grid((s.n_q + PL_T - 1) / PL_T, s.B * s.H);
-    kern<<<grid, PL_T, PlSmem<D>::BYTES, st>>>(s, Q, lv);
+    kern<<<grid, PL_NT, PlSmem<D>::BYTES, st>>>(s, Q, lv);
     return cudaGetLastError();
 }
 
@@ -845,12 +974,14 @@ static cudaError_t launch_level_t(const LookupShape &s, const T *Q, const LevelA
     const int nqt = (s.n_q + QT - 1) / QT;
     dim3 g1(nqt, s.B * s.H);
     dim3 g2(nch, nqt, s.B * s.H);
+    // staged: phase 1 = row statistics only, phase 2 = column sums against the
+    // folded LSE (written into lv.rowlse by the fold)
     if (rl) {
-        k_prefill_rowlse<T, D, true><<<g1, NT, 0, st>>>(s, Q, lv);
-        k_prefill_colsum<T, D, true><<<g2, NT, 0, st>>>(s, Q, lv);
+        if (lv.phase != 2) k_prefill_rowlse<T, D, true><<<g1, NT, 0, st>>>(s, Q, lv);
+        if (lv.phase != 1) k_prefill_colsum<T, D, true><<<g2, NT, 0, st>>>(s, Q, lv);
     } else {
-        k_prefill_rowlse<T, D, false><<<g1, NT, 0, st>>>(s, Q, lv);
-        k_prefill_colsum<T, D, false><<<g2, NT, 0, st>>>(s, Q, lv);
+        if (lv.phase != 2) k_prefill_rowlse<T, D, false><<<g1, NT, 0, st>>>(s, Q, lv);
+        if (lv.phase != 1) k_prefill_colsum<T, D, false><<<g2, NT, 0, st>>>(s, Q, lv);
     }
     return cudaGetLastError();
 }

@@ -24,14 +24,17 @@ SO = os.path.join(HERE, "libsqz.so")
 
 SQZ_F32, SQZ_BF16 = 0, 1
 SQZ_OK, SQZ_ERR_INVALID_ARG, SQZ_ERR_FORMAT, SQZ_ERR_INVARIANT = 0, 2, 3, 4
-SQZ_ERR_CUDA, SQZ_ERR_EMPTY, SQZ_ERR_UNSUPPORTED = 5, 7, 8
+SQZ_ERR_CUDA, SQZ_ERR_NCCL, SQZ_ERR_EMPTY, SQZ_ERR_UNSUPPORTED = 5, 6, 7, 8
+ABI_VERSION = 2
 
 EXPORTS = [
     "sqz_cluster_keys_workspace", "sqz_cluster_keys", "sqz_index_validate_workspace",
     "sqz_index_validate", "sqz_lookup_workspace", "sqz_centroid_lookup",
     "sqz_attention_workspace", "sqz_sparse_attention", "sqz_attention_status",
     "sqz_merge_partials", "sqz_workspace_init", "sqz_last_error", "sqz_abi_version",
-    "sqz_device_check",
+    "sqz_device_check", "sqz_centroid_lookup_stage", "sqz_shard_plan_compute", "sqz_index_shard",
+    "sqz_comm_unique_id", "sqz_comm_init", "sqz_comm_destroy", "sqz_lookup_workspace_comm",
+    "sqz_comm_merge_workspace", "sqz_comm_allgather_merge",
 ]
 
 
@@ -40,7 +43,14 @@ class sqz_index(ctypes.Structure):
                 ("levels", ctypes.c_int32), ("c1", ctypes.c_int32), ("c2", ctypes.c_int32),
                 ("dtype", ctypes.c_int32), ("C1", ctypes.c_void_p), ("N1", ctypes.c_void_p),
                 ("child_off", ctypes.c_void_p), ("C2", ctypes.c_void_p), ("N2", ctypes.c_void_p),
-                ("key_off", ctypes.c_void_p), ("perm", ctypes.c_void_p)]
+                ("key_off", ctypes.c_void_p), ("perm", ctypes.c_void_p),
+                ("L_total", ctypes.c_int64)]
+
+
+class sqz_shard_plan(ctypes.Structure):
+    _fields_ = [("c1", ctypes.c_int32), ("c2", ctypes.c_int32), ("L", ctypes.c_int64)] + [
+        (n, ctypes.c_void_p) for n in ("c1_src", "c2_src", "key_src", "N1", "child_off", "N2",
+                                       "key_off")]
 
 
 class sqz_kmeans_params(ctypes.Structure):
@@ -48,7 +58,8 @@ class sqz_kmeans_params(ctypes.Structure):
 
 
 class sqz_lookup_params(ctypes.Structure):
-    _fields_ = [("scale", ctypes.c_float), ("T", ctypes.c_float), ("T1", ctypes.c_float)]
+    _fields_ = [("scale", ctypes.c_float), ("T", ctypes.c_float), ("T1", ctypes.c_float),
+                ("comm", ctypes.c_void_p)]
 
 
 class sqz_selection(ctypes.Structure):
@@ -99,6 +110,21 @@ def lib():
         L.sqz_attention_status.argtypes = [vp, sz, vp]
         L.sqz_merge_partials.argtypes = [i32, vp, vp, i64, i32, vp, vp, i32, vp]
         L.sqz_workspace_init.argtypes = [vp, sz, vp]
+        L.sqz_centroid_lookup_stage.argtypes = [ip, vp, i32, i32, ctypes.POINTER(sqz_lookup_params),
+                                                i32, i32, vp, vp, ctypes.POINTER(sqz_selection), vp,
+                                                sz, vp]
+        L.sqz_shard_plan_compute.argtypes = [i32, i32, i32, i32, i64, vp, vp, i32, i32,
+                                             ctypes.POINTER(sqz_shard_plan)]
+        L.sqz_index_shard.argtypes = [ip, vp, vp, vp, vp, vp, ip, vp, vp, vp]
+        L.sqz_comm_unique_id.argtypes = [ctypes.c_char_p]
+        L.sqz_comm_init.argtypes = [ctypes.c_char_p, i32, i32, ctypes.POINTER(ctypes.c_void_p)]
+        L.sqz_comm_destroy.argtypes = [vp]
+        L.sqz_lookup_workspace_comm.argtypes = [ip, i32, i32, i32, szp]
+        L.sqz_comm_merge_workspace.argtypes = [i32, i64, i32, szp]
+        L.sqz_comm_allgather_merge.argtypes = [vp, vp, vp, i64, i32, vp, vp, i32, vp, sz, vp]
+        if L.sqz_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"{SO} has ABI {L.sqz_abi_version()}, binding expects {ABI_VERSION}: "
+                               "rebuild with __graft_entry__.build()")
         for n in EXPORTS:
             getattr(L, n).restype = ctypes.c_char_p if n == "sqz_last_error" else ctypes.c_int
         _lib = L
@@ -160,6 +186,8 @@ class Index:
     C1: torch.Tensor = None
     N1: torch.Tensor = None
     child_off: torch.Tensor = None
+    L_total: int = 0          # > 0: a fixed-context shard (see shard_index)
+    c2_src: torch.Tensor = None  # shard: global Level-2 id of each local row (-1 = padding)
 
     @property
     def levels(self):
@@ -172,6 +200,7 @@ class Index:
         for f in ("C1", "N1", "child_off", "C2", "N2", "key_off", "perm"):
             t = getattr(self, f)
             setattr(s, f, None if t is None else t.data_ptr())
+        s.L_total = self.L_total
         return s
 
     @staticmethod
@@ -282,16 +311,25 @@ def attention_workspace_bytes(idx: Index, B, n_q, n_u):
 
 
 def centroid_lookup(idx: Index, Q: torch.Tensor, scale: float, T: float, T1: float = 0.0,
-                    sel: Selection = None, ws: torch.Tensor = None, debug=False) -> Selection:
-    """sqz_centroid_lookup on Q[B,H,n_q,d]."""
+                    sel: Selection = None, ws: torch.Tensor = None, debug=False,
+                    comm: "Comm" = None) -> Selection:
+    """sqz_centroid_lookup on Q[B,H,n_q,d].  `comm`: idx is this rank's
+    fixed-context shard; the lookup exchanges the per-level statistics."""
     B, H, n_q, d = Q.shape
     if sel is None:
         sel = Selection.empty(idx, B, n_q, debug, Q.device)
     s = idx.struct()
     if ws is None:
-        ws = _WS.get(("lookup", Q.device, idx.H, idx.L, idx.c1, idx.c2, B, n_q),
-                     lookup_workspace_bytes(idx, B, n_q), Q.device)
-    p = sqz_lookup_params(scale, T, T1)
+        if comm is None:
+            nb = lookup_workspace_bytes(idx, B, n_q)
+        else:
+            nbc = ctypes.c_size_t(0)
+            _check(lib().sqz_lookup_workspace_comm(ctypes.byref(s), B, n_q, comm.world,
+                                                   ctypes.byref(nbc)))
+            nb = nbc.value
+        ws = _WS.get(("lookup", Q.device, idx.H, idx.L, idx.c1, idx.c2, B, n_q,
+                      0 if comm is None else comm.world), nb, Q.device)
+    p = sqz_lookup_params(scale, T, T1, None if comm is None else comm.handle)
     ss = sel.struct()
     _check(lib().sqz_centroid_lookup(ctypes.byref(s), _p(Q), B, n_q, ctypes.byref(p),
                                      ctypes.byref(ss), _p(ws), ws.numel(), _stream()))
@@ -344,3 +382,127 @@ def merge_partials(O_parts: torch.Tensor, LSE_parts: torch.Tensor, out_dtype=SQZ
 
 def device_check():
     _check(lib().sqz_device_check())
+
+
+# --------------------------------------------------------------------------
+# multi-GPU: fixed-context sharding by cluster
+# --------------------------------------------------------------------------
+def centroid_lookup_stage(idx: Index, Q, scale, T, T1, stage, stats_in, stats_out, sel: Selection,
+                          ws: torch.Tensor):
+    """sqz_centroid_lookup_stage: one stage of the sharded lookup (the caller
+    exchanges the statistics between stages).  stats_in [P,B,H,n_q,2] fp32 or
+    None (stage 0); stats_out [B,H,n_q,2] fp32 or None (last stage)."""
+    B, H, n_q, d = Q.shape
+    s = idx.struct()
+    p = sqz_lookup_params(scale, T, T1, None)
+    P = 0 if stats_in is None else stats_in.shape[0]
+    ss = sel.struct()
+    _check(lib().sqz_centroid_lookup_stage(ctypes.byref(s), _p(Q), B, n_q, ctypes.byref(p), stage,
+                                           P, _p(stats_in), _p(stats_out), ctypes.byref(ss),
+                                           _p(ws), ws.numel(), _stream()))
+
+
+def shard_plan(H, levels, c1, c2, L, key_off: np.ndarray, child_off: np.ndarray, rank, world):
+    """sqz_shard_plan_compute (host only): the rank's share of the clusters
+    (Level-1 / single-level cluster p -> rank p mod world).  Returns a dict of
+    numpy arrays: c1, c2, L and c1_src, c2_src, key_src, N1, child_off, N2,
+    key_off of the shard."""
+    ko = np.ascontiguousarray(key_off, dtype=np.int32)
+    co = None if child_off is None else np.ascontiguousarray(child_off, dtype=np.int32)
+    pl = sqz_shard_plan()
+    cp = lambda a: None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+    _check(lib().sqz_shard_plan_compute(H, levels, c1, c2, L, cp(ko), cp(co), rank, world,
+                                        ctypes.byref(pl)))
+    C1, C2, LL = pl.c1, pl.c2, pl.L
+    out = dict(c1=C1, c2=C2, L=LL,
+               c2_src=np.zeros((H, C2), np.int32), key_src=np.zeros((H, LL), np.int32),
+               N2=np.zeros((H, C2), np.int32), key_off=np.zeros((H, C2 + 1), np.int32))
+    if levels == 2:
+        out.update(c1_src=np.zeros((H, C1), np.int32), N1=np.zeros((H, C1), np.int32),
+                   child_off=np.zeros((H, C1 + 1), np.int32))
+    for f in ("c1_src", "c2_src", "key_src", "N1", "child_off", "N2", "key_off"):
+        setattr(pl, f, cp(out.get(f)))
+    _check(lib().sqz_shard_plan_compute(H, levels, c1, c2, L, cp(ko), cp(co), rank, world,
+                                        ctypes.byref(pl)))
+    return out
+
+
+def shard_index(idx: Index, Kp: torch.Tensor, Vp: torch.Tensor, rank: int, world: int):
+    """This rank's fixed-context shard of a full index: (Index, Kp_local,
+    Vp_local).  Offline step (copies the integer tables to the host once)."""
+    dev = Kp.device
+    plan = shard_plan(idx.H, idx.levels, idx.c1, idx.c2, idx.L, idx.key_off.cpu().numpy(),
+                      None if idx.child_off is None else idx.child_off.cpu().numpy(), rank, world)
+    td = torch_dtype(idx.dtype)
+    up = lambda a: torch.from_numpy(a).to(dev)
+    H, d = idx.H, idx.d
+    loc = Index(H=H, d=d, L=plan["L"], c2=plan["c2"], dtype=idx.dtype,
+                C2=torch.empty(H, plan["c2"], d, dtype=td, device=dev), N2=up(plan["N2"]),
+                key_off=up(plan["key_off"]), perm=torch.empty(H, plan["L"], dtype=torch.int32,
+                                                              device=dev),
+                c1=plan["c1"], L_total=idx.L, c2_src=up(plan["c2_src"]))
+    if idx.levels == 2:
+        loc.C1 = torch.empty(H, plan["c1"], d, dtype=td, device=dev)
+        loc.N1 = up(plan["N1"])
+        loc.child_off = up(plan["child_off"])
+    Kl = torch.empty(H, plan["L"], d, dtype=td, device=dev)
+    Vl = torch.empty_like(Kl)
+    c1s = up(plan["c1_src"]) if idx.levels == 2 else None
+    c2s, ks = loc.c2_src, up(plan["key_src"])
+    sf, sl = idx.struct(), loc.struct()
+    _check(lib().sqz_index_shard(ctypes.byref(sf), _p(Kp), _p(Vp), _p(c1s), _p(c2s), _p(ks),
+                                 ctypes.byref(sl), _p(Kl), _p(Vl), _stream()))
+    return loc, Kl, Vl
+
+
+class Comm:
+    """sqz_comm over the ranks of a torch.distributed process group (one
+    process per GPU).  The NCCL unique id is created by rank 0 and broadcast
+    through the process group (any backend)."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch.distributed as dist
+
+        self.rank, self.world = rank, world
+        buf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _check(lib().sqz_comm_unique_id(buf))
+        t = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
+        if world > 1:
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, 0, group=group)
+        raw = bytes(t.cpu().numpy().tobytes())
+        h = ctypes.c_void_p()
+        _check(lib().sqz_comm_init(raw, rank, world, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _check(lib().sqz_comm_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def allgather_merge(comm: Comm, O_part: torch.Tensor, LSE_part: torch.Tensor, out_dtype=SQZ_BF16,
+                    O=None, LSE=None, ws=None):
+    """sqz_comm_allgather_merge: every rank's partial (O fp32 [..., d], LSE fp32
+    [...]) -> the merged O (out_dtype) and LSE, identical on every rank."""
+    d = O_part.shape[-1]
+    rows = O_part.numel() // d
+    if O is None:
+        O = torch.empty(O_part.shape, dtype=torch_dtype(out_dtype), device=O_part.device)
+    if LSE is None:
+        LSE = torch.empty(LSE_part.shape, dtype=torch.float32, device=O_part.device)
+    if ws is None:
+        nb = ctypes.c_size_t(0)
+        _check(lib().sqz_comm_merge_workspace(comm.world, rows, d, ctypes.byref(nb)))
+        ws = _WS.get(("merge", O_part.device, comm.world, rows, d), nb.value, O_part.device)
+    _check(lib().sqz_comm_allgather_merge(comm.handle, _p(O_part), _p(LSE_part), rows, d, _p(O),
+                                          _p(LSE), out_dtype, _p(ws), ws.numel(), _stream()))
+    return O, LSE

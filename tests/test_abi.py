@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(lib):
     for name in decl:
         assert hasattr(lib, name), name
     assert sorted(sqz.EXPORTS) == decl
-    assert lib.sqz_abi_version() == 1
+    assert lib.sqz_abi_version() == sqz.ABI_VERSION == 2
 
 
 def test_struct_layout_matches_header(tmp_path):
@@ -41,16 +41,19 @@ def test_struct_layout_matches_header(tmp_path):
 
     prog = tmp_path / "lay.c"
     prog.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "sqz.h"\n'
-                    "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(sqz_index),"
+                    "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(sqz_index),"
                     " offsetof(sqz_index, C1), offsetof(sqz_index, perm), sizeof(sqz_selection),"
-                    " sizeof(sqz_lookup_params), sizeof(sqz_attn_params), sizeof(sqz_kmeans_params));"
+                    " sizeof(sqz_lookup_params), sizeof(sqz_attn_params), sizeof(sqz_kmeans_params),"
+                    " offsetof(sqz_index, L_total), sizeof(sqz_shard_plan), offsetof(sqz_shard_plan, key_off));"
                     "return 0;}\n")
     exe = tmp_path / "lay"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)])
     got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
     want = [ctypes.sizeof(sqz.sqz_index), sqz.sqz_index.C1.offset, sqz.sqz_index.perm.offset,
             ctypes.sizeof(sqz.sqz_selection), ctypes.sizeof(sqz.sqz_lookup_params),
-            ctypes.sizeof(sqz.sqz_attn_params), ctypes.sizeof(sqz.sqz_kmeans_params)]
+            ctypes.sizeof(sqz.sqz_attn_params), ctypes.sizeof(sqz.sqz_kmeans_params),
+            sqz.sqz_index.L_total.offset, ctypes.sizeof(sqz.sqz_shard_plan),
+            sqz.sqz_shard_plan.key_off.offset]
     assert got == want
 
 
