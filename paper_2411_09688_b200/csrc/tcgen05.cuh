@@ -231,6 +231,9 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void *src, 
 }
 __device__ __forceinline__ void cp_async_commit_grp() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait_grp() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // byte offset of 16-byte chunk `c` (0..7) of row `r` in a SW128 tile
 __device__ __forceinline__ uint32_t sw128_off(int r, int c) {
