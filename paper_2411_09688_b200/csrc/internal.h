@@ -1,6 +1,7 @@
 // internal.h -- launcher interfaces between the C-ABI layer (api.cu) and the
 // kernel translation units.  Not part of the public ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -101,6 +102,10 @@ int cluster_keys(const void *K, const void *V, const int64_t *init2, const int64
 size_t validate_workspace_bytes(const sqz_index &idx);
 int index_validate(const sqz_index &idx, void *ws, size_t ws_bytes, cudaStream_t st, char *err,
                    size_t errlen);
+
+// tmap.cu: TMA tensor map of a contiguous bf16 [dims2][dims1][dims0] tensor
+// (128-byte swizzle, zero out-of-bounds fill); 0 on success
+int encode_tmap_bf16_3d(CUtensorMap *m, const void *ptr, const uint64_t dims[3], const uint32_t box[3]);
 
 // shard.cu: gathers of the shard index rows
 cudaError_t launch_shard_gather(const sqz_index &full, const void *Kp, const void *Vp,

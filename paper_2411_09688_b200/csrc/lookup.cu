@@ -24,10 +24,42 @@
 #include "common.cuh"
 #include "internal.h"
 #include "tcgen05.cuh"
+#include "tma.cuh"
+#include <cuda.h>
 
 namespace sqz {
 
 SQZ_TRACE_DECL(g_trace_look)
+SQZ_TRACE_DECL(g_trace_pl)
+#ifdef SQZ_TRACE
+__device__ unsigned long long g_trace_pl_it[64 * 4];
+#define PL_IT(it, slot)                                                                    \
+    do {                                                                                   \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && (it) < 64) {         \
+            unsigned long long t_;                                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+            g_trace_pl_it[(it) * 4 + (slot)] = t_;                                         \
+        }                                                                                  \
+    } while (0)
+extern "C" int sqz_trace_pl_it(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, g_trace_pl_it, bytes < sizeof(g_trace_pl_it) ? bytes : sizeof(g_trace_pl_it));
+}
+__device__ unsigned long long g_trace_fin[64 * 8];
+#define PL_FIN(bh, slot)                                                                   \
+    do {                                                                                   \
+        if (threadIdx.x == 0 && (bh) < 64) {                                               \
+            unsigned long long t_;                                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+            g_trace_fin[(bh) * 8 + (slot)] = t_;                                           \
+        }                                                                                  \
+    } while (0)
+extern "C" int sqz_trace_fin(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, g_trace_fin, bytes < sizeof(g_trace_fin) ? bytes : sizeof(g_trace_fin));
+}
+#else
+#define PL_IT(it, slot) do { } while (0)
+#define PL_FIN(bh, slot) do { } while (0)
+#endif
 
 constexpr int CH = 128;     // centroid rows per CTA
 constexpr int NT = 256;     // threads per CTA
@@ -132,52 +164,112 @@ __device__ __forceinline__ void tile_scan(bool sel, int n, int &pos, int &kpre, 
     __syncthreads();
 }
 
-// Epilogue of the prefill path (one CTA per (b,h)): threshold + ascending
-// compaction + range expansion, tile by tile, with the ranges staged in smem.
-template <bool ROWLIST, typename SelFn>
-__device__ void finalize_rows(const LevelArgs &lv, int bh, int h, int nrows, SelFn selfn) {
-    __shared__ int s_st[NT], s_n[NT], s_kp[NT];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+// Prefill epilogue (the last CTA of a (b,h)): S-bar_i = (1/n_q) sum over the
+// q-tile partials (fixed tile order), threshold, ascending compaction and
+// range expansion.  Rows are processed R per thread per pass with every
+// partial load issued before the first use, so the pass costs one or two L2
+// round trips instead of one per row tile.
+template <bool ROWLIST, int R = 4>
+__device__ void finalize_colpart(const LevelArgs &lv, int bh, int h, int nrows, int nqt, int BH,
+                                 float inv_nq) {
+    const int tid = threadIdx.x;
+    const int nt = blockDim.x;
     const int32_t *off = lv.off + (size_t)h * (lv.c + 1);
     int32_t *list = lv.list + (size_t)bh * lv.c;
-    int32_t *exp_list = lv.exp_list + (size_t)bh * lv.exp_stride;
     const int32_t *rows = ROWLIST ? lv.rows + (size_t)bh * lv.row_stride : nullptr;
-    const int nt = blockDim.x, nwp = nt >> 5;  // works for 128- and 256-thread CTAs
+    const bool all = !(lv.T > 0.f);
+    PL_FIN(bh, 0);
     if (lv.dbg_S && ROWLIST)
         for (int r = tid; r < lv.c; r += nt) lv.dbg_S[(size_t)bh * lv.c + r] = NAN;
     __syncthreads();
+    const float *cp = lv.colpart + (size_t)bh * lv.c;
+    const size_t stride = (size_t)BH * lv.c;
     int run = 0, runk = 0;
-    for (int base = 0; base < nrows; base += nt) {
-        const int r = base + tid;
-        const bool valid = r < nrows;
-        const int row = valid ? (ROWLIST ? ldcg(rows + r) : r) : 0;
-        float dbg = 0.f;
-        const bool sel = valid && selfn(row, dbg);
-        if (valid && lv.dbg_S) lv.dbg_S[(size_t)bh * lv.c + row] = dbg;
-        if (valid && lv.bitmap) lv.bitmap[(size_t)bh * lv.c + row] = sel ? 1 : 0;
-        int st = 0, n = 0;
-        if (sel) { st = off[row]; n = off[row + 1] - st; }
-        int pos, kpre, tc, tk;
-        tile_scan(sel, n, pos, kpre, tc, tk);
-        if (sel) {
-            list[run + pos] = row;
-            s_st[pos] = st;
-            s_n[pos] = n;
-            s_kp[pos] = runk + kpre;
+    for (int sb = 0; sb < nrows; sb += nt * R) {
+        int row[R], st[R], n[R];
+        bool sel[R];
+        float acc[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int r = sb + i * nt + tid;
+            row[i] = r < nrows ? (ROWLIST ? ldcg(rows + r) : r) : -1;
+            acc[i] = 0.f;
         }
-        __syncthreads();
-        for (int j = warp; j < tc; j += nwp) {
-            const int st_j = s_st[j], n_j = s_n[j], kp_j = s_kp[j];
-            for (int t = lane; t < n_j; t += 32) exp_list[kp_j + t] = st_j + t;
+        int t = 0;
+        for (; t + 4 <= nqt; t += 4) {
+            float x[4][R];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int i = 0; i < R; ++i) x[u][i] = row[i] >= 0 ? ldcg(cp + (t + u) * stride + row[i]) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int i = 0; i < R; ++i) acc[i] += x[u][i];
         }
-        __syncthreads();
-        run += tc;
-        runk += tk;
+        for (; t < nqt; ++t)
+#pragma unroll
+            for (int i = 0; i < R; ++i) acc[i] += row[i] >= 0 ? ldcg(cp + t * stride + row[i]) : 0.f;
+        PL_FIN(bh, 1);
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const float Sbar = acc[i] * inv_nq;
+            sel[i] = row[i] >= 0 && (all || Sbar > lv.T);
+            st[i] = 0;
+            n[i] = 0;
+            if (sel[i]) {
+                st[i] = __ldg(off + row[i]);
+                n[i] = __ldg(off + row[i] + 1) - st[i];
+            }
+            if (row[i] >= 0 && lv.dbg_S) lv.dbg_S[(size_t)bh * lv.c + row[i]] = Sbar;
+            if (row[i] >= 0 && lv.bitmap) lv.bitmap[(size_t)bh * lv.c + row[i]] = sel[i] ? 1 : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            if (sb + i * nt >= nrows) break;  // uniform
+            int pos, kpre, tc, tk;
+            PL_FIN(bh, 2 + i);
+            tile_scan(sel[i], n[i], pos, kpre, tc, tk);
+            if (sel[i]) {  // the keys are expanded by k_expand_ranges (many CTAs)
+                list[run + pos] = row[i];
+                lv.sel_pref[(size_t)bh * lv.c + run + pos] = runk + kpre;
+            }
+            if (i == 0) PL_FIN(bh, 7);
+            run += tc;
+            runk += tk;
+        }
     }
     if (tid == 0) {
         lv.n_list[bh] = run;
         lv.n_exp[bh] = runk;
     }
+    PL_FIN(bh, 6);
+}
+
+// Range expansion of a finished selection, spread over many CTAs: list entry j
+// of (b,h) (row id, key offset sel_pref[j]) becomes the positions
+// [off[row], off[row + 1]) at exp_list[sel_pref[j] ...].  One warp per list
+// entry; grid (ceil(c / EXP_ROWS), B*H).
+constexpr int EXP_ROWS = 32;
+__global__ void __launch_bounds__(NT) k_expand_ranges(LevelArgs lv, int H) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int bh = blockIdx.y, h = bh % H;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = ldcg(lv.n_list + bh);
+    const int32_t *off = lv.off + (size_t)h * (lv.c + 1);
+    int32_t *exp_list = lv.exp_list + (size_t)bh * lv.exp_stride;
+    for (int j = blockIdx.x * EXP_ROWS + warp; j < min(n, (blockIdx.x + 1) * EXP_ROWS); j += NW) {
+        const int row = ldcg(lv.list + (size_t)bh * lv.c + j);
+        const int kp = ldcg(lv.sel_pref + (size_t)bh * lv.c + j);
+        const int st = __ldg(off + row), cnt = __ldg(off + row + 1) - st;
+        for (int q = lane; q < cnt; q += 32) exp_list[kp + q] = st + q;
+    }
+}
+
+static cudaError_t launch_expand(const LookupShape &s, const LevelArgs &lv, cudaStream_t st) {
+    dim3 grid((lv.c + EXP_ROWS - 1) / EXP_ROWS, s.B * s.H);
+    k_expand_ranges<<<grid, NT, 0, st>>>(lv, s.H);
+    return cudaGetLastError();
 }
 
 // --------------------------------------------------------------------------
@@ -456,6 +548,7 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
 }
 
 SQZ_TRACE_EXPORT(g_trace_look, sqz_trace_look)
+SQZ_TRACE_EXPORT(g_trace_pl, sqz_trace_pl)
 
 // --------------------------------------------------------------------------
 // Fold of the shards' (m, D) statistics, sequentially in rank order (every
@@ -608,15 +701,7 @@ __global__ void __launch_bounds__(NT) k_prefill_colsum(LookupShape s, const T *_
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const bool all = !(lv.T > 0.f);
-    const float inv_nq = 1.0f / (float)s.n_q;
-    finalize_rows<ROWLIST>(lv, bh, h, nrows, [&](int row, float &dbg) {
-        float acc = 0.f;
-        for (int t = 0; t < nqt; ++t) acc += ldcg(lv.colpart + ((size_t)t * s.B * s.H + bh) * c + row);
-        const float Sbar = acc * inv_nq;
-        dbg = Sbar;
-        return all || (Sbar > lv.T);
-    });
+    finalize_colpart<ROWLIST>(lv, bh, h, nrows, nqt, s.B * s.H, 1.0f / (float)s.n_q);
 }
 
 // --------------------------------------------------------------------------
@@ -676,18 +761,24 @@ static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelAr
 constexpr int PL_T = 128;   // query rows per CTA = centroid rows per tile
 constexpr int PL_NT = 256;  // 8 warps: (TMEM lane quarter) x (column half)
 
+struct PlMaps {
+    CUtensorMap c;  // centroids [H][c][D] bf16, box {64, 128, 1}, 128B swizzle
+    CUtensorMap q;  // queries [B*H][n_q][D] bf16, same box
+};
+
 template <int D> struct PlSmem {
     static constexpr int TILE = PL_T * D * 2;
     static constexpr int Q = 0;
     static constexpr int C0 = Q + TILE;              // 2 buffers
-    static constexpr int MISC = C0 + 2 * TILE;
+    static constexpr int MISC = C0 + 2 * TILE;  // 5 mbarriers + TMEM address
     static constexpr int BYTES = MISC + 64 + 1024;
 };
 
 template <int D, bool ROWLIST>
 __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
                                                                  const __nv_bfloat16 *__restrict__ Q,
-                                                                 LevelArgs lv) {
+                                                                 LevelArgs lv,
+                                                                 const __grid_constant__ PlMaps maps) {
     using SM = PlSmem<D>;
     constexpr int CPR = D * 2 / 16;
     constexpr int HB = PL_T * 128;
@@ -696,12 +787,15 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
     unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     const uint32_t sbase = smem_u32(sm);
     // small per-tile metadata in static shared memory (plain LDS/STS)
-    __shared__ float s_nw[4 * PL_T];
+    __shared__ __align__(16) float s_nw[4 * PL_T];
     __shared__ int s_rid[4 * PL_T];
-    __shared__ float s_lse[PL_T];
+    __shared__ __align__(16) float s_lse[PL_T];
     __shared__ float2 s_half[2 * PL_T];
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + SM::MISC);
-    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sm + SM::MISC + 16);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(sm + SM::MISC);     // [2] MMA done
+    uint64_t *tbar = mbar + 2;                                           // [2] C tile landed (TMA)
+    uint64_t *qbar = mbar + 4;                                           // Q tile landed (TMA)
+    uint32_t *s_tmem = reinterpret_cast<uint32_t *>(sm + SM::MISC + 48);
+    constexpr uint32_t TILE_BYTES = PL_T * D * 2;
     __shared__ int s_last;
 
     asm volatile("griddepcontrol.launch_dependents;");
@@ -718,8 +812,7 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
 
     if (warp == 0) tmem_alloc(s_tmem, 256);
     if (tid == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
+        for (int i = 0; i < 5; ++i) mbar_init(&mbar[i], 1);
         mbar_fence_init();
     }
     tc_fence_before();
@@ -727,14 +820,23 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
     tc_fence_after();
     const uint32_t tmem = *s_tmem;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    SQZ_TRACE_AT(g_trace_pl, 0);
 
-    // Q tile (rows beyond n_q are zero)
-    const __nv_bfloat16 *Qb = Q + ((size_t)bh * s.n_q + t0) * D;
-    for (int e = tid; e < PL_T * CPR; e += PL_NT) {
-        const int rr = e / CPR, cc = e % CPR;
-        const bool valid = t0 + rr < s.n_q;
-        cp_async16_zfill(sbase + SM::Q + (cc >> 3) * HB + sw128_off(rr, cc & 7),
-                         Qb + (size_t)(valid ? rr : 0) * D + cc * 8, valid);
+    // Q tile (rows beyond n_q are zero): TMA for contiguous tables, else cp.async
+    if constexpr (!ROWLIST) {
+        if (tid == 0) {
+            mbar_arrive_expect_tx(qbar, TILE_BYTES);
+#pragma unroll
+            for (int hb = 0; hb < D / 64; ++hb) tma_load_3d(sbase + SM::Q + hb * HB, &maps.q, hb * 64, t0, bh, qbar);
+        }
+    } else {
+        const __nv_bfloat16 *Qb = Q + ((size_t)bh * s.n_q + t0) * D;
+        for (int e = tid; e < PL_T * CPR; e += PL_NT) {
+            const int rr = e / CPR, cc = e % CPR;
+            const bool valid = t0 + rr < s.n_q;
+            cp_async16_zfill(sbase + SM::Q + (cc >> 3) * HB + sw128_off(rr, cc & 7),
+                             Qb + (size_t)(valid ? rr : 0) * D + cc * 8, valid);
+        }
     }
     // pass 1 then pass 2 over the same tiles; the staged lookup runs them as
     // separate launches (phase 1: pass 1 only; phase 2: pass 2 only, with the
@@ -763,10 +865,27 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
             s_nw[(k & 3) * PL_T + rr] = nw;
         }
         const uint32_t dst = sbase + SM::C0 + (k & 1) * SM::TILE;
-        for (int cc = (tid / PL_T) * (CPR / 2); cc < (tid / PL_T + 1) * (CPR / 2); ++cc)
-            cp_async16_zfill(dst + (cc >> 3) * HB + sw128_off(rr, cc & 7),
-                             C + (size_t)(rid >= 0 ? rid : 0) * D + cc * 8, rid >= 0);
-        cp_async_commit_grp();
+        if constexpr (!ROWLIST) {  // one thread: two 64-column boxes, rows past c zero-filled
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&tbar[k & 1], TILE_BYTES);
+#pragma unroll
+                for (int hb = 0; hb < D / 64; ++hb)
+                    tma_load_3d(dst + hb * HB, &maps.c, hb * 64, (j % ntile) * PL_T, h, &tbar[k & 1]);
+            }
+        } else {
+            for (int cc = (tid / PL_T) * (CPR / 2); cc < (tid / PL_T + 1) * (CPR / 2); ++cc)
+                cp_async16_zfill(dst + (cc >> 3) * HB + sw128_off(rr, cc & 7),
+                                 C + (size_t)(rid >= 0 ? rid : 0) * D + cc * 8, rid >= 0);
+            cp_async_commit_grp();
+        }
+    };
+    // thread 0, before issuing MMA(j): the TMA loads of its operands have landed
+    auto wait_tile = [&](int j) {
+        if constexpr (!ROWLIST) {
+            const int k = j - first;
+            if (k == 0) mbar_wait(qbar, 0);
+            mbar_wait(&tbar[k & 1], (k >> 1) & 1);
+        }
     };
     auto issue_mma = [&](int j) {  // one elected thread
         const int k = j - first;
@@ -806,12 +925,15 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
     tc_fence_before();
     __syncthreads();
     if (tid == 0 && first < total) {
+        wait_tile(first);
         tc_fence_after();
         issue_mma(first);
     }
 
+    SQZ_TRACE_AT(g_trace_pl, 1);
     float m = -INFINITY, Dsum = 0.f;
     for (int it = first; it < total; ++it) {
+        if (it == ntile) SQZ_TRACE_AT(g_trace_pl, 2);
         const int k = it - first, buf = k & 1, tl = it % ntile, pass = it / ntile;
         // MMA of the next tile into the other TMEM buffer, overlapping this epilogue
         cp_async_wait_all();
@@ -819,42 +941,51 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
         tc_fence_before();
         __syncthreads();
         if (tid == 0 && it + 1 < total) {
+            wait_tile(it + 1);
             tc_fence_after();
             issue_mma(it + 1);
         }
+        PL_IT(k, 0);
         mbar_wait(&mbar[buf], (k >> 1) & 1);
         tc_fence_after();
+        PL_IT(k, 1);
         if (it + 2 < total) load_tile(it + 2, rid_pf, nw_pf);  // MMA(it) no longer reads buffer `buf`
         tile_meta(it + 3, rid_pf, nw_pf);  // latency hidden behind this epilogue
         const float *nwb = s_nw + (k & 3) * PL_T;
         if (pass == 0) {
             // thread = query row r; columns = centroids hf*64 + [0, 64) of tile tl
-#pragma unroll 1
-            for (int ch = 0; ch < 2; ++ch) {
-                const int col0 = hf * 64 + ch * 32;
-                float v[32];
-                tmem_ld32(tmem + buf * 128 + lane_off + col0, v);
-                tmem_wait_ld();
-                float cmx = -INFINITY;
+            float v0[32], v1[32];
+            tmem_ld32(tmem + buf * 128 + lane_off + hf * 64, v0);
+            tmem_ld32(tmem + buf * 128 + lane_off + hf * 64 + 32, v1);
+            tmem_wait_ld();
+            const int lim = nrows - tl * PL_T - hf * 64;  // valid columns of this half
+            float cmx = -INFINITY;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const bool valid = tl * PL_T + col0 + j < nrows;
-                    v[j] = valid ? v[j] * s.scale : -INFINITY;
-                    cmx = fmaxf(cmx, v[j]);
-                }
-                const float mn = fmaxf(m, cmx);
-                if (mn != -INFINITY) {
-                    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            for (int j = 0; j < 32; ++j) {
+                v0[j] = j < lim ? v0[j] * s.scale : -INFINITY;
+                v1[j] = j + 32 < lim ? v1[j] * s.scale : -INFINITY;
+                cmx = fmaxf(cmx, fmaxf(v0[j], v1[j]));
+            }
+            const float mn = fmaxf(m, cmx);
+            if (mn != -INFINITY) {
+                const float4 *nw4 = reinterpret_cast<const float4 *>(nwb + hf * 64);
+                float a[8];
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        a0 = fmaf(nwb[col0 + j], exp_fast(v[j] - mn), a0);
-                        a1 = fmaf(nwb[col0 + j + 1], exp_fast(v[j + 1] - mn), a1);
-                        a2 = fmaf(nwb[col0 + j + 2], exp_fast(v[j + 2] - mn), a2);
-                        a3 = fmaf(nwb[col0 + j + 3], exp_fast(v[j + 3] - mn), a3);
-                    }
-                    Dsum = Dsum * expf(m - mn) + ((a0 + a1) + (a2 + a3));
-                    m = mn;
+                for (int u = 0; u < 8; ++u) a[u] = 0.f;
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    const float4 w0 = nw4[j / 4], w1 = nw4[8 + j / 4];
+                    a[0] = fmaf(w0.x, exp_fast(v0[j] - mn), a[0]);
+                    a[1] = fmaf(w0.y, exp_fast(v0[j + 1] - mn), a[1]);
+                    a[2] = fmaf(w0.z, exp_fast(v0[j + 2] - mn), a[2]);
+                    a[3] = fmaf(w0.w, exp_fast(v0[j + 3] - mn), a[3]);
+                    a[4] = fmaf(w1.x, exp_fast(v1[j] - mn), a[4]);
+                    a[5] = fmaf(w1.y, exp_fast(v1[j + 1] - mn), a[5]);
+                    a[6] = fmaf(w1.z, exp_fast(v1[j + 2] - mn), a[6]);
+                    a[7] = fmaf(w1.w, exp_fast(v1[j + 3] - mn), a[7]);
                 }
+                Dsum = Dsum * expf(m - mn) + (((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
+                m = mn;
             }
             if (tl == ntile - 1) {  // fold the two column halves of each query row
                 s_half[hf * PL_T + r] = make_float2(m, Dsum);
@@ -880,21 +1011,27 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
             }
         } else {
             // S^T: thread = centroid row r of tile tl; columns = queries hf*64 + [0, 64)
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 1
-            for (int ch = 0; ch < 2; ++ch) {
-                const int col0 = hf * 64 + ch * 32;
-                float v[32];
-                tmem_ld32(tmem + buf * 128 + lane_off + col0, v);
-                tmem_wait_ld();
+            float v0[32], v1[32];
+            tmem_ld32(tmem + buf * 128 + lane_off + hf * 64, v0);
+            tmem_ld32(tmem + buf * 128 + lane_off + hf * 64 + 32, v1);
+            tmem_wait_ld();
+            const float4 *l4 = reinterpret_cast<const float4 *>(s_lse + hf * 64);
+            float a[8];
 #pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    a0 += exp_fast(fmaf(v[j], s.scale, -s_lse[col0 + j]));
-                    a1 += exp_fast(fmaf(v[j + 1], s.scale, -s_lse[col0 + j + 1]));
-                    a2 += exp_fast(fmaf(v[j + 2], s.scale, -s_lse[col0 + j + 2]));
-                    a3 += exp_fast(fmaf(v[j + 3], s.scale, -s_lse[col0 + j + 3]));
-                }
+            for (int u = 0; u < 8; ++u) a[u] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+                const float4 e0 = l4[j / 4], e1 = l4[8 + j / 4];
+                a[0] += exp_fast(fmaf(v0[j], s.scale, -e0.x));
+                a[1] += exp_fast(fmaf(v0[j + 1], s.scale, -e0.y));
+                a[2] += exp_fast(fmaf(v0[j + 2], s.scale, -e0.z));
+                a[3] += exp_fast(fmaf(v0[j + 3], s.scale, -e0.w));
+                a[4] += exp_fast(fmaf(v1[j], s.scale, -e1.x));
+                a[5] += exp_fast(fmaf(v1[j + 1], s.scale, -e1.y));
+                a[6] += exp_fast(fmaf(v1[j + 2], s.scale, -e1.z));
+                a[7] += exp_fast(fmaf(v1[j + 3], s.scale, -e1.w));
             }
+            const float a0 = a[0] + a[1], a1 = a[2] + a[3], a2 = a[4] + a[5], a3 = a[6] + a[7];
             s_half[hf * PL_T + r].x = (a0 + a1) + (a2 + a3);
             __syncthreads();
             if (tid < PL_T) {
@@ -903,9 +1040,11 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
                     lv.colpart[((size_t)qt * s.B * s.H + bh) * c + rid] = s_half[tid].x + s_half[PL_T + tid].x;
             }
         }
+        PL_IT(k, 2);
         tc_fence_before();
     }
     __syncthreads();
+    SQZ_TRACE_AT(g_trace_pl, 3);
     if (warp == 0) tmem_dealloc(tmem, 256);
     if (lv.phase == 1) {
         if (ntile == 0 && tid < PL_T && t0 + tid < s.n_q)  // no rows: the identity statistics
@@ -922,28 +1061,10 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
     }
     __syncthreads();
     if (!s_last) return;
+    SQZ_TRACE_AT(g_trace_pl, 4);
     __threadfence();
-    const int nqt = gridDim.x;
-    const bool all = !(lv.T > 0.f);
-    const float inv_nq = 1.0f / (float)s.n_q;
-    finalize_rows<ROWLIST>(lv, bh, h, nrows, [&](int row, float &dbg) {
-        float acc = 0.f;
-        const float *cp = lv.colpart + (size_t)bh * c + row;
-        const size_t stride = (size_t)s.B * s.H * c;
-        int t = 0;
-        for (; t + 4 <= nqt; t += 4) {  // independent loads, summed in tile order
-            const float x0 = ldcg(cp + t * stride), x1 = ldcg(cp + (t + 1) * stride);
-            const float x2 = ldcg(cp + (t + 2) * stride), x3 = ldcg(cp + (t + 3) * stride);
-            acc += x0;
-            acc += x1;
-            acc += x2;
-            acc += x3;
-        }
-        for (; t < nqt; ++t) acc += ldcg(cp + t * stride);
-        const float Sbar = acc * inv_nq;
-        dbg = Sbar;
-        return all || (Sbar > lv.T);
-    });
+    finalize_colpart<ROWLIST>(lv, bh, h, nrows, gridDim.x, s.B * s.H, 1.0f / (float)s.n_q);
+    SQZ_TRACE_AT(g_trace_pl, 5);
 }
 
 template <int D, bool RL>
@@ -957,9 +1078,21 @@ static cudaError_t launch_prefill_tc(const LookupShape &s, const __nv_bfloat16 *
         if (e != cudaSuccess) return e;
         set = true;
     }
+    PlMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    if (!RL) {
+        const uint64_t dc[3] = {(uint64_t)D, (uint64_t)lv.c, (uint64_t)s.H};
+        const uint64_t dq[3] = {(uint64_t)D, (uint64_t)s.n_q, (uint64_t)s.B * s.H};
+        const uint32_t box[3] = {64, PL_T, 1};
+        if (encode_tmap_bf16_3d(&maps.c, lv.C, dc, box) != 0 ||
+            encode_tmap_bf16_3d(&maps.q, Q, dq, box) != 0)
+            return cudaErrorInvalidValue;
+    }
     dim3 grid((s.n_q + PL_T - 1) / PL_T, s.B * s.H);
-    kern<<<grid, PL_NT, PlSmem<D>::BYTES, st>>>(s, Q, lv);
-    return cudaGetLastError();
+    kern<<<grid, PL_NT, PlSmem<D>::BYTES, st>>>(s, Q, lv, maps);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && lv.phase != 1) e = launch_expand(s, lv, st);
+    return e;
 }
 
 template <typename T, int D>
@@ -994,7 +1127,9 @@ static cudaError_t launch_level_t(const LookupShape &s, const T *Q, const LevelA
         if (lv.phase != 2) k_prefill_rowlse<T, D, false><<<g1, NT, 0, st>>>(s, Q, lv);
         if (lv.phase != 1) k_prefill_colsum<T, D, false><<<g2, NT, 0, st>>>(s, Q, lv);
     }
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && lv.phase != 1) e = launch_expand(s, lv, st);
+    return e;
 }
 
 cudaError_t launch_lookup_level(const LookupShape &s, const void *Q, const LevelArgs &lv,

@@ -53,6 +53,15 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void *map, int x
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
+// 3-D tensor-map (TMA) tile load (coordinates innermost first)
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void *map, int x, int y, int z,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
 // TMA gather of 4 rows y0..y3 (box = {width, 1}) into 4 consecutive smem rows
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const void *map, int x, int y0, int y1,
                                             int y2, int y3, uint64_t *bar) {
