@@ -46,9 +46,19 @@ CONFIGS = {
                  mode="prefill", H=32, d=128, L=32768, c2=1024, c1=0, B=1, n_q=1024, n_u=1024,
                  dtype=1, retention=0.3, cfgno=3),
     "cfg4": dict(workload="cfg4: 128K hierarchical decode, H=32 d128, L=131072, c1=1311, c2=6554, "
-                          "L1 prunes 50%, retention 10%, B=8, n_u=1024, bf16",
+                          "L1 prunes 50%, retention 10%, B=8, n_u=1024, bf16; heads sharded over the GPUs",
                  mode="decode", H=32, d=128, L=131072, c2=6554, c1=1311, B=8, n_q=1, n_u=1024,
-                 dtype=1, retention=0.1, cfgno=4),
+                 dtype=1, retention=0.1, cfgno=4, shard="heads", device_gen=True),
+    "cfg5": dict(workload="cfg5: LWM-Text-Chat-1M decode, H=32 d128, L=1048576, c1=10486, c2=52429 "
+                          "hierarchical, L1 prunes 50%, retention 10%, B=1, n_u=1024, bf16; fixed context "
+                          "sharded by cluster over the GPUs (stats all-gather + (O, LSE) all-gather merge)",
+                 mode="decode", H=32, d=128, L=1048576, c2=52429, c1=10486, B=1, n_q=1, n_u=1024,
+                 dtype=1, retention=0.1, cfgno=5, shard="clusters", device_gen=True, kmeans_iters=2),
+    "cfg5p": dict(workload="cfg5 prefill: LWM-Text-Chat-1M, H=32 d128, L=1048576, c1=10486, c2=52429 "
+                           "hierarchical, retention 10%, n_q=n_u=4096 causal, bf16; fixed context "
+                           "sharded by cluster over the GPUs",
+                  mode="prefill", H=32, d=128, L=1048576, c2=52429, c1=10486, B=1, n_q=4096, n_u=4096,
+                  dtype=1, retention=0.1, cfgno=5, shard="clusters", device_gen=True, kmeans_iters=2),
 }
 
 
@@ -128,11 +138,19 @@ def cpu_oracle_run(cfg, steps=None, warmup=0, seconds=12.0, h_sample=4):
     from paper_2411_09688_b200 import calib, synth
 
     hs = min(h_sample, cfg["H"])
-    fc = synth.fixed_context(cfg["H"], cfg["L"], cfg["d"], cfg["c2"], dtype=cfg["dtype"],
+    # contexts beyond 32K keys: a 32K-key sample with the same centroid fractions,
+    # time scaled linearly in L (lookup rows and selected keys are both ~ L)
+    Ls = min(cfg["L"], 32768)
+    fL = cfg["L"] / Ls
+    L_full = cfg["L"]
+    c2s = int(np.ceil(cfg["c2"] / fL))
+    c1s = int(np.ceil(cfg["c1"] / fL)) if cfg["c1"] else 0
+    cfg = dict(cfg, L=Ls, c2=c2s, c1=c1s)
+    fc = synth.fixed_context(hs, cfg["L"], cfg["d"], cfg["c2"], dtype=cfg["dtype"],
                              seed=1000 + cfg["cfgno"], G1=cfg["c1"])
-    K, V = fc.K[:hs], fc.V[:hs]
-    init2 = synth.kmeans_init(cfg["H"], cfg["L"], cfg["c2"], seed=2000 + cfg["cfgno"])[:hs]
-    init1 = (synth.kmeans_init(cfg["H"], cfg["c2"], cfg["c1"], seed=2100 + cfg["cfgno"])[:hs]
+    K, V = fc.K, fc.V
+    init2 = synth.kmeans_init(hs, cfg["L"], cfg["c2"], seed=2000 + cfg["cfgno"])
+    init1 = (synth.kmeans_init(hs, cfg["c2"], cfg["c1"], seed=2100 + cfg["cfgno"])
              if cfg["c1"] else None)
     idx = oracle.build_index(K, cfg["c2"], init2, cfg["c1"], init1, max_iters=10)
     scale = 1.0 / np.sqrt(cfg["d"])
@@ -187,17 +205,19 @@ def cpu_oracle_run(cfg, steps=None, warmup=0, seconds=12.0, h_sample=4):
             break
         if steps is None and (time.perf_counter() - t_start > seconds or i >= 2000) and i >= 3:
             break
-    per = float(np.mean(times))
+    per = float(np.mean(times)) * fL
     scale_h = cfg["H"] / hs
     if cfg["mode"] == "decode":
         value = per * scale_h * 1e6 / cfg["B"] if cfg["B"] == 1 else per * scale_h * 1e6
-        sample = (f"{hs} of {cfg['H']} heads, full L={cfg['L']}, c={cfg['c2']}, n_u={cfg['n_u']}; "
+        sample = (f"{hs} of {cfg['H']} heads, L={cfg['L']} (x{fL:g} to L={L_full}), c={cfg['c2']}, "
+                  f"c1={cfg['c1']}, n_u={cfg['n_u']}; "
                   f"oracle K-means index (10 Lloyd iters); {len(times)} decode tokens x 1 layer; "
                   f"time x{scale_h:g} to all heads")
     else:
         # lookup on all n_q rows + attention on 64 rows: scale the attention part
         value = cfg["n_q"] / (per * scale_h * (cfg["n_q"] / 64.0))
-        sample = (f"{hs} of {cfg['H']} heads; lookup over all {cfg['n_q']} rows + attention on 64 "
+        sample = (f"{hs} of {cfg['H']} heads, L={cfg['L']} (x{fL:g} to L={L_full}); lookup over all "
+                  f"{cfg['n_q']} rows + attention on 64 "
                   f"of {cfg['n_q']} rows; {len(times)} prefill blocks; scaled x{scale_h:g} heads and "
                   f"x{cfg['n_q'] / 64:g} rows (upper bound on oracle throughput)")
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
@@ -254,67 +274,141 @@ def run_gpu(args, cfg, rank, world, local_rank):
     dt = cfg["dtype"]
     H, d, L, c2, c1, B, n_q, n_u = (cfg[k] for k in ("H", "d", "L", "c2", "c1", "B", "n_q", "n_u"))
     scale = 1.0 / float(np.sqrt(d))
+    # ---- sharding of the work over the ranks ----
+    shard = cfg.get("shard", "replicas") if world > 1 else "none"
+    cno = cfg["cfgno"]
+    if shard == "heads":  # H/g heads per GPU, no exchange on the hot path
+        if H % world:
+            raise SystemExit(f"{H} heads do not split over {world} GPUs")
+        heads = list(range(rank * H // world, (rank + 1) * H // world))
+    else:
+        heads = list(range(H))
+    Hl = len(heads)
+    # cluster sharding: rank r holds a contiguous 1/g slice of the
+    # fixed context with its own index (clusters never straddle ranks); the lookup
+    # all-gathers the per-level (m, D) statistics, the attention partials are
+    # all-gathered and merged -- all inside libsqz (NCCL)
+    Ls = L // world if shard == "clusters" else L
+    c2s = -(-c2 // world) if shard == "clusters" else c2
+    c1s = (-(-c1 // world) if c1 else 0) if shard == "clusters" else c1
+    kiters = cfg.get("kmeans_iters", args.kmeans_iters) if args.kmeans_iters_set is None \
+        else args.kmeans_iters_set
     # ---- offline: data + index (not timed) ----
-    fc = synth.fixed_context(H, L, d, c2, dtype=dt, seed=1000 + cfg["cfgno"], G1=c1)
-    K, V = sqz.to_device(fc.K, dev), sqz.to_device(fc.V, dev)
-    init2 = torch.from_numpy(synth.kmeans_init(H, L, c2, seed=2000 + cfg["cfgno"])).to(dev)
-    init1 = (torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=2100 + cfg["cfgno"])).to(dev)
-             if c1 else None)
+    if cfg.get("device_gen"):
+        mix = synth.device_mixture(H, c2, d, G1=c1, seed=1000 + cno, device=dev)
+        K, V = synth.device_keys(mix, Ls, seed=1000 + cno + 7919 * (rank + 1) if shard == "clusters"
+                                 else 1000 + cno, dtype=dt, heads=heads)
+        init2 = synth.device_kmeans_init(Hl, Ls, c2s, seed=2000 + cno + 13 * rank, device=dev)
+        init1 = synth.device_kmeans_init(Hl, c2s, c1s, seed=2100 + cno + 13 * rank, device=dev) \
+            if c1 else None
+    else:
+        fc = synth.fixed_context(H, L, d, c2, dtype=dt, seed=1000 + cno, G1=c1)
+        mix = fc.mix
+        K, V = sqz.to_device(fc.K, dev), sqz.to_device(fc.V, dev)
+        init2 = torch.from_numpy(synth.kmeans_init(H, L, c2, seed=2000 + cno)).to(dev)
+        init1 = (torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=2100 + cno)).to(dev)
+                 if c1 else None)
     t0 = time.time()
-    idx, Kp, Vp, iters = sqz.cluster_keys(K, V, c2, init2, c1, init1, max_iters=args.kmeans_iters)
+    idx, Kp, Vp, iters = sqz.cluster_keys(K, V, c2s, init2, c1s, init1, max_iters=kiters)
     torch.cuda.synchronize()
     t_index = time.time() - t0
     del K, V
-    mix = fc.mix
-    # ---- calibration (App. C): 100 separate queries ----
+    comm = sqz.Comm(rank, world) if shard == "clusters" else None
+
+    def allsum(x):
+        if world == 1 or shard not in ("heads", "clusters"):
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        return float(t.item())
+
+    # ---- queries: 100 calibration (App. C) + test inputs, user KV ----
     if cfg["mode"] == "decode":
-        Qc = sqz.to_device(synth.decode_queries(mix, 100, seed=3000 + cfg["cfgno"], dtype=dt), dev)
-        Qt = sqz.to_device(synth.decode_queries(mix, 100 * B, seed=4000 + cfg["cfgno"], dtype=dt),
-                           dev).view(100, B, H, 1, d)
-        n_inputs = 100
+        n_cal, n_inputs = (100, 100) if not cfg.get("device_gen") else (32, 16)
     else:
-        Qc = sqz.to_device(synth.prefill_queries(mix, 4, n_q, seed=3000 + cfg["cfgno"], dtype=dt),
-                           dev)
-        n_inputs = 4
-        Qt = sqz.to_device(synth.prefill_queries(mix, n_inputs * B, n_q, seed=4000 + cfg["cfgno"],
-                                                 dtype=dt), dev).view(n_inputs, B, H, n_q, d)
-    Ku, Vu = (sqz.to_device(a, dev) for a in synth.user_kv(mix, B, n_u, seed=5000 + cfg["cfgno"],
-                                                            dtype=dt))
+        n_cal, n_inputs = 4, 4
+    if cfg.get("device_gen"):
+        if cfg["mode"] == "decode":
+            Qc = synth.device_decode_queries(mix, n_cal, seed=3000 + cno, dtype=dt, heads=heads)
+            Qt = synth.device_decode_queries(mix, n_inputs * B, seed=4000 + cno, dtype=dt,
+                                             heads=heads).view(n_inputs, B, Hl, 1, d)
+        else:
+            Qc = synth.device_prefill_queries(mix, 1, n_q, seed=3000 + cno, dtype=dt, heads=heads)
+            n_inputs = 2
+            Qt = synth.device_prefill_queries(mix, n_inputs * B, n_q, seed=4000 + cno, dtype=dt,
+                                              heads=heads).view(n_inputs, B, Hl, n_q, d)
+        Ku, Vu = synth.device_user_kv(mix, B, n_u, seed=5000 + cno, dtype=dt, heads=heads)
+    else:
+        if cfg["mode"] == "decode":
+            Qc = sqz.to_device(synth.decode_queries(mix, n_cal, seed=3000 + cno, dtype=dt), dev)
+            Qt = sqz.to_device(synth.decode_queries(mix, n_inputs * B, seed=4000 + cno, dtype=dt),
+                               dev).view(n_inputs, B, H, 1, d)
+        else:
+            Qc = sqz.to_device(synth.prefill_queries(mix, n_cal, n_q, seed=3000 + cno, dtype=dt), dev)
+            Qt = sqz.to_device(synth.prefill_queries(mix, n_inputs * B, n_q, seed=4000 + cno,
+                                                     dtype=dt), dev).view(n_inputs, B, H, n_q, d)
+        Ku, Vu = (sqz.to_device(a, dev) for a in synth.user_kv(mix, B, n_u, seed=5000 + cno, dtype=dt))
+    if shard == "clusters" and rank != 0:
+        Ku = Vu = None  # the user KV partial is computed once, on rank 0
+    n_u_r = 0 if Ku is None else n_u
     Bc = Qc.shape[0]
+    # ---- calibration of the global thresholds (R12, R13) ----
     T1 = 0.0
+    sharded_cal = shard in ("heads", "clusters") or cfg.get("device_gen")
     if c1:
-        s = sqz.centroid_lookup(idx, Qc, scale, 0.0, 0.0, debug=True)
-        T1 = calib.weighted_threshold(s.dbg_S1.cpu().numpy(), idx.N1.cpu().numpy()[None], 0.5)
-    s = sqz.centroid_lookup(idx, Qc, scale, 0.0, T1, debug=True)
-    T = calib.weighted_threshold(s.dbg_S.cpu().numpy(), idx.N2.cpu().numpy()[None],
-                                 cfg["retention"], total_weight=Bc * H * L)
+        s = sqz.centroid_lookup(idx, Qc, scale, 0.0, 0.0, debug=True, comm=comm)
+        if sharded_cal:
+            T1 = calib.distributed_threshold(s.dbg_S1, idx.N1[None], 0.5, allsum(float(
+                Bc * idx.N1.sum())), allreduce=allsum)
+        else:
+            T1 = calib.weighted_threshold(s.dbg_S1.cpu().numpy(), idx.N1.cpu().numpy()[None], 0.5)
+    s = sqz.centroid_lookup(idx, Qc, scale, 0.0, T1, debug=True, comm=comm)
+    if sharded_cal:
+        T = calib.distributed_threshold(s.dbg_S, idx.N2[None], cfg["retention"], float(Bc * H * L),
+                                        allreduce=allsum)
+    else:
+        T = calib.weighted_threshold(s.dbg_S.cpu().numpy(), idx.N2.cpu().numpy()[None],
+                                     cfg["retention"], total_weight=Bc * H * L)
     del s, Qc
     # ---- per-step work: selection sizes for the algorithmic-byte count ----
     sel = sqz.Selection.empty(idx, B, n_q, False, dev)
     esz = 2 if dt == 1 else 4
-    ks, scanned = [], []
+    ks = []
     for i in range(n_inputs):
-        sqz.centroid_lookup(idx, Qt[i], scale, T, T1, sel=sel)
+        sqz.centroid_lookup(idx, Qt[i], scale, T, T1, sel=sel, comm=comm)
         ks.append(int(sel.n_keys.sum()))
     torch.cuda.synchronize()
-    k_mean = float(np.mean(ks))
-    # algorithmic bytes / flops
-    lookup_rows = c2 + c1  # rows scanned per head (hier: L2 restricted, approximated below)
-    bytes_lookup = H * (c1 if c1 else c2) * (d * esz + 4)
+    k_mean = float(np.mean(ks))  # this rank's selected keys per step
+    k_glob = allsum(k_mean)
+    # algorithmic bytes / flops of THIS rank
+    c1l, c2l = idx.c1, idx.c2
+    lookup_rows = c2l + c1l  # rows scanned per head (hier: L2 restricted, approximated below)
+    bytes_lookup = Hl * (c1l if c1l else c2l) * (d * esz + 4)
     if c1:
-        bytes_lookup += H * 0.5 * c2 * (d * esz + 4) * B  # ~50% of L2 rows scanned per query
-    bytes_attn = k_mean * 2 * d * esz + B * H * n_u * 2 * d * esz + 2 * B * H * n_q * d * esz
-    flops_attn = 4.0 * n_q * d * k_mean + 4.0 * d * B * H * (n_q * n_u - n_q * (n_q - 1) / 2)
-    flops_lookup = 2.0 * B * H * n_q * lookup_rows * d
-    O = torch.empty(B, H, n_q, d, dtype=sqz.torch_dtype(dt), device=dev)
-    LSE = torch.empty(B, H, n_q, dtype=torch.float32, device=dev)
+        bytes_lookup += Hl * 0.5 * c2l * (d * esz + 4) * B  # ~50% of L2 rows scanned per query
+    bytes_attn = k_mean * 2 * d * esz + B * Hl * n_u_r * 2 * d * esz + 2 * B * Hl * n_q * d * esz
+    flops_attn = 4.0 * n_q * d * k_mean + (4.0 * d * B * Hl * (n_q * n_u_r - n_q * (n_q - 1) / 2)
+                                          if n_u_r else 0.0)
+    flops_lookup = 2.0 * B * Hl * n_q * lookup_rows * d
+    O = torch.empty(B, Hl, n_q, d, dtype=sqz.torch_dtype(dt), device=dev)
+    LSE = torch.empty(B, Hl, n_q, dtype=torch.float32, device=dev)
+    Op = torch.empty(B, Hl, n_q, d, dtype=torch.float32, device=dev) if comm else None
+    Lp = torch.empty(B, Hl, n_q, dtype=torch.float32, device=dev) if comm else None
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    causal = cfg["mode"] == "prefill"
+
+    def attend(q):
+        if comm is None:
+            sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=causal, O=O, LSE=LSE)
+        else:  # partial over this shard, then the all-gather merge (P:361-363 across GPUs)
+            sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=causal, partial=True,
+                                 out_dtype=sqz.SQZ_F32, O=Op, LSE=Lp)
+            sqz.allgather_merge(comm, Op, Lp, out_dtype=dt, O=O, LSE=LSE)
 
     def step(i):
         q = Qt[i % n_inputs]
-        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel)
-        sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=cfg["mode"] == "prefill",
-                             O=O, LSE=LSE)
+        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel, comm=comm)
+        attend(q)
 
     for i in range(args.warmup):
         step(i)
@@ -355,10 +449,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
         flush.zero_()
         q = Qt[i % n_inputs]
         evp[i][0].record()
-        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel)
+        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel, comm=comm)
         evp[i][1].record()
-        sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale,
-                             causal=cfg["mode"] == "prefill", O=O, LSE=LSE)
+        attend(q)
         evp[i][2].record()
     torch.cuda.synchronize()
     t_look = sum(e[0].elapsed_time(e[1]) for e in evp) / K_
@@ -370,31 +463,31 @@ def run_gpu(args, cfg, rank, world, local_rank):
     hO = torch.empty(O.shape, dtype=O.dtype, **pin)
     hL = torch.empty(LSE.shape, dtype=LSE.dtype, **pin)
     dQ = torch.empty_like(Qt[0])
-    if cfg["mode"] == "decode":
+    hKn = hVn = None
+    if Ku is not None and cfg["mode"] == "decode":
         # the new token's k/v row enters the user cache each step
-        hKn = torch.empty(B, H, 1, d, dtype=Ku.dtype, **pin)
+        hKn = torch.empty(B, Hl, 1, d, dtype=Ku.dtype, **pin)
         hKn.copy_(Ku[:, :, -1:].cpu())
         hVn = torch.empty(hKn.shape, dtype=hKn.dtype, **pin)
         hVn.copy_(Vu[:, :, -1:].cpu())
-        h2d = hQ[0].numel() * esz + 2 * hKn.numel() * esz
-    else:
+    elif Ku is not None:
         hKn = torch.empty(Ku.shape, dtype=Ku.dtype, **pin)
         hKn.copy_(Ku.cpu())
         hVn = torch.empty(Vu.shape, dtype=Vu.dtype, **pin)
         hVn.copy_(Vu.cpu())
-        h2d = hQ[0].numel() * esz + 2 * hKn.numel() * esz
+    h2d = hQ[0].numel() * esz + (2 * hKn.numel() * esz if hKn is not None else 0)
     d2h = hO.numel() * O.element_size() + hL.numel() * 4
+
     def e2e_step(i):
         dQ.copy_(hQ[i % n_inputs], non_blocking=True)
-        if cfg["mode"] == "decode":
+        if hKn is not None and cfg["mode"] == "decode":
             Ku[:, :, -1:].copy_(hKn, non_blocking=True)
             Vu[:, :, -1:].copy_(hVn, non_blocking=True)
-        else:
+        elif hKn is not None:
             Ku.copy_(hKn, non_blocking=True)
             Vu.copy_(hVn, non_blocking=True)
-        sqz.centroid_lookup(idx, dQ, scale, T, T1, sel=sel)
-        sqz.sparse_attention(dQ, Kp, Vp, idx, sel, Ku, Vu, scale,
-                             causal=cfg["mode"] == "prefill", O=O, LSE=LSE)
+        sqz.centroid_lookup(idx, dQ, scale, T, T1, sel=sel, comm=comm)
+        attend(dQ)
         hO.copy_(O, non_blocking=True)
         hL.copy_(LSE, non_blocking=True)
 
@@ -422,7 +515,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step, t_look, t_attn, t_e2e, t_eager = tt.tolist()
     hbm, bf16, peak_kind = load_peaks()
-    tokens = B * n_q * world
+    # replicas: every rank runs its own step (weak); heads / clusters: the ranks
+    # share one step of B sequences (strong)
+    tokens = B * n_q * (world if shard in ("none", "replicas") else 1)
     if cfg["mode"] == "decode":
         value = t_step * 1e3 / tokens
         e2e_v = t_e2e * 1e3 / tokens
@@ -449,19 +544,29 @@ def run_gpu(args, cfg, rank, world, local_rank):
         step_flops = flops_attn + flops_lookup
         whole = {"flops_per_step": int(step_flops),
                  "achieved_TFLOPs": round(step_flops / (t_step * 1e-3) / 1e12, 2)}
-    n_lookup_k = (2 if c1 else 1) * (1 if cfg["mode"] == "decode" else 2)
-    launches = K_ * (n_lookup_k + 1)
+    # libsqz kernels per step (NCCL's own kernels not counted)
+    levels = 2 if c1 else 1
+    per_select = 1 if cfg["mode"] == "decode" else (2 if dt == 1 and d in (64, 128) else 3)
+    if comm is None:
+        n_look = levels * per_select
+    else:  # stats, then per level: fold + select (+ next level's stats)
+        n_look = 1 + levels * (1 + per_select) + (levels - 1)
+    launches = K_ * (n_look + 1 + (1 if comm else 0))
     metric, unit, hib = metric_of(cfg)
     line = {
         "metric": metric, "value": round(value, 3), "unit": unit, "n_gpus": world,
         "steps": K_, "warmup": args.warmup, "ms_per_step": round(t_step, 5),
-        "higher_is_better": hib, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": hib, "scaling": "weak" if shard in ("none", "replicas") else "strong",
+        "vs_baseline": None,
         "dtype": "bf16" if dt == 1 else "f32", "data": "synthetic (SYN-MIX v1 clustered keys)",
         "config": {"workload": cfg["workload"], "global_batch": B * world, "seq_len": L,
-                   "n_q": n_q, "n_u": n_u, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "n_q": n_q, "n_u": n_u,
+                   "parallelism": {"none": "1 GPU", "replicas": f"replicas x{world}",
+                                   "heads": f"heads sharded x{world}",
+                                   "clusters": f"fixed context sharded by cluster x{world}"}[shard],
                    "l2": "flushed (512 MB write) between timed steps",
-                   "T": T, "T1": T1, "mean_selected_keys_per_step": k_mean,
-                   "retention_realized": k_mean / (B * H * L), "kmeans_iters": list(iters),
+                   "T": T, "T1": T1, "mean_selected_keys_per_step": k_glob,
+                   "retention_realized": k_glob / (B * H * L), "kmeans_iters": list(iters),
                    "index_build_s": round(t_index, 2)},
         "phases_ms": {"lookup": round(t_look, 5), "sparse_attention": round(t_attn, 5),
                       "eager_step": round(t_eager, 5), "graph_replay": bool(args.graph)},
@@ -483,6 +588,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--kmeans-iters", type=int, default=30)
+    ap.add_argument("--kmeans-iters-set", type=int, default=None,
+                    help="override the per-config Lloyd iteration count (cfg5: 3)")
     ap.add_argument("--retention", type=float, default=None,
                     help="override the config's retention target (1.0 = T = 0, dense)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -39,3 +39,31 @@ def weighted_threshold(S, N, retention: float, total_weight: float = None) -> fl
     lower = lower[lower < hi]
     lo = lower[0] if len(lower) else 0.0
     return float(0.5 * (hi + lo))
+
+
+def distributed_threshold(S, N, retention: float, total_weight: float, allreduce=None,
+                          iters: int = 80) -> float:
+    """The same calibration when the scores are spread over ranks (head or
+    cluster shards): bisection on log T of the global retained weight
+    sum_{S > T} N (NaN = not scanned), each probe summed over the ranks by
+    `allreduce` (float -> float; identity on one process), so every rank gets
+    the identical T.  S, N: torch tensors (any device), N broadcastable to S."""
+    import torch
+
+    if retention >= 1.0:
+        return 0.0
+    S = S.double()
+    W = torch.broadcast_to(N.double(), S.shape)
+    ok = ~torch.isnan(S)
+    S, W = S[ok], W[ok]
+    red = allreduce or (lambda x: x)
+    target = retention * float(total_weight)
+    lo, hi = np.log(1e-30), np.log(2.0)  # retained(lo) >= target >= retained(hi)
+    for _ in range(iters):
+        mid = 0.5 * (lo + hi)
+        kept = red(float(W[S > np.exp(mid)].sum()))
+        if kept > target:
+            lo = mid
+        else:
+            hi = mid
+    return float(np.exp(0.5 * (lo + hi)))

@@ -281,14 +281,15 @@ static cudaError_t launch_expand(const LookupShape &s, const LevelArgs &lv, cuda
 // come from a DSMEM prefix over the ranks.  No global scratch round trip, no
 // serial last-CTA epilogue.
 // --------------------------------------------------------------------------
-constexpr int NC = 8;  // CTAs per cluster (portable maximum)
+// CTAs per cluster: 8 (portable maximum), or 16 (non-portable, B200) when the
+// row space is too large for 8 CTAs' shared memory (e.g. 52K Level-2 rows at 1M)
 
 template <int NB> struct DecodeSmem {
     float2 md[NB];
     int cnt[NB], keys[NB];
 };
 
-template <typename T, int D, int NB, bool ROWLIST>
+template <typename T, int D, int NB, bool ROWLIST, int NC>
 __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__restrict__ Q,
                                                       LevelArgs lv, int rpc) {
     namespace cg = cooperative_groups;
@@ -322,8 +323,11 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
     __shared__ float s_wm[NW][NB], s_wd[NW][NB];
 
     const int nrows = ROWLIST ? ldcg(lv.n_rows + (size_t)b0 * H + h) : c;
-    const int r0 = rank * rpc;
-    const int nloc = max(0, min(rpc, nrows - r0));
+    // a candidate list is split evenly over the cluster by its actual length
+    // (the smem is sized for the capacity rpc >= that share)
+    const int per = ROWLIST ? (nrows + NC - 1) / NC : rpc;
+    const int r0 = rank * per;
+    const int nloc = max(0, min(per, nrows - r0));
     const int32_t *rows = ROWLIST ? lv.rows + ((size_t)b0 * H + h) * lv.row_stride : nullptr;
     if (ROWLIST && lv.dbg_S) {  // rows outside the candidate list are "not scanned"
         const int per = (c + NC - 1) / NC;
@@ -352,6 +356,10 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
         }
     } else {
     // ---- scan: logits of the CTA's rows for the NB queries ----
+    if (ROWLIST) {  // the CTA's row ids in one coalesced pass (not one round trip per batch)
+        for (int rr = tid; rr < nloc; rr += NT) s_row[rr] = ldcg(rows + r0 + rr);
+        __syncthreads();
+    }
     float q[NB][D / 32];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
@@ -371,8 +379,7 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
         const int myrr = rr0 + lane;
         int myrow = -1;
         if (lane < U && myrr < nloc) {
-            myrow = ROWLIST ? ldcg(rows + r0 + myrr) : r0 + myrr;
-            s_row[myrr] = myrow;
+            myrow = ROWLIST ? s_row[myrr] : r0 + myrr;
             s_Nw[myrr] = (float)__ldg(N + myrow);
             s_o0[myrr] = __ldg(off + myrow);
             s_o1[myrr] = __ldg(off + myrow + 1);
@@ -705,15 +712,24 @@ __global__ void __launch_bounds__(NT) k_prefill_colsum(LookupShape s, const T *_
 }
 
 // --------------------------------------------------------------------------
-template <typename T, int D, int NB, bool RL>
-static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
-                                 int groups, cudaStream_t st) {
+constexpr size_t DECODE_SMEM_MAX = 200 * 1024;
+static bool decode_fits(int NB, int rowspace, int nc) {
+    return decode_smem_bytes(NB, (rowspace + nc - 1) / nc) <= DECODE_SMEM_MAX;
+}
+
+template <typename T, int D, int NB, bool RL, int NC>
+static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
+                                    int groups, cudaStream_t st) {
     const int rpc = (rowspace + NC - 1) / NC;
     const size_t smem = decode_smem_bytes(NB, rpc);
-    if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    auto kern = k_lookup_decode<T, D, NB, RL>;
+    if (smem > DECODE_SMEM_MAX) return cudaErrorInvalidValue;
+    auto kern = k_lookup_decode<T, D, NB, RL, NC>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    if (NC > 8) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t cfg = {};
@@ -738,6 +754,13 @@ static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelAr
     }
 #endif
     return cudaLaunchKernelEx(&cfg, kern, s, Q, lv, rpc);
+}
+
+template <typename T, int D, int NB, bool RL>
+static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
+                                 int groups, cudaStream_t st) {
+    if (decode_fits(NB, rowspace, 8)) return launch_decode_nc<T, D, NB, RL, 8>(s, Q, lv, rowspace, groups, st);
+    return launch_decode_nc<T, D, NB, RL, 16>(s, Q, lv, rowspace, groups, st);
 }
 
 // --------------------------------------------------------------------------
@@ -1109,10 +1132,14 @@ static cudaError_t launch_level_t(const LookupShape &s, const T *Q, const LevelA
     const int rowspace = rl ? lv.row_stride : lv.c;
     const int nch = (rowspace + CH - 1) / CH;
     if (s.n_q == 1) {
+        // queries per cluster: the largest NB <= B whose logits fit a 16-CTA cluster
         if (rl) return launch_decode<T, D, 1, true>(s, Q, lv, rowspace, s.B, st);
-        if (s.B >= 8) return launch_decode<T, D, 8, false>(s, Q, lv, rowspace, (s.B + 7) / 8, st);
-        if (s.B >= 4) return launch_decode<T, D, 4, false>(s, Q, lv, rowspace, (s.B + 3) / 4, st);
-        if (s.B >= 2) return launch_decode<T, D, 2, false>(s, Q, lv, rowspace, (s.B + 1) / 2, st);
+        if (s.B >= 8 && decode_fits(8, rowspace, 16))
+            return launch_decode<T, D, 8, false>(s, Q, lv, rowspace, (s.B + 7) / 8, st);
+        if (s.B >= 4 && decode_fits(4, rowspace, 16))
+            return launch_decode<T, D, 4, false>(s, Q, lv, rowspace, (s.B + 3) / 4, st);
+        if (s.B >= 2 && decode_fits(2, rowspace, 16))
+            return launch_decode<T, D, 2, false>(s, Q, lv, rowspace, (s.B + 1) / 2, st);
         return launch_decode<T, D, 1, false>(s, Q, lv, rowspace, s.B, st);
     }
     const int nqt = (s.n_q + QT - 1) / QT;

@@ -151,3 +151,123 @@ def kmeans_init(H, n, c, seed=2000):
 def centroid_counts(L, frac_fine=0.05, frac_coarse=0.01):
     """Centroid counts ceil(frac * L)."""
     return int(np.ceil(frac_coarse * L)), int(np.ceil(frac_fine * L))
+
+
+# --------------------------------------------------------------------------
+# Device-side SYN-MIX v1 (same recipe, torch Philox on the GPU) for the large
+# configurations (128K-1M keys x 32 heads), where host generation would take
+# minutes.  Not bit-identical to the numpy generator above (different RNG);
+# the parity tests use the host generator, the benches at 128K+ this one.
+# --------------------------------------------------------------------------
+@dataclass
+class DeviceMixture:
+    u: "torch.Tensor"      # [H,G,d] fp32 unit directions
+    pi: "torch.Tensor"     # [H,G] fp32 weights
+    beta: "torch.Tensor"   # [H] fp32 sharpness
+    rho: float
+    sigma: float
+
+
+def _torch_storage(x, dtype):
+    import torch
+
+    return x.to(torch.bfloat16 if dtype == BF16 else torch.float32)
+
+
+def device_mixture(H, G, d, G1=0, seed=1000, device="cuda", rho=4.0, beta_range=(0.5, 2.5)):
+    """The generating mixture of fixed_context(), drawn on the device."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    unit = lambda *s: torch.nn.functional.normalize(torch.randn(*s, generator=g, device=device), dim=-1)
+    if G1 > 0:
+        sup = unit(H, G1, d)
+        u = torch.nn.functional.normalize(sup[:, torch.arange(G, device=device) % G1] + 0.5 * unit(H, G, d),
+                                          dim=-1)
+    else:
+        u = unit(H, G, d)
+    e = -torch.log(torch.rand(H, G, generator=g, device=device).clamp_min(1e-30))  # Dirichlet(1)
+    pi = e / e.sum(-1, keepdim=True)
+    lo, hi = np.log(beta_range[0]), np.log(beta_range[1])
+    beta = torch.exp(lo + (hi - lo) * torch.rand(H, generator=g, device=device))
+    return DeviceMixture(u=u, pi=pi, beta=beta, rho=rho, sigma=rho / (2.0 * np.sqrt(d)))
+
+
+def device_keys(mix: DeviceMixture, L, seed, dtype=BF16, heads=None):
+    """K, V [len(heads), L, d] storage dtype on the mixture's device."""
+    import torch
+
+    dev = mix.u.device
+    heads = range(mix.u.shape[0]) if heads is None else heads
+    g = torch.Generator(device=dev).manual_seed(seed)
+    d = mix.u.shape[2]
+    K = torch.empty(len(heads), L, d, dtype=torch.bfloat16 if dtype == BF16 else torch.float32, device=dev)
+    V = torch.empty_like(K)
+    for i, h in enumerate(heads):
+        lab = torch.multinomial(mix.pi[h], L, replacement=True, generator=g)
+        K[i] = _torch_storage(mix.rho * mix.u[h][lab] + mix.sigma * torch.randn(L, d, generator=g, device=dev),
+                              dtype)
+        V[i] = _torch_storage(torch.randn(L, d, generator=g, device=dev), dtype)
+    return K, V
+
+
+def device_decode_queries(mix: DeviceMixture, B, seed, dtype=BF16, heads=None):
+    """decode_queries() on the device: Q [B, len(heads), 1, d]."""
+    import torch
+
+    dev = mix.u.device
+    heads = range(mix.u.shape[0]) if heads is None else heads
+    g = torch.Generator(device=dev).manual_seed(seed)
+    d = mix.u.shape[2]
+    Q = torch.empty(B, len(heads), 1, d, device=dev)
+    for i, h in enumerate(heads):
+        tp = torch.multinomial(mix.pi[h], 2 * B, replacement=True, generator=g).view(B, 2)
+        xi = torch.nn.functional.normalize(torch.randn(B, d, generator=g, device=dev), dim=-1)
+        v = mix.u[h][tp[:, 0]] + mix.u[h][tp[:, 1]] + 0.3 * xi
+        Q[:, i, 0] = mix.beta[h] * np.sqrt(d) * torch.nn.functional.normalize(v, dim=-1)
+    return _torch_storage(Q, dtype)
+
+
+def device_prefill_queries(mix: DeviceMixture, B, n_q, seed, dtype=BF16, heads=None):
+    """prefill_queries() on the device: Q [B, len(heads), n_q, d]."""
+    import torch
+
+    dev = mix.u.device
+    heads = range(mix.u.shape[0]) if heads is None else heads
+    g = torch.Generator(device=dev).manual_seed(seed)
+    d = mix.u.shape[2]
+    Q = torch.empty(B, len(heads), n_q, d, device=dev)
+    for b in range(B):
+        for i, h in enumerate(heads):
+            nt = int(torch.randint(2, 5, (1,), generator=g, device=dev))
+            topics = torch.multinomial(mix.pi[h], nt, replacement=True, generator=g)
+            pick = topics[torch.randint(0, nt, (n_q,), generator=g, device=dev)]
+            xi = torch.nn.functional.normalize(torch.randn(n_q, d, generator=g, device=dev), dim=-1)
+            v = torch.nn.functional.normalize(mix.u[h][pick] + 0.5 * xi, dim=-1)
+            Q[b, i] = mix.beta[h] * np.sqrt(d) * v
+    return _torch_storage(Q, dtype)
+
+
+def device_user_kv(mix: DeviceMixture, B, n_u, seed, dtype=BF16, heads=None):
+    """user_kv() on the device: Ku, Vu [B, len(heads), n_u, d]."""
+    import torch
+
+    dev = mix.u.device
+    heads = range(mix.u.shape[0]) if heads is None else heads
+    g = torch.Generator(device=dev).manual_seed(seed)
+    d = mix.u.shape[2]
+    Ku = torch.empty(B, len(heads), n_u, d, device=dev)
+    for b in range(B):
+        for i, h in enumerate(heads):
+            lab = torch.multinomial(mix.pi[h], n_u, replacement=True, generator=g)
+            Ku[b, i] = mix.rho * mix.u[h][lab] + mix.sigma * torch.randn(n_u, d, generator=g, device=dev)
+    Vu = torch.randn(B, len(heads), n_u, d, generator=g, device=dev)
+    return _torch_storage(Ku, dtype), _torch_storage(Vu, dtype)
+
+
+def device_kmeans_init(H, n, c, seed, device="cuda"):
+    """kmeans_init() on the device: [H, c] int64 distinct indices per head."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    return torch.stack([torch.randperm(n, generator=g, device=device)[:c] for _ in range(H)])
