@@ -309,15 +309,20 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
     const int32_t *off = lv.off + (size_t)h * (c + 1);
 
     extern __shared__ __align__(16) unsigned char dyn[];
+    // per-row arrays; with one query (NB == 1) the compaction writes its output
+    // in place over the row arrays (output position <= input position, and a
+    // tile's reads precede its writes), 20 B per row instead of 36
+    constexpr int NCMP = NB == 1 ? 0 : NB;                         // separate compaction arrays
     float *s_log = reinterpret_cast<float *>(dyn);                 // [NB][rpc]
     int *s_row = reinterpret_cast<int *>(s_log + NB * rpc);        // [rpc] (ROWLIST)
-    int *s_sel = s_row + rpc;                                      // [NB][rpc]
-    int *s_st = s_sel + NB * rpc;                                  // [NB][rpc]
-    int *s_n = s_st + NB * rpc;                                    // [NB][rpc]
-    int *s_kp = s_n + NB * rpc;                                    // [NB][rpc]
-    float *s_Nw = reinterpret_cast<float *>(s_kp + NB * rpc);      // [rpc] N of the row
+    float *s_Nw = reinterpret_cast<float *>(s_row + rpc);          // [rpc] N of the row
     int *s_o0 = reinterpret_cast<int *>(s_Nw + rpc);               // [rpc] off[row]
     int *s_o1 = s_o0 + rpc;                                        // [rpc] off[row + 1]
+    int *s_cmp = s_o1 + rpc;                                       // [4][NCMP][rpc]
+    int *s_sel = NB == 1 ? s_row : s_cmp;                          // [NB][rpc] selected row ids
+    int *s_st = NB == 1 ? s_o0 : s_cmp + NCMP * rpc;               // [NB][rpc] range starts
+    int *s_n = NB == 1 ? s_o1 : s_cmp + 2 * NCMP * rpc;            // [NB][rpc] range lengths
+    int *s_kp = NB == 1 ? reinterpret_cast<int *>(s_Nw) : s_cmp + 3 * NCMP * rpc;  // key offsets
     __shared__ DecodeSmem<NB> sh;
     __shared__ float s_M[NB], s_lD[NB];
     __shared__ float s_wm[NW][NB], s_wd[NW][NB];
@@ -583,7 +588,9 @@ cudaError_t launch_fold_stats(int P, const float2 *stats_in, int64_t n, float2 *
     return cudaGetLastError();
 }
 
-static size_t decode_smem_bytes(int NB, int rpc) { return (size_t)rpc * 4 * (NB + 4 + 4 * NB) + 16; }
+static size_t decode_smem_bytes(int NB, int rpc) {
+    return (size_t)rpc * 4 * (NB + 4 + (NB == 1 ? 0 : 4 * NB)) + 16;
+}
 
 // --------------------------------------------------------------------------
 // Prefill pass 1: LSE_t over the row space for every query row.
@@ -759,7 +766,9 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
 template <typename T, int D, int NB, bool RL>
 static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
                                  int groups, cudaStream_t st) {
-    if (decode_fits(NB, rowspace, 8)) return launch_decode_nc<T, D, NB, RL, 8>(s, Q, lv, rowspace, groups, st);
+    // 8-CTA clusters while a CTA's rows fit ~72 KB (3 CTAs per SM), else 16
+    if (decode_smem_bytes(NB, (rowspace + 7) / 8) <= 72 * 1024)
+        return launch_decode_nc<T, D, NB, RL, 8>(s, Q, lv, rowspace, groups, st);
     return launch_decode_nc<T, D, NB, RL, 16>(s, Q, lv, rowspace, groups, st);
 }
 
