@@ -8,6 +8,9 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["SQZ_NVCC_EXTRA"] = "-DSQZ_TRACE"
+from paper_2411_09688_b200 import build as bld  # noqa: E402
+bld.build(force=True)
 from paper_2411_09688_b200 import calib, sqz, synth  # noqa: E402
 
 ret = float(sys.argv[1]) if len(sys.argv) > 1 else 0.3

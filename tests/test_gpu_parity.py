@@ -123,6 +123,8 @@ DECODE_CASES = [
     ("bf16_d64_B9", 2, 2500, 64, 61, 0, synth.BF16, 9, 5, 0.2),
     ("hier_bf16", 3, 4000, 128, 200, 40, synth.BF16, 2, 33, 0.1),
     ("hier_fp32_B8", 2, 3000, 64, 150, 30, synth.F32, 8, 0, 0.15),
+    # B >= 4: Level 2 scans the whole table with per-query parent masks
+    ("hier_bf16_B5", 3, 4000, 128, 200, 40, synth.BF16, 5, 20, 0.1),
 ]
 
 

@@ -74,13 +74,12 @@ def _run_sharded(P, g, Kp, Vp, scale, T, T1, world):
     return Q, shards, sels
 
 
-@pytest.mark.parametrize("levels,prefill,world", [
-    (1, False, 1), (1, False, 2), (1, False, 3), (2, False, 2), (2, False, 4),
-    (1, True, 2), (2, True, 3)])
-def test_sharded_lookup_and_merge_match_oracle(levels, prefill, world):
+@pytest.mark.parametrize("levels,prefill,world,B", [
+    (1, False, 1, 2), (1, False, 2, 2), (1, False, 3, 2), (2, False, 2, 2), (2, False, 4, 2),
+    (2, False, 3, 5), (1, True, 2, 1), (2, True, 3, 1)])
+def test_sharded_lookup_and_merge_match_oracle(levels, prefill, world, B):
     sqz = _sqz()
-    P, idx, g, Kp, Vp, scale, T, T1 = _setup(levels, prefill, B=1 if prefill else 2,
-                                             n_q=200 if prefill else 1)
+    P, idx, g, Kp, Vp, scale, T, T1 = _setup(levels, prefill, B=B, n_q=200 if prefill else 1)
     Q, shards, sels = _run_sharded(P, g, Kp, Vp, scale, T, T1, world)
     B, H, n_q, d = Q.shape
     torch.cuda.synchronize()
