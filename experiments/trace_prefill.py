@@ -7,6 +7,9 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["SQZ_NVCC_EXTRA"] = "-DSQZ_TRACE"
+from paper_2411_09688_b200 import build as bld  # noqa: E402
+bld.build(force=True)
 from paper_2411_09688_b200 import calib, sqz, synth  # noqa: E402
 
 H, L, d, c, n_q = 32, 32768, 128, 1024, 1024

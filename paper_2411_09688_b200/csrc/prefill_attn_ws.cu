@@ -172,8 +172,12 @@ struct TmaMaps {
 // (masked; nkf4 = nkf rounded up to 4 when user keys follow, so that every TMA
 // gather4 group of 4 stream slots reads from one tensor), user keys
 // [nkf4, nkf4 + nuv)
+// Partition cost of a segment: its tiles plus SEG_W tiles' worth for the
+// per-piece setup/drain (Q load, pipeline fill, epilogue; measured ~3 tiles),
+// so CTAs holding many short segments are not the stragglers.
+constexpr int SEG_W = 3;
 struct Seg {
-    int bh, pair, nkf, nkf4, len, tiles;
+    int bh, pair, nkf, nkf4, len, tiles, cost;
 };
 __device__ __forceinline__ Seg seg_of(const AttnArgs &a, int npairs, int s) {
     Seg g;
@@ -186,6 +190,7 @@ __device__ __forceinline__ Seg seg_of(const AttnArgs &a, int npairs, int s) {
     g.nkf4 = nuv > 0 ? (g.nkf + 3) & ~3 : g.nkf;
     g.len = g.nkf4 + nuv;
     g.tiles = (g.len + ws::KT - 1) / ws::KT;
+    g.cost = g.tiles > 0 ? g.tiles + SEG_W : 0;
     return g;
 }
 // CTA owning global tile x when T tiles are cut into G equal ranges
@@ -206,7 +211,8 @@ struct PieceWalk {
             const bool last_cta = c == G - 1;
             if (st > hi || (st == hi && !last_cta)) return false;
             g = seg_of(a, npairs, s);
-            const long long st0 = st, en = st + g.tiles;
+            // cost units [st0, en): SEG_W setup units, then one unit per tile
+            const long long st0 = st, en = st + g.cost;
             const long long b = max(st0, lo), e = min(en, hi);
             seg_id = s;
             seg_st = st0;
@@ -220,9 +226,9 @@ struct PieceWalk {
                 continue;
             }
             if (e > b) {
-                pb = (int)(b - st0);
-                pe = (int)(e - st0);
-                return true;
+                pb = (int)max(0LL, b - st0 - SEG_W);
+                pe = (int)max(0LL, e - st0 - SEG_W);
+                if (pe > pb) return true;  // (a range holding only setup units skips it)
             }
         }
         return false;
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(ws::NT, 1)
     const int R = (nseg + NT - 1) / NT;
     const int sb = min(nseg, tid * R), se = min(nseg, sb + R);
     long long run = 0;
-    for (int s = sb; s < se; ++s) run += seg_of(a, npairs, s).tiles;
+    for (int s = sb; s < se; ++s) run += seg_of(a, npairs, s).cost;
     scan[tid] = run;
     if (tid == 0) {
         misc[1] = nseg;
@@ -280,14 +286,16 @@ __global__ void __launch_bounds__(ws::NT, 1)
     const long long T = scan[NT - 1];
     // at most one CTA per tile, so every CTA range is non-empty and the owners of
     // a segment's tiles are consecutive CTAs each holding one piece of it
-    const int G = (int)(T < 1 ? 1 : (T < (long long)gridDim.x ? T : (long long)gridDim.x));
+    // (>= SEG_W + 1 units per CTA, so a CTA range never lies inside one segment's setup units)
+    const long long Gmax = T / (SEG_W + 1);
+    const int G = (int)(Gmax < 1 ? 1 : (Gmax < (long long)gridDim.x ? Gmax : (long long)gridDim.x));
     if (c >= G) return;
     const long long lo = T * c / G, hi = T * (c + 1) / G;
     {
         // first segment of this CTA: the first s that is not (entirely before lo)
         long long st = scan[tid] - run;
         for (int s = sb; s < se; ++s) {
-            const long long en = st + seg_of(a, npairs, s).tiles;
+            const long long en = st + seg_of(a, npairs, s).cost;
             if (!(en <= lo && st < lo)) {
                 atomicMin(&misc[1], s);
                 break;
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(ws::NT, 1)
         const int s0 = misc[1];
         if (s0 >= sb && s0 < se) {
             long long st = scan[tid] - run;
-            for (int s = sb; s < s0; ++s) st += seg_of(a, npairs, s).tiles;
+            for (int s = sb; s < s0; ++s) st += seg_of(a, npairs, s).cost;
             misc64[0] = st;
         }
     }
@@ -591,7 +599,8 @@ __global__ void __launch_bounds__(ws::NT, 1)
             mbar_wait(&o_fin[g], piece & 1);
             ++piece;
             tc_fence_after();
-            const int c0 = owner_of(walk.seg_st, T, G), c1 = owner_of(walk.seg_st + sg.tiles - 1, T, G);
+            const int c0 = owner_of(walk.seg_st + SEG_W, T, G),
+                      c1 = owner_of(walk.seg_st + SEG_W + sg.tiles - 1, T, G);
             const bool have = row_ok && l > 0.f;
             const float inv_l = have ? 1.0f / l : 0.f;
             const float lse = have ? (m_used + log2f(l)) * LN2 : -INFINITY;
@@ -658,32 +667,34 @@ __global__ void __launch_bounds__(ws::NT, 1)
     WS_TRACE(tid == 0, 0, 21);
     WS_CTA_T(1);
     if (warp == 0) tmem_dealloc(tmem, 512);
-    // ---- tickets: the CTA completing a cut segment's last piece merges it ----
-    if (tid == 0) {
-        for (int k = 0; k < 2; ++k) {
-            misc[8 + k] = 0;
-            const int s = misc[6 + k];
-            if (s < 0) continue;
-            const int c0 = misc[10 + 2 * k], c1 = misc[11 + 2 * k];
-            int *cnt = a.row_cnt + s;
-            const int t = atomicAdd(cnt, 1);
-            if (t == c1 - c0) {
-                *cnt = 0;
-                misc[8 + k] = 1;
-            }
-        }
-    }
+    // ---- cut segments: every CTA holding a piece of one merges an equal slice of
+    // its rows once all pieces are written (grid = one resident CTA per SM, so
+    // waiting on the other pieces cannot deadlock); the merge's memory traffic is
+    // spread over the segment's CTAs instead of landing on one SM ----
+    int *done_cnt = a.row_cnt + nseg;  // second self-cleaning counter per segment
+    if (tid == 0)
+        for (int k = 0; k < 2; ++k)
+            if (misc[6 + k] >= 0) atomicAdd(a.row_cnt + misc[6 + k], 1);
     __syncthreads();
     float *wgt = reinterpret_cast<float *>(sm + OFF_K);  // [parts][256] merge weights (rings are dead)
     for (int k = 0; k < 2; ++k) {
-        if (!misc[8 + k]) continue;
-        __threadfence();
-        const int s = misc[6 + k], c0 = misc[10 + 2 * k], c1 = misc[11 + 2 * k];
+        const int s = misc[6 + k];
+        if (s < 0) continue;
+        const int c0 = misc[10 + 2 * k], c1 = misc[11 + 2 * k];
         const int np = c1 - c0 + 1;
+        if (tid == 0) {
+            volatile int *cnt = a.row_cnt + s;
+            while (*cnt < np) __nanosleep(200);
+        }
+        __syncthreads();
+        __threadfence();
         const int bh = s / npairs, pair = s - bh * npairs;
-        const int nrow = min(PR, a.n_q - pair * PR);
-        const float *lse_p = a.part_lse + (size_t)(s + c0) * PR;  // part p, row rr: lse_p[p * PR + rr]
-        const float *o_p = a.part_o + (size_t)(s + c0) * PR * D;
+        const int nrow_seg = min(PR, a.n_q - pair * PR);
+        const int r_lo = (c - c0) * nrow_seg / np, r_hi = (c - c0 + 1) * nrow_seg / np;
+        const int nrow = r_hi - r_lo;
+        const float *lse_p = a.part_lse + (size_t)(s + c0) * PR + r_lo;  // part p, row rr: lse_p[p * PR + rr]
+        const float *o_p = a.part_o + ((size_t)(s + c0) * PR + r_lo) * D;
+        const int row0 = pair * PR + r_lo;
         for (int rr = tid; rr < nrow; rr += NT) {
             float M = -INFINITY;
             for (int p = 0; p < np; ++p) M = fmaxf(M, ldcg(lse_p + (size_t)p * PR + rr));
@@ -695,7 +706,7 @@ __global__ void __launch_bounds__(ws::NT, 1)
             }
             const float inv = M == -INFINITY ? 0.f : 1.f / L;
             for (int p = 0; p < np; ++p) wgt[p * PR + rr] *= inv;
-            const size_t orow = (size_t)bh * a.n_q + pair * PR + rr;
+            const size_t orow = (size_t)bh * a.n_q + row0 + rr;
             a.LSE[orow] = M == -INFINITY ? -INFINITY : M + logf(L);
             if (M == -INFINITY && !a.partial) atomicOr(a.status, 1);
         }
@@ -729,7 +740,7 @@ __global__ void __launch_bounds__(ws::NT, 1)
                 acc.z = fmaf(w, o.z, acc.z);
                 acc.w = fmaf(w, o.w, acc.w);
             }
-            const size_t orow = (size_t)bh * a.n_q + pair * PR + rr;
+            const size_t orow = (size_t)bh * a.n_q + row0 + rr;
             if (a.out_dtype == SQZ_BF16) {
                 __nv_bfloat162 *dst = reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<__nv_bfloat16 *>(a.O) + orow * D + ch * 4);
                 dst[0] = __floats2bfloat162_rn(acc.x, acc.y);
@@ -739,6 +750,13 @@ __global__ void __launch_bounds__(ws::NT, 1)
             }
         }
         __syncthreads();
+        if (tid == 0) {  // the last CTA done with this segment resets both counters
+            __threadfence();
+            if (atomicAdd(done_cnt + s, 1) == np - 1) {
+                a.row_cnt[s] = 0;
+                done_cnt[s] = 0;
+            }
+        }
     }
     WS_TRACE(tid == 0, 0, 22);
     WS_CTA_T(2);
