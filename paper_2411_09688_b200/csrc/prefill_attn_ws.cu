@@ -38,8 +38,8 @@ namespace sqz {
 
 namespace ws {
 constexpr int D = 128;
-constexpr int MMAW = 8;               // MMA warp index (warps 9-11 idle in the main loop)
-constexpr int NWK = 4, NWV = 2;       // K loader warps 9, 10, 12, 13; V loader warps 14, 15
+constexpr int MMAW = 8;               // MMA warp index
+constexpr int NWK = 4, NWV = 3;       // K loader warps 9, 10, 12, 13; V loader warps 11, 14, 15
 constexpr int NT = 512;               // 16 warps = 4 warpgroups
 constexpr int QT = 128;               // rows per query tile
 constexpr int PR = 2 * QT;            // rows per segment (query-tile pair)
@@ -143,9 +143,9 @@ __device__ __forceinline__ void tmem_st32f(uint32_t taddr, const float *v) {
 }
 
 // NW warps gather a 64-row K/V tile into the SW128 layout.  Warp w (0..NW-1)
-// copies rows 2(w + NW j) + (lane/16), j < 32/NW, 16-byte chunk lane%16; the
-// row's key position is held by lane 2j + (lane/16) of the same warp and
-// broadcast by shuffle.
+// copies row pairs w + NW j (< KT/2), rows 2(w + NW j) + (lane/16), 16-byte
+// chunk lane%16; the row's key position is held by lane 2j + (lane/16) of the
+// same warp and broadcast by shuffle.
 template <int NW>
 __device__ __forceinline__ void gather_rows(uint32_t dst, const __nv_bfloat16 *fixed,
                                             const __nv_bfloat16 *user, int pos_mine, int w, int lane) {
@@ -153,9 +153,10 @@ __device__ __forceinline__ void gather_rows(uint32_t dst, const __nv_bfloat16 *f
     const int hh = lane >> 4, c = lane & 15;
     const uint32_t coff = (uint32_t)((c >> 3) * HBK);
 #pragma unroll
-    for (int j = 0; j < KT / (2 * NW); ++j) {
+    for (int j = 0; j < (KT / 2 + NW - 1) / NW; ++j) {
         const int pos = __shfl_sync(FULL, pos_mine, 2 * j + hh);
         const int row = 2 * (w + NW * j) + hh;
+        if (w + NW * j >= KT / 2) break;  // (NW not dividing 32: the last round is partial)
         const bool valid = pos != INVALID;
         const __nv_bfloat16 *src = pos >= 0 ? fixed + (size_t)pos * D : user + (size_t)(-1 - pos) * D;
         cp_async16_zfill(dst + coff + sw128_off(row, c & 7), valid ? src + c * 8 : fixed, valid);
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(ws::NT, 1)
     WS_TRACE(tid == 0, 0, 20);
 
     const int kw = warp == 9 ? 0 : warp == 10 ? 1 : (warp == 12 || warp == 13) ? warp - 10 : -1;
-    const int vw = warp >= 14 ? warp - 14 : -1;
+    const int vw = warp == 11 ? 0 : warp >= 14 ? warp - 13 : -1;
     if (kw >= 0 || vw >= 0) {
         // ======================= loaders =======================
         // K/V rows gathered by key position with 16-byte cp.async (a TMA gather4
@@ -473,8 +474,6 @@ __global__ void __launch_bounds__(ws::NT, 1)
             }
         }
         __syncwarp();
-    } else if (warp > MMAW) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");  // idle warp 11
     } else {
         // ======================= softmax groups =======================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
