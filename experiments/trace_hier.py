@@ -8,7 +8,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["SQZ_NVCC_EXTRA"] = "-DSQZ_TRACE"
+os.environ["SQZ_NVCC_EXTRA"] = "-DSQZ_TRACE " + os.environ.get("TRACE_EXTRA", "")
 from paper_2411_09688_b200 import build as bld  # noqa: E402
 bld.build(force=True)
 from paper_2411_09688_b200 import calib, sqz, synth  # noqa: E402

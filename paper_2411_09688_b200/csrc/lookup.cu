@@ -69,31 +69,57 @@ constexpr int QT = 64;      // prefill queries per tile (8 warps x 8 queries)
 int lookup_chunk_rows() { return CH; }
 int lookup_qtile() { return QT; }
 
-// lane-slice loads: lane holds D/32 consecutive elements of a row
+// lane-slice loads: lane holds D/32 consecutive elements of a row.  `Raw` is the
+// stored form (bf16 stays packed in registers until used, so a warp can keep
+// twice as many rows in flight), `cvt` widens it to fp32 exactly.
 template <typename T, int D> struct Lane;
 template <> struct Lane<__nv_bfloat16, 128> {
-    static __device__ __forceinline__ void load(const __nv_bfloat16 *row, int lane, float (&f)[4]) {
-        uint2 u = __ldg(reinterpret_cast<const uint2 *>(row) + lane);
+    using Raw = uint2;
+    static __device__ __forceinline__ Raw load_raw(const __nv_bfloat16 *row, int lane) {
+        return __ldg(reinterpret_cast<const uint2 *>(row) + lane);
+    }
+    static __device__ __forceinline__ void cvt(const Raw &u, float (&f)[4]) {
         f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xffff0000u);
         f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xffff0000u);
     }
+    static __device__ __forceinline__ void load(const __nv_bfloat16 *row, int lane, float (&f)[4]) {
+        cvt(load_raw(row, lane), f);
+    }
 };
 template <> struct Lane<__nv_bfloat16, 64> {
-    static __device__ __forceinline__ void load(const __nv_bfloat16 *row, int lane, float (&f)[2]) {
-        uint32_t u = __ldg(reinterpret_cast<const uint32_t *>(row) + lane);
+    using Raw = uint32_t;
+    static __device__ __forceinline__ Raw load_raw(const __nv_bfloat16 *row, int lane) {
+        return __ldg(reinterpret_cast<const uint32_t *>(row) + lane);
+    }
+    static __device__ __forceinline__ void cvt(const Raw &u, float (&f)[2]) {
         f[0] = __uint_as_float(u << 16); f[1] = __uint_as_float(u & 0xffff0000u);
+    }
+    static __device__ __forceinline__ void load(const __nv_bfloat16 *row, int lane, float (&f)[2]) {
+        cvt(load_raw(row, lane), f);
     }
 };
 template <> struct Lane<float, 128> {
-    static __device__ __forceinline__ void load(const float *row, int lane, float (&f)[4]) {
-        float4 u = __ldg(reinterpret_cast<const float4 *>(row) + lane);
+    using Raw = float4;
+    static __device__ __forceinline__ Raw load_raw(const float *row, int lane) {
+        return __ldg(reinterpret_cast<const float4 *>(row) + lane);
+    }
+    static __device__ __forceinline__ void cvt(const Raw &u, float (&f)[4]) {
         f[0] = u.x; f[1] = u.y; f[2] = u.z; f[3] = u.w;
+    }
+    static __device__ __forceinline__ void load(const float *row, int lane, float (&f)[4]) {
+        cvt(load_raw(row, lane), f);
     }
 };
 template <> struct Lane<float, 64> {
-    static __device__ __forceinline__ void load(const float *row, int lane, float (&f)[2]) {
-        float2 u = __ldg(reinterpret_cast<const float2 *>(row) + lane);
+    using Raw = float2;
+    static __device__ __forceinline__ Raw load_raw(const float *row, int lane) {
+        return __ldg(reinterpret_cast<const float2 *>(row) + lane);
+    }
+    static __device__ __forceinline__ void cvt(const Raw &u, float (&f)[2]) {
         f[0] = u.x; f[1] = u.y;
+    }
+    static __device__ __forceinline__ void load(const float *row, int lane, float (&f)[2]) {
+        cvt(load_raw(row, lane), f);
     }
 };
 
@@ -290,7 +316,7 @@ template <int NB> struct DecodeSmem {
 };
 
 template <typename T, int D, int NB, bool ROWLIST, int NC>
-__global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__restrict__ Q,
+__global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T *__restrict__ Q,
                                                       LevelArgs lv, int rpc) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -373,10 +399,12 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
 #pragma unroll
             for (int k = 0; k < D / 32; ++k) q[i][k] = 0.f;
     }
-    // A warp loads U = 16 rows at once (one memory round trip), forms the
-    // U x NB partial dot products, and reduces them 16 at a time with the
-    // transposed butterfly: value v = row_local * NB + query.
-    constexpr int U = 16;
+    // A warp loads U rows at once (one memory round trip; U = 32 for packed bf16
+    // rows with one or two queries, whose raw rows take the registers 16 fp32
+    // rows would), forms the U x NB partial dot products, and reduces them 16 at
+    // a time with the transposed butterfly: value v = row_local * NB + query.
+    using LaneT = Lane<T, D>;
+    constexpr int U = (sizeof(T) == 2 && NB <= 2) ? 32 : 16;
     constexpr int RPT = 16 / NB;  // rows per 16-value transpose
     for (int rr0 = warp * U; rr0 < nloc; rr0 += NW * U) {
         // lane l < U owns row rr0 + l: its id and its N / key-range metadata are
@@ -389,30 +417,34 @@ __global__ void __launch_bounds__(NT) k_lookup_decode(LookupShape s, const T *__
             s_o0[myrr] = __ldg(off + myrow);
             s_o1[myrr] = __ldg(off + myrow + 1);
         }
-        float cf[U][D / 32];
-        int rowid[U];
+        typename LaneT::Raw raw[U];
+        bool have[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            rowid[u] = __shfl_sync(FULL, myrow, u);
-            if (rowid[u] >= 0) {
-                Lane<T, D>::load(C + (size_t)rowid[u] * D, lane, cf[u]);
-            } else {
-#pragma unroll
-                for (int k = 0; k < D / 32; ++k) cf[u][k] = 0.f;
-            }
+            const int rid = __shfl_sync(FULL, myrow, u);
+            have[u] = rid >= 0;
+            if (have[u]) raw[u] = LaneT::load_raw(C + (size_t)rid * D, lane);
         }
 #pragma unroll
         for (int gq = 0; gq < U / RPT; ++gq) {
             float v[16];
 #pragma unroll
-            for (int u = 0; u < RPT; ++u)
+            for (int u = 0; u < RPT; ++u) {
+                float cf[D / 32];
+                if (have[gq * RPT + u]) {
+                    LaneT::cvt(raw[gq * RPT + u], cf);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < D / 32; ++k) cf[k] = 0.f;
+                }
 #pragma unroll
                 for (int i = 0; i < NB; ++i) {
                     float acc = 0.f;
 #pragma unroll
-                    for (int k = 0; k < D / 32; ++k) acc = fmaf(q[i][k], cf[gq * RPT + u][k], acc);
+                    for (int k = 0; k < D / 32; ++k) acc = fmaf(q[i][k], cf[k], acc);
                     v[u * NB + i] = acc;
                 }
+            }
             const float sv = transpose_reduce<16>(v, lane) * s.scale;
             const int vi = transpose_index<16>(lane);
             const int rr = rr0 + gq * RPT + vi / NB;
