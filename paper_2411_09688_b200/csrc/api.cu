@@ -131,7 +131,7 @@ LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base, int worl
 // ---------------- attention workspace ----------------
 struct AttnWs {
     float *part_o, *part_lse;
-    int32_t *status, *row_cnt;
+    int32_t *status, *row_cnt, *cut;
     int32_t kch, max_chunks;
     size_t bytes;
 };
@@ -143,6 +143,7 @@ AttnWs attn_carve(const sqz_index *idx, int B, int n_q, int n_u, char *base) {
     const size_t rows = (size_t)B * idx->H * n_q;
     w.status = cv.take<int32_t>(64);
     w.row_cnt = cv.take<int32_t>(rows);
+    w.cut = cv.take<int32_t>(4 + 3 * 1024);
     // partial rows: [rows, max_chunks] for the split-KV kernels, one 256-row slot
     // per piece for the persistent prefill kernel
     const size_t prow = prefill_ws_applies(idx->d, idx->dtype, n_q)
@@ -437,6 +438,7 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
     a.kch = w.kch; a.max_chunks = w.max_chunks;
     a.part_o = w.part_o; a.part_lse = w.part_lse; a.status = w.status; a.row_cnt = w.row_cnt;
     a.sched = w.status + 1;
+    a.cut = w.cut;
     a.O = O; a.LSE = LSE;
     cudaError_t e = launch_attention(a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "sparse attention launch");

@@ -78,6 +78,7 @@ struct AttnArgs {
     int32_t *status;  // [1]
     int32_t *row_cnt; // [rows] self-cleaning tile tickets
     int32_t *sched;   // [2] dynamic tile counter + finished-CTA counter (self-cleaning)
+    int32_t *cut;     // [4 + 3 * 1024] cut-segment list of the persistent prefill kernel
     void *O;
     float *LSE;
 };

@@ -666,99 +666,122 @@ __global__ void __launch_bounds__(ws::NT, 1)
     WS_TRACE(tid == 0, 0, 21);
     WS_CTA_T(1);
     if (warp == 0) tmem_dealloc(tmem, 512);
-    // ---- cut segments: every CTA holding a piece of one merges an equal slice of
-    // its rows once all pieces are written (grid = one resident CTA per SM, so
-    // waiting on the other pieces cannot deadlock); the merge's memory traffic is
-    // spread over the segment's CTAs instead of landing on one SM ----
-    int *done_cnt = a.row_cnt + nseg;  // second self-cleaning counter per segment
-    if (tid == 0)
-        for (int k = 0; k < 2; ++k)
-            if (misc[6 + k] >= 0) atomicAdd(a.row_cnt + misc[6 + k], 1);
-    __syncthreads();
-    float *wgt = reinterpret_cast<float *>(sm + OFF_K);  // [parts][256] merge weights (rings are dead)
-    for (int k = 0; k < 2; ++k) {
-        const int s = misc[6 + k];
-        if (s < 0) continue;
-        const int c0 = misc[10 + 2 * k], c1 = misc[11 + 2 * k];
-        const int np = c1 - c0 + 1;
-        if (tid == 0) {
-            volatile int *cnt = a.row_cnt + s;
-            while (*cnt < np) __nanosleep(200);
-        }
-        __syncthreads();
-        __threadfence();
-        const int bh = s / npairs, pair = s - bh * npairs;
-        const int nrow_seg = min(PR, a.n_q - pair * PR);
-        const int r_lo = (c - c0) * nrow_seg / np, r_hi = (c - c0 + 1) * nrow_seg / np;
-        const int nrow = r_hi - r_lo;
-        const float *lse_p = a.part_lse + (size_t)(s + c0) * PR + r_lo;  // part p, row rr: lse_p[p * PR + rr]
-        const float *o_p = a.part_o + ((size_t)(s + c0) * PR + r_lo) * D;
-        const int row0 = pair * PR + r_lo;
-        for (int rr = tid; rr < nrow; rr += NT) {
-            float M = -INFINITY;
-            for (int p = 0; p < np; ++p) M = fmaxf(M, ldcg(lse_p + (size_t)p * PR + rr));
-            float L = 0.f;
-            for (int p = 0; p < np; ++p) {
-                const float w = M == -INFINITY ? 0.f : expf(ldcg(lse_p + (size_t)p * PR + rr) - M);
-                wgt[p * PR + rr] = w;
-                L += w;
-            }
-            const float inv = M == -INFINITY ? 0.f : 1.f / L;
-            for (int p = 0; p < np; ++p) wgt[p * PR + rr] *= inv;
-            const size_t orow = (size_t)bh * a.n_q + row0 + rr;
-            a.LSE[orow] = M == -INFINITY ? -INFINITY : M + logf(L);
-            if (M == -INFINITY && !a.partial) atomicOr(a.status, 1);
-        }
-        __syncthreads();
-        // item = (row, 4-dim chunk); loads independent across parts and items
-        for (int it = tid; it < nrow * (D / 4); it += NT) {
-            const int rr = it / (D / 4), ch = it % (D / 4);
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            int p = 0;
-            for (; p + 4 <= np; p += 4) {
-                float4 o[4];
-                float w[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    o[q] = __ldcg(reinterpret_cast<const float4 *>(o_p + ((size_t)(p + q) * PR + rr) * D) + ch);
-                    w[q] = wgt[(p + q) * PR + rr];
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    acc.x = fmaf(w[q], o[q].x, acc.x);
-                    acc.y = fmaf(w[q], o[q].y, acc.y);
-                    acc.z = fmaf(w[q], o[q].z, acc.z);
-                    acc.w = fmaf(w[q], o[q].w, acc.w);
-                }
-            }
-            for (; p < np; ++p) {
-                const float4 o = __ldcg(reinterpret_cast<const float4 *>(o_p + ((size_t)p * PR + rr) * D) + ch);
-                const float w = wgt[p * PR + rr];
-                acc.x = fmaf(w, o.x, acc.x);
-                acc.y = fmaf(w, o.y, acc.y);
-                acc.z = fmaf(w, o.z, acc.z);
-                acc.w = fmaf(w, o.w, acc.w);
-            }
-            const size_t orow = (size_t)bh * a.n_q + row0 + rr;
-            if (a.out_dtype == SQZ_BF16) {
-                __nv_bfloat162 *dst = reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<__nv_bfloat16 *>(a.O) + orow * D + ch * 4);
-                dst[0] = __floats2bfloat162_rn(acc.x, acc.y);
-                dst[1] = __floats2bfloat162_rn(acc.z, acc.w);
-            } else {
-                reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.O) + orow * D)[ch] = acc;
-            }
-        }
-        __syncthreads();
-        if (tid == 0) {  // the last CTA done with this segment resets both counters
-            __threadfence();
-            if (atomicAdd(done_cnt + s, 1) == np - 1) {
-                a.row_cnt[s] = 0;
-                done_cnt[s] = 0;
+    // ---- cut segments are merged by k_merge_cut (next launch, all SMs): the
+    // first piece's owner c0 lists (segment, c0, c1) ----
+    if (tid == 0) {
+        asm volatile("griddepcontrol.launch_dependents;");
+        for (int k = 0; k < 2; ++k) {
+            const int s = misc[6 + k];
+            if (s >= 0 && misc[10 + 2 * k] == c) {
+                const int slot = atomicAdd(a.cut, 1);
+                a.cut[4 + 3 * slot] = s;
+                a.cut[5 + 3 * slot] = misc[10 + 2 * k];
+                a.cut[6 + 3 * slot] = misc[11 + 2 * k];
             }
         }
     }
     WS_TRACE(tid == 0, 0, 22);
     WS_CTA_T(2);
+}
+
+// Merge of the cut segments' pieces: CTA (k, slice) merges rows
+// [slice * 64, +64) of the k-th listed segment from its pieces' (O/l, lse)
+// partials.  Launched with programmatic stream serialization after the main
+// kernel; the last CTA resets the list counter (self-cleaning workspace).
+constexpr int MERGE_ROWS = 64;
+__global__ void __launch_bounds__(256) k_merge_cut(AttnArgs a, int npairs) {
+    using namespace ws;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ float wgt[8][MERGE_ROWS];  // up to 8 pieces in registers' worth of weights
+    __shared__ int s_last;
+    const int tid = threadIdx.x;
+    const int ncut = ldcg(a.cut);
+    const int k = blockIdx.x;
+    if (k < ncut) {
+        const int s = ldcg(a.cut + 4 + 3 * k), c0 = ldcg(a.cut + 5 + 3 * k), c1 = ldcg(a.cut + 6 + 3 * k);
+        const int np = c1 - c0 + 1;
+        const int bh = s / npairs, pair = s - bh * npairs;
+        const int nrow_seg = min(PR, a.n_q - pair * PR);
+        const int r_lo = blockIdx.y * MERGE_ROWS, nrow = min(MERGE_ROWS, nrow_seg - r_lo);
+        if (nrow > 0) {
+            const float *lse_p = a.part_lse + (size_t)(s + c0) * PR + r_lo;
+            const float *o_p = a.part_o + ((size_t)(s + c0) * PR + r_lo) * D;
+            const int row0 = pair * PR + r_lo;
+            float *wg = &wgt[0][0];
+            const bool small = np <= 8;
+            if (tid < nrow) {
+                const int rr = tid;
+                float M = -INFINITY;
+                for (int p = 0; p < np; ++p) M = fmaxf(M, ldcg(lse_p + (size_t)p * PR + rr));
+                float L = 0.f;
+                for (int p = 0; p < np; ++p) {
+                    const float w = M == -INFINITY ? 0.f : expf(ldcg(lse_p + (size_t)p * PR + rr) - M);
+                    if (small) wg[p * MERGE_ROWS + rr] = w;
+                    L += w;
+                }
+                const float inv = M == -INFINITY ? 0.f : 1.f / L;
+                if (small)
+                    for (int p = 0; p < np; ++p) wg[p * MERGE_ROWS + rr] *= inv;
+                const size_t orow = (size_t)bh * a.n_q + row0 + rr;
+                a.LSE[orow] = M == -INFINITY ? -INFINITY : M + logf(L);
+                if (M == -INFINITY && !a.partial) atomicOr(a.status, 1);
+            }
+            __syncthreads();
+            for (int it = tid; it < nrow * (D / 4); it += blockDim.x) {
+                const int rr = it / (D / 4), ch = it % (D / 4);
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                float4 o[8];
+#pragma unroll
+                for (int p = 0; p < 8; ++p)
+                    if (p < np) o[p] = __ldcg(reinterpret_cast<const float4 *>(o_p + ((size_t)p * PR + rr) * D) + ch);
+                float wsum_inv = 1.f;
+                if (!small) {  // > 8 pieces (never at the configured sizes): recompute the weights
+                    float M = -INFINITY;
+                    for (int p = 0; p < np; ++p) M = fmaxf(M, ldcg(lse_p + (size_t)p * PR + rr));
+                    float L = 0.f;
+                    for (int p = 0; p < np; ++p) {
+                        const float w = M == -INFINITY ? 0.f : expf(ldcg(lse_p + (size_t)p * PR + rr) - M);
+                        L += w;
+                        const float4 op = __ldcg(reinterpret_cast<const float4 *>(o_p + ((size_t)p * PR + rr) * D) + ch);
+                        acc.x = fmaf(w, op.x, acc.x);
+                        acc.y = fmaf(w, op.y, acc.y);
+                        acc.z = fmaf(w, op.z, acc.z);
+                        acc.w = fmaf(w, op.w, acc.w);
+                    }
+                    wsum_inv = L > 0.f ? 1.f / L : 0.f;
+                } else {
+#pragma unroll
+                    for (int p = 0; p < 8; ++p)
+                        if (p < np) {
+                            const float w = wg[p * MERGE_ROWS + rr];
+                            acc.x = fmaf(w, o[p].x, acc.x);
+                            acc.y = fmaf(w, o[p].y, acc.y);
+                            acc.z = fmaf(w, o[p].z, acc.z);
+                            acc.w = fmaf(w, o[p].w, acc.w);
+                        }
+                }
+                acc.x *= wsum_inv; acc.y *= wsum_inv; acc.z *= wsum_inv; acc.w *= wsum_inv;
+                const size_t orow = (size_t)bh * a.n_q + row0 + rr;
+                if (a.out_dtype == SQZ_BF16) {
+                    __nv_bfloat162 *dst = reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<__nv_bfloat16 *>(a.O) + orow * D + ch * 4);
+                    dst[0] = __floats2bfloat162_rn(acc.x, acc.y);
+                    dst[1] = __floats2bfloat162_rn(acc.z, acc.w);
+                } else {
+                    reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.O) + orow * D)[ch] = acc;
+                }
+            }
+        }
+    }
+    // self-cleaning: the last CTA resets the list counter
+    __syncthreads();
+    if (tid == 0) {
+        const int t = atomicAdd(a.cut + 1, 1);
+        s_last = t == (int)(gridDim.x * gridDim.y) - 1;
+        if (s_last) {
+            a.cut[0] = 0;
+            a.cut[1] = 0;
+        }
+    }
 }
 
 namespace {
@@ -833,7 +856,14 @@ cudaError_t launch_prefill_attention_ws(const AttnArgs &a, cudaStream_t st) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_prefill_attend_ws, a, npairs, maps);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_prefill_attend_ws, a, npairs, maps);
+    if (e != cudaSuccess) return e;
+    // merge of the cut segments on all SMs (at most one cut per CTA boundary)
+    cudaLaunchConfig_t mc = cfg;
+    mc.gridDim = dim3(ws_grid(), ws::PR / MERGE_ROWS);
+    mc.blockDim = dim3(256);
+    mc.dynamicSmemBytes = 0;
+    return cudaLaunchKernelEx(&mc, k_merge_cut, a, npairs);
 }
 
 }  // namespace sqz
