@@ -54,16 +54,18 @@ if ws:
             last = min(pr * 256 + 256, n_q) - 1
             nuv = max(0, min(last + 1, n_q))  # causal, n_u == n_q
             nkf4 = (int(nk[bh]) + 3) // 4 * 4 if nuv else int(nk[bh])
-            seg_t.append((nkf4 + nuv + 127) // 128)
+            seg_t.append((nkf4 + nuv + 63) // 64)
     seg_t = np.array(seg_t)
-    st = np.concatenate([[0], np.cumsum(seg_t)])
+    SEG_W = 6
+    seg_c = np.where(np.array(seg_t) > 0, np.array(seg_t) + SEG_W, 0)
+    st = np.concatenate([[0], np.cumsum(seg_c)])
     Ttot = int(st[-1])
     print(f"segments {len(seg_t)} tiles min/med/max {seg_t.min()}/{int(np.median(seg_t))}/{seg_t.max()} total {Ttot}")
-    for cta in (0, 64, 113):
+    for cta in [int(i) for i in order[:6]] + [int(order[-1])]:
         lo_, hi_ = Ttot * cta // n, Ttot * (cta + 1) // n
-        pcs = [(si, int(max(st[si], lo_) - st[si]), int(min(st[si + 1], hi_) - st[si]), int(seg_t[si]))
+        pcs = [(si, max(0, int(max(st[si], lo_) - st[si]) - SEG_W), max(0, int(min(st[si + 1], hi_) - st[si]) - SEG_W), int(seg_t[si]))
                for si in range(len(seg_t)) if st[si + 1] > lo_ and st[si] < hi_]
-        print(f"CTA {cta}: tiles [{lo_},{hi_}) pieces (seg, from, to, seg_tiles): {pcs}")
+        print(f"CTA {cta} (loop end {lend[cta]:.1f}): units [{lo_},{hi_}) pieces (seg, from, to, seg_tiles): {pcs}")
     print("slowest CTAs:", [(int(i), round(ex[i], 1), round(lend[i], 1)) for i in order[:12]])
     f = 1.965e3
     print(f"entry 0  scan+setup {(tr[0,20]-t0)/f:.2f}  loop end {(tr[0,21]-t0)/f:.2f}  exit {(tr[0,22]-t0)/f:.2f} us")

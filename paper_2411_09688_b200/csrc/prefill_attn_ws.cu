@@ -174,9 +174,10 @@ struct TmaMaps {
 // gather4 group of 4 stream slots reads from one tensor), user keys
 // [nkf4, nkf4 + nuv)
 // Partition cost of a segment: its tiles plus SEG_W tiles' worth for the
-// per-piece setup/drain (Q load, pipeline fill, epilogue; measured ~3 tiles),
+// per-piece setup/drain (Q load, pipeline fill, epilogue; fitted ~6 tiles on cfg3;
+// 3 and 8 were slower),
 // so CTAs holding many short segments are not the stragglers.
-constexpr int SEG_W = 3;
+constexpr int SEG_W = 6;
 struct Seg {
     int bh, pair, nkf, nkf4, len, tiles, cost;
 };
