@@ -371,7 +371,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                      cfg["retention"], total_weight=Bc * H * L)
     del s, Qc
     # ---- per-step work: selection sizes for the algorithmic-byte count ----
-    sel = sqz.Selection.empty(idx, B, n_q, False, dev)
+    # the expanded key-index tensor is materialised: the attention kernels' run-length
+    # reader (key_idx=False) measured slower than the lookup's expansion on every config
+    sel = sqz.Selection.empty(idx, B, n_q, False, dev, key_idx=True)
     esz = 2 if dt == 1 else 4
     ks = []
     for i in range(n_inputs):

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQZ_ABI_VERSION 2
+#define SQZ_ABI_VERSION 3
 
 enum {
     SQZ_OK = 0,
@@ -164,9 +164,14 @@ typedef struct {
  *              the first n_clusters[b,h] entries are valid
  *   n_clusters [B, H] int32
  *   n_keys     [B, H] int32: k = sum of N_i over the selected clusters
- *   key_idx    [B, H, L] int32: cluster-major positions (into Kp/Vp) of the
- *              selected keys, ascending; the first n_keys[b,h] are valid.
- *              This is the paper's key-index tensor.
+ *   key_pref   [B, H, c2] int32: the key-index tensor of P:354 in run-length
+ *              form: the selected keys are the runs [key_off[h][clusters[j]],
+ *              + N) of Kp/Vp, and key_pref[j] = sum of N over clusters[0..j) is
+ *              the first key of run j in the (b,h)'s selection stream.
+ *              sqz_sparse_attention reads the runs (no O(k) index tensor).
+ *   key_idx    optional [B, H, L] int32: the same selection expanded, one
+ *              cluster-major position (into Kp/Vp) per selected key, ascending;
+ *              the first n_keys[b,h] are valid.  NULL: not materialised.
  *   l1_surv    optional [B, H, c1] uint8: Level-1 survivors (levels == 2)
  *   dbg_S      optional [B, H, c2] fp32: finest-level S_i (decode) or S-bar_i
  *              (prefill) as the kernel evaluated it, NaN for rows not scanned
@@ -182,6 +187,7 @@ typedef struct {
     float *dbg_S;
     float *dbg_S1;
     float *dbg_lse;
+    int32_t *key_pref;
 } sqz_selection;
 
 int sqz_lookup_workspace(const sqz_index *idx, int32_t B, int32_t n_q, size_t *ws_bytes);
@@ -237,7 +243,8 @@ int sqz_attention_workspace(const sqz_index *idx, int32_t B, int32_t n_q, int32_
                             size_t *ws_bytes);
 
 /* Q [B,H,n_q,d] dtype; Kp, Vp [H,L,d] dtype (cluster-major); sel: output of
- * sqz_centroid_lookup (n_keys and key_idx are read); Ku, Vu [B,H,n_u,d] dtype
+ * sqz_centroid_lookup (n_keys, n_clusters, clusters and key_pref are read, with
+ * idx->key_off; key_idx is not needed); Ku, Vu [B,H,n_u,d] dtype
  * (may be NULL when n_u == 0).  Outputs: O [B,H,n_q,d] out_dtype and
  * LSE [B,H,n_q] fp32 = natural-log sum of exp(z) over the attended keys.
  * For each query row the attended set is the selected fixed keys of its (b,h)

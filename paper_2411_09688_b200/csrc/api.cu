@@ -254,8 +254,8 @@ static int lookup_check(const sqz_index *idx, const void *Q, int32_t B, int32_t 
     if (idx->levels == 2 && (!(p->T1 >= 0.f) || std::isinf(p->T1)))
         return fail(SQZ_ERR_INVALID_ARG, "T1 = %g must be finite and >= 0", (double)p->T1);
     if (!std::isfinite(p->scale)) return fail(SQZ_ERR_INVALID_ARG, "scale must be finite");
-    if (!out || !out->clusters || !out->n_clusters || !out->n_keys || !out->key_idx)
-        return fail(SQZ_ERR_INVALID_ARG, "selection outputs clusters/n_clusters/n_keys/key_idx required");
+    if (!out || !out->clusters || !out->n_clusters || !out->n_keys || !out->key_pref)
+        return fail(SQZ_ERR_INVALID_ARG, "selection outputs clusters/n_clusters/n_keys/key_pref required");
     if (!ws) return fail(SQZ_ERR_INVALID_ARG, "ws is NULL");
     return SQZ_OK;
 }
@@ -271,7 +271,8 @@ static void lookup_levels(const sqz_index *idx, const sqz_lookup_params *p, cons
     l2.T = p->T;
     l2.list = out->clusters;
     l2.n_list = out->n_clusters;
-    l2.exp_list = out->key_idx;
+    l2.exp_list = out->key_idx;  // optional expansion
+    l2.sel_pref = out->key_pref;
     l2.n_exp = out->n_keys;
     l2.exp_stride = idx->L;
     l2.dbg_S = out->dbg_S;
@@ -417,8 +418,11 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
     if (n_u > 0 && (!Ku || !Vu)) return fail(SQZ_ERR_INVALID_ARG, "Ku, Vu required when n_u > 0");
     if (n_u > 0 && (!aligned16(Ku) || !aligned16(Vu)))
         return fail(SQZ_ERR_INVALID_ARG, "Ku, Vu must be 16-byte aligned");
-    if (!sel || !sel->n_keys || !sel->key_idx)
-        return fail(SQZ_ERR_INVALID_ARG, "sel->n_keys and sel->key_idx are required");
+    if (!sel || !sel->n_keys ||
+        (!sel->key_idx && (!sel->clusters || !sel->n_clusters || !sel->key_pref || !idx->key_off)))
+        return fail(SQZ_ERR_INVALID_ARG,
+                    "sel->n_keys and either sel->key_idx or (sel->clusters, n_clusters, key_pref, "
+                    "idx->key_off) are required");
     if (!p) return fail(SQZ_ERR_INVALID_ARG, "params is NULL");
     if (p->out_dtype != SQZ_F32 && p->out_dtype != SQZ_BF16)
         return fail(SQZ_ERR_INVALID_ARG, "out_dtype = %d is not a sqz_dtype", p->out_dtype);
@@ -432,6 +436,8 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
     std::memset(&a, 0, sizeof(a));
     a.Q = Q; a.Kp = Kp; a.Vp = Vp; a.Ku = Ku; a.Vu = Vu;
     a.n_keys = sel->n_keys; a.key_idx = sel->key_idx;
+    a.sel_cl = sel->clusters; a.sel_pref = sel->key_pref; a.sel_n = sel->n_clusters;
+    a.key_off = idx->key_off; a.c2 = idx->c2;
     a.B = B; a.H = idx->H; a.n_q = n_q; a.n_u = n_u; a.d = idx->d; a.dtype = idx->dtype;
     a.causal = p->causal ? 1 : 0; a.partial = p->partial ? 1 : 0; a.out_dtype = p->out_dtype;
     a.L = idx->L; a.scale = p->scale;

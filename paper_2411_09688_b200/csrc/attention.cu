@@ -314,9 +314,32 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
         const T *Vf = reinterpret_cast<const T *>(a.Vp) + (size_t)ri.h * a.L * D;
         const T *Ku = reinterpret_cast<const T *>(a.Ku) + (size_t)ri.bh * a.n_u * D;
         const T *Vu = reinterpret_cast<const T *>(a.Vu) + (size_t)ri.bh * a.n_u * D;
-        const int32_t *kidx = a.key_idx + (size_t)ri.bh * a.L;
-        // source position of stream key k: >= 0 fixed key row, < 0 user key -1-u
-        auto pos_of = [&](int k) -> int {
+        const int32_t *kidx = a.key_idx ? a.key_idx + (size_t)ri.bh * a.L : nullptr;
+        RunList rl;
+        RunWin rw;
+        if (!kidx) {
+            rl.cl = a.sel_cl + (size_t)ri.bh * a.c2;
+            rl.pref = a.sel_pref + (size_t)ri.bh * a.c2;
+            rl.koff = a.key_off + (size_t)ri.h * (a.c2 + 1);
+            rl.n = ldcg(a.sel_n + ri.bh);
+            rl.nkf = ri.nkf;
+            rw.J = 0;
+            rw.end = -1;  // empty: the first cover loads
+            rw.p0 = rw.p1 = 0x7fffffff;
+        }
+        // source position of stream key k (this lane's key of a warp round starting
+        // at stream key j): >= 0 fixed key row, < 0 user key -1-u.  Warp-collective.
+        auto pos_of = [&](int j, int k) -> int {
+            if (!kidx) {
+                const int kmax = min(min(j + KR, sg.a1), ri.nkf) - 1;
+                if (j <= kmax) {  // warp-uniform
+                    runwin_cover(rw, rl, j, kmax, lane);
+                    const int p = runwin_pos(rw, min(k, kmax));
+                    if (k <= kmax) return p;
+                }
+                if (k >= sg.a1) return 0;
+                return -1 - (k - ri.nkf);
+            }
             if (k >= sg.a1) return 0;
             return k < ri.nkf ? ldcg(kidx + k) : -1 - (k - ri.nkf);
         };
@@ -331,7 +354,7 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
 
         // lane l (< KR) holds the position of key l of this warp's current round
         int j0 = sg.a0 + warp * KR;
-        int pos_cur = pos_of(j0 + (lane & (KR - 1)));
+        int pos_cur = pos_of(j0, j0 + (lane & (KR - 1)));
         for (; j0 < sg.a1; j0 += NCW * KR) {
             const int nk = min(KR, sg.a1 - j0);
             Raw<T> kr[NS], vr[NS];
@@ -351,7 +374,7 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
                 }
             }
             // prefetch the next round's positions while this round's rows are in flight
-            pos_cur = pos_of(j0 + NCW * KR + (lane & (KR - 1)));
+            pos_cur = pos_of(j0 + NCW * KR, j0 + NCW * KR + (lane & (KR - 1)));
             float v[NS];
 #pragma unroll
             for (int s = 0; s < NS; ++s) {

@@ -79,6 +79,70 @@ __device__ __forceinline__ float exp_fast(float x) { return fast_exp2(x * LOG2E)
 // ld.global that bypasses L1 (data written by other CTAs of this launch).
 template <typename T> __device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
 
+// ---- run-length selection streams (sqz_selection.key_pref) ------------------
+// The selected keys of one (b,h) are the runs j < n: stream keys
+// [pref[j], pref[j+1]) (pref[n] = nkf) at cluster-major positions
+// key_off[cl[j]] + (k - pref[j]).
+struct RunList {
+    const int32_t *cl, *pref, *koff;
+    int n, nkf;
+};
+// A warp's window of 64 consecutive runs [J, J + 64): lane m holds runs J + m
+// and J + 32 + m (first stream key, cluster-major start); `end` is the first
+// stream key past the window.  Locating a key is a 6-step shuffle search.
+struct RunWin {
+    int J, end;
+    int p0, p1, s0, s1;
+};
+__device__ __forceinline__ void runwin_load(RunWin &w, const RunList &r, int J, int lane) {
+    w.J = J;
+    const int j0 = J + lane, j1 = J + 32 + lane;
+    w.p0 = j0 < r.n ? ldcg(r.pref + j0) : 0x7fffffff;
+    w.p1 = j1 < r.n ? ldcg(r.pref + j1) : 0x7fffffff;
+    const int c0 = j0 < r.n ? ldcg(r.cl + j0) : 0, c1 = j1 < r.n ? ldcg(r.cl + j1) : 0;
+    w.end = J + 64 < r.n ? ldcg(r.pref + J + 64) : r.nkf;
+    w.s0 = j0 < r.n ? __ldg(r.koff + c0) : 0;
+    w.s1 = j1 < r.n ? __ldg(r.koff + c1) : 0;
+}
+// run index (absolute) of stream key k < nkf, by binary search over the list
+__device__ __forceinline__ int run_of(const RunList &r, int k) {
+    int lo = 0, hi = r.n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ldcg(r.pref + mid) <= k) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+// make the window hold the runs of stream keys [kmin, kmax] (warp-uniform,
+// kmin <= kmax < nkf; at most 64 runs apart)
+__device__ __forceinline__ void runwin_cover(RunWin &w, const RunList &r, int kmin, int kmax, int lane) {
+    const int first = __shfl_sync(FULL, w.p0, 0);
+    if (kmin >= first && kmax < w.end) return;
+    int J;
+    if (kmin >= first && kmin < w.end) {  // slide: the run of kmin is in the window
+        const unsigned b0 = __ballot_sync(FULL, w.p0 <= kmin), b1 = __ballot_sync(FULL, w.p1 <= kmin);
+        J = w.J + __popc(b0) + __popc(b1) - 1;
+    } else {
+        J = run_of(r, kmin);
+    }
+    runwin_load(w, r, J, lane);
+}
+// cluster-major position of stream key k (the window must cover k)
+__device__ __forceinline__ int runwin_pos(const RunWin &w, int k) {
+    int m = 0;  // last window slot with first key <= k
+#pragma unroll
+    for (int step = 32; step >= 1; step >>= 1) {
+        const int cand = m + step;
+        const int v0 = __shfl_sync(FULL, w.p0, cand & 31), v1 = __shfl_sync(FULL, w.p1, cand & 31);
+        const int v = cand < 32 ? v0 : v1;
+        if (cand < 64 && v <= k) m = cand;
+    }
+    const int q0 = __shfl_sync(FULL, w.p0, m & 31), q1 = __shfl_sync(FULL, w.p1, m & 31);
+    const int t0 = __shfl_sync(FULL, w.s0, m & 31), t1 = __shfl_sync(FULL, w.s1, m & 31);
+    return (m < 32 ? t0 : t1) + (k - (m < 32 ? q0 : q1));
+}
+
 }  // namespace sqz
 
 // ---- optional device-side timeline tracing (experiments only: -DSQZ_TRACE) ----

@@ -69,6 +69,9 @@ int lookup_qtile();
 struct AttnArgs {
     const void *Q, *Kp, *Vp, *Ku, *Vu;
     const int32_t *n_keys, *key_idx;
+    // run-length selection (sqz_selection.key_pref): used when key_idx is null
+    const int32_t *sel_cl, *sel_pref, *sel_n, *key_off;
+    int32_t c2;
     int32_t B, H, n_q, n_u, d, dtype, causal, partial, out_dtype;
     int64_t L;
     float scale;

@@ -579,8 +579,13 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         const int oc = s_oc[i], ok = s_ok[i];
         const int mine = sh.cnt[i];
         int32_t *list = lv.list + (size_t)bh * c + oc;
-        int32_t *exp_list = lv.exp_list + (size_t)bh * lv.exp_stride + ok;
-        for (int j = tid; j < mine; j += NT) list[j] = s_sel[i * rpc + j];
+        int32_t *exp_list = lv.exp_list ? lv.exp_list + (size_t)bh * lv.exp_stride + ok : nullptr;
+        int32_t *kpref = lv.sel_pref + (size_t)bh * c + oc;  // run-length key offsets
+        for (int j = tid; j < mine; j += NT) {
+            list[j] = s_sel[i * rpc + j];
+            kpref[j] = ok + s_kp[i * rpc + j];
+        }
+        if (exp_list)
         for (int j = warp; j < mine; j += NW) {
             const int st = s_st[i * rpc + j], n = s_n[i * rpc + j], kp = s_kp[i * rpc + j];
             for (int t = lane; t < n; t += 32) exp_list[kp + t] = st + t;
@@ -1155,7 +1160,7 @@ static cudaError_t launch_prefill_tc(const LookupShape &s, const __nv_bfloat16 *
     dim3 grid((s.n_q + PL_T - 1) / PL_T, s.B * s.H);
     kern<<<grid, PL_NT, PlSmem<D>::BYTES, st>>>(s, Q, lv, maps);
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess && lv.phase != 1) e = launch_expand(s, lv, st);
+    if (e == cudaSuccess && lv.phase != 1 && lv.exp_list) e = launch_expand(s, lv, st);
     return e;
 }
 
@@ -1196,7 +1201,7 @@ static cudaError_t launch_level_t(const LookupShape &s, const T *Q, const LevelA
         if (lv.phase != 1) k_prefill_colsum<T, D, false><<<g2, NT, 0, st>>>(s, Q, lv);
     }
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess && lv.phase != 1) e = launch_expand(s, lv, st);
+    if (e == cudaSuccess && lv.phase != 1 && lv.exp_list) e = launch_expand(s, lv, st);
     return e;
 }
 

@@ -121,10 +121,23 @@ __global__ void __launch_bounds__(PF_NT, 1) k_prefill_attend(AttnArgs a, int qti
     const __nv_bfloat16 *Vf = reinterpret_cast<const __nv_bfloat16 *>(a.Vp) + (size_t)h * a.L * D;
     const __nv_bfloat16 *Ku = reinterpret_cast<const __nv_bfloat16 *>(a.Ku) + (size_t)bh * a.n_u * D;
     const __nv_bfloat16 *Vu = reinterpret_cast<const __nv_bfloat16 *>(a.Vu) + (size_t)bh * a.n_u * D;
-    const int32_t *kidx = a.key_idx + (size_t)bh * a.L;
+    const int32_t *kidx = a.key_idx ? a.key_idx + (size_t)bh * a.L : nullptr;
+    RunList rl;  // run-length selection when key_idx is not materialised
+    if (!kidx) {
+        rl.cl = a.sel_cl + (size_t)bh * a.c2;
+        rl.pref = a.sel_pref + (size_t)bh * a.c2;
+        rl.koff = a.key_off + (size_t)h * (a.c2 + 1);
+        rl.n = ldcg(a.sel_n + bh);
+        rl.nkf = nkf;
+    }
     const int k_begin = split * PF_SPLIT, k_end = min(len, k_begin + PF_SPLIT);
     const int ntile = (k_end - k_begin + PF_KT - 1) / PF_KT;
-    auto pos_of = [&](int k) -> int { return k < nkf ? ldcg(kidx + k) : -1 - (k - nkf); };
+    auto pos_of = [&](int k) -> int {
+        if (k >= nkf) return -1 - (k - nkf);
+        if (kidx) return ldcg(kidx + k);
+        const int j = run_of(rl, k);  // (d = 64 path: a plain search per key)
+        return __ldg(rl.koff + ldcg(rl.cl + j)) + (k - ldcg(rl.pref + j));
+    };
 
     // Q tile (rows beyond n_q zero-filled)
     for (int e = tid; e < PF_QT * CPR; e += PF_NT) {

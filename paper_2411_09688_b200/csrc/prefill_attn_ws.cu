@@ -367,15 +367,38 @@ __global__ void __launch_bounds__(ws::NT, 1)
             const int h = g.bh % a.H;
             const __nv_bfloat16 *Fx = reinterpret_cast<const __nv_bfloat16 *>(isK ? a.Kp : a.Vp) + (size_t)h * a.L * D;
             const __nv_bfloat16 *Us = reinterpret_cast<const __nv_bfloat16 *>(isK ? a.Ku : a.Vu) + (size_t)g.bh * a.n_u * D;
-            const int32_t *kidx = a.key_idx + (size_t)g.bh * a.L;
-            // stream slot -> key position (>= 0 fixed, < 0 user), INVALID when masked
-            auto pos_of = [&](int k) -> int {
+            const int32_t *kidx = a.key_idx ? a.key_idx + (size_t)g.bh * a.L : nullptr;
+            RunList rl;
+            RunWin rw;
+            if (!kidx) {
+                rl.cl = a.sel_cl + (size_t)g.bh * a.c2;
+                rl.pref = a.sel_pref + (size_t)g.bh * a.c2;
+                rl.koff = a.key_off + (size_t)h * (a.c2 + 1);
+                rl.n = ldcg(a.sel_n + g.bh);
+                rl.nkf = g.nkf;
+                rw.J = 0;
+                rw.end = -1;
+                rw.p0 = rw.p1 = 0x7fffffff;
+            }
+            // stream slot -> key position (>= 0 fixed, < 0 user), INVALID when masked;
+            // warp-collective (k0 uniform: the tile's first slot)
+            auto pos_of = [&](int k0, int k) -> int {
+                int p = INVALID;
+                if (!kidx) {
+                    const int kmax = min(k0 + KT, g.nkf) - 1;
+                    if (k0 <= kmax) {  // warp-uniform
+                        runwin_cover(rw, rl, k0, kmax, lane);
+                        p = runwin_pos(rw, min(k, kmax));
+                    }
+                } else if (k < g.nkf) {
+                    p = ldcg(kidx + k);
+                }
                 if (k >= g.len || (k >= g.nkf && k < g.nkf4)) return INVALID;
-                return k < g.nkf ? ldcg(kidx + k) : -1 - (k - g.nkf4);
+                return k < g.nkf ? p : -1 - (k - g.nkf4);
             };
             for (int tt = pb; tt < pe; ++tt, ++tau) {
                 const int st = tau % nst, k0 = tt * KT;
-                const int pA = pos_of(k0 + rA);
+                const int pA = pos_of(k0, k0 + rA);
                 if (tau >= nst) mbar_wait(&empty[st], ((tau / nst) - 1) & 1);
                 WS_TRACE(w == 0 && lane == 0, tau, isK ? 10 : 11);
                 if (isK)

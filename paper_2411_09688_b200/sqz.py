@@ -25,7 +25,7 @@ SO = os.path.join(HERE, "libsqz.so")
 SQZ_F32, SQZ_BF16 = 0, 1
 SQZ_OK, SQZ_ERR_INVALID_ARG, SQZ_ERR_FORMAT, SQZ_ERR_INVARIANT = 0, 2, 3, 4
 SQZ_ERR_CUDA, SQZ_ERR_NCCL, SQZ_ERR_EMPTY, SQZ_ERR_UNSUPPORTED = 5, 6, 7, 8
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 EXPORTS = [
     "sqz_cluster_keys_workspace", "sqz_cluster_keys", "sqz_index_validate_workspace",
@@ -65,7 +65,7 @@ class sqz_lookup_params(ctypes.Structure):
 class sqz_selection(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
                 ("clusters", "n_clusters", "n_keys", "key_idx", "l1_surv", "dbg_S", "dbg_S1",
-                 "dbg_lse")]
+                 "dbg_lse", "key_pref")]
 
 
 class sqz_attn_params(ctypes.Structure):
@@ -249,20 +249,26 @@ class Selection:
     clusters: torch.Tensor
     n_clusters: torch.Tensor
     n_keys: torch.Tensor
-    key_idx: torch.Tensor
+    key_idx: torch.Tensor          # optional expanded key positions (None: runs only)
     l1_surv: torch.Tensor = None
     dbg_S: torch.Tensor = None
     dbg_S1: torch.Tensor = None
     dbg_lse: torch.Tensor = None
+    key_pref: torch.Tensor = None  # run-length key offsets of the selected clusters
 
     @staticmethod
-    def empty(idx: Index, B, n_q, debug=False, device="cuda"):
+    def empty(idx: Index, B, n_q, debug=False, device="cuda", key_idx=True):
+        """Output buffers of a lookup.  key_idx=False leaves the selection in its
+        run-length form (clusters + key_pref), which sqz_sparse_attention reads
+        directly; True also materialises the expanded key positions."""
         i32 = dict(dtype=torch.int32, device=device)
         f32 = dict(dtype=torch.float32, device=device)
         H = idx.H
         return Selection(
             clusters=torch.empty(B, H, idx.c2, **i32), n_clusters=torch.empty(B, H, **i32),
-            n_keys=torch.empty(B, H, **i32), key_idx=torch.empty(B, H, idx.L, **i32),
+            n_keys=torch.empty(B, H, **i32),
+            key_idx=torch.empty(B, H, idx.L, **i32) if key_idx else None,
+            key_pref=torch.empty(B, H, idx.c2, **i32),
             l1_surv=torch.empty(B, H, idx.c1, dtype=torch.uint8, device=device)
             if (debug and idx.c1) else None,
             dbg_S=torch.empty(B, H, idx.c2, **f32) if debug else None,

@@ -116,6 +116,30 @@ def _device(P):
     return t
 
 
+def _check_runs(t, sel, O, LSE, scale, T, T1, causal, partial):
+    """The run-length selection (key_pref, no key_idx) gives the same selection and
+    bit-identical attention: key_pref is the exclusive prefix of N over the
+    selected clusters, and the attention kernels read the same positions."""
+    sqz = _sqz()
+    B, H = sel.n_keys.shape
+    r = sqz.Selection.empty(t["idx"], B, t["Q"].shape[2], key_idx=False)
+    sqz.centroid_lookup(t["idx"], t["Q"], scale, T, T1, sel=r)
+    O2, L2 = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], r, t["Ku"], t["Vu"], scale,
+                                  causal=causal, partial=partial)
+    torch.cuda.synchronize()
+    assert torch.equal(r.n_clusters, sel.n_clusters) and torch.equal(r.n_keys, sel.n_keys)
+    N2 = t["idx"].N2.cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            n = int(sel.n_clusters[b, h])
+            cl = sel.clusters[b, h, :n].cpu().numpy()
+            assert np.array_equal(r.clusters[b, h, :n].cpu().numpy(), cl)
+            pref = np.concatenate([[0], np.cumsum(N2[h][cl])[:-1]]) if n else np.zeros(0)
+            assert np.array_equal(r.key_pref[b, h, :n].cpu().numpy(), pref)
+            assert np.array_equal(sel.key_pref[b, h, :n].cpu().numpy(), pref)
+    assert torch.equal(O2, O) and torch.equal(L2, LSE), "run-length attention differs"
+
+
 DECODE_CASES = [
     # id, H, L, d, c2, c1, dtype, B, n_u, retention
     ("cfg1_fp32", 1, 1024, 64, 32, 0, synth.F32, 1, 16, 0.3),
@@ -145,6 +169,7 @@ def test_decode_lookup_and_attention(case):
     fp32 = dt == synth.F32
     _check_attention(P, sel, O, LSE, scale, False, B, 1e-4 if fp32 else 2e-2,
                      None if fp32 else 5e-3)
+    _check_runs(t, sel, O, LSE, scale, T, T1, False, True)
 
 
 PREFILL_CASES = [
@@ -179,6 +204,7 @@ def test_prefill_lookup_and_attention(case):
     fp32 = dt == synth.F32
     _check_attention(P, sel, O, LSE, scale, causal, B, 1e-4 if fp32 else 2e-2,
                      None if fp32 else 5e-3)
+    _check_runs(t, sel, O, LSE, scale, T, T1, causal, False)
 
 
 def test_threshold_zero_is_dense_attention():
