@@ -143,7 +143,7 @@ AttnWs attn_carve(const sqz_index *idx, int B, int n_q, int n_u, char *base) {
     const size_t rows = (size_t)B * idx->H * n_q;
     w.status = cv.take<int32_t>(64);
     w.row_cnt = cv.take<int32_t>(rows);
-    w.cut = cv.take<int32_t>(4 + 3 * 1024);
+    w.cut = cv.take<int32_t>(3 * 1024);  // one (segment, c0, c1) slot per persistent CTA
     // partial rows: [rows, max_chunks] for the split-KV kernels, one 256-row slot
     // per piece for the persistent prefill kernel
     const size_t prow = prefill_ws_applies(idx->d, idx->dtype, n_q)

@@ -81,7 +81,7 @@ struct AttnArgs {
     int32_t *status;  // [1]
     int32_t *row_cnt; // [rows] self-cleaning tile tickets
     int32_t *sched;   // [2] dynamic tile counter + finished-CTA counter (self-cleaning)
-    int32_t *cut;     // [4 + 3 * 1024] cut-segment list of the persistent prefill kernel
+    int32_t *cut;     // [3 * 1024] cut-segment slots of the persistent prefill kernel (one per CTA)
     void *O;
     float *LSE;
 };

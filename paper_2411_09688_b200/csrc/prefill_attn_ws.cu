@@ -291,7 +291,10 @@ __global__ void __launch_bounds__(ws::NT, 1)
     // (>= SEG_W + 1 units per CTA, so a CTA range never lies inside one segment's setup units)
     const long long Gmax = T / (SEG_W + 1);
     const int G = (int)(Gmax < 1 ? 1 : (Gmax < (long long)gridDim.x ? Gmax : (long long)gridDim.x));
-    if (c >= G) return;
+    if (c >= G) {
+        if (tid == 0) a.cut[3 * c] = -1;
+        return;
+    }
     const long long lo = T * c / G, hi = T * (c + 1) / G;
     {
         // first segment of this CTA: the first s that is not (entirely before lo)
@@ -692,37 +695,38 @@ __global__ void __launch_bounds__(ws::NT, 1)
     if (warp == 0) tmem_dealloc(tmem, 512);
     // ---- cut segments are merged by k_merge_cut (next launch, all SMs): the
     // first piece's owner c0 lists (segment, c0, c1) ----
+    // (slot c: the cut segment whose first piece this CTA holds, or -1; every slot
+    // is rewritten by every call, so the list needs no counter or reset)
     if (tid == 0) {
         asm volatile("griddepcontrol.launch_dependents;");
-        for (int k = 0; k < 2; ++k) {
-            const int s = misc[6 + k];
-            if (s >= 0 && misc[10 + 2 * k] == c) {
-                const int slot = atomicAdd(a.cut, 1);
-                a.cut[4 + 3 * slot] = s;
-                a.cut[5 + 3 * slot] = misc[10 + 2 * k];
-                a.cut[6 + 3 * slot] = misc[11 + 2 * k];
-            }
-        }
+        int seg = -1, k1 = -1;
+        for (int k = 0; k < 2; ++k)
+            if (misc[6 + k] >= 0 && misc[10 + 2 * k] == c) { seg = misc[6 + k]; k1 = misc[11 + 2 * k]; }
+        a.cut[3 * c] = seg;
+        a.cut[3 * c + 1] = c;
+        a.cut[3 * c + 2] = k1;
     }
     WS_TRACE(tid == 0, 0, 22);
     WS_CTA_T(2);
 }
 
 // Merge of the cut segments' pieces: CTA (k, slice) merges rows
-// [slice * 64, +64) of the k-th listed segment from its pieces' (O/l, lse)
-// partials.  Launched with programmatic stream serialization after the main
-// kernel; the last CTA resets the list counter (self-cleaning workspace).
-constexpr int MERGE_ROWS = 64;
+// [slice * MERGE_ROWS, +MERGE_ROWS) of the segment whose first piece main-kernel
+// CTA k holds (slot k; -1: none) from its pieces' (O/l, lse) partials.
+// Launched with programmatic stream serialization after the main kernel.
+#ifndef SQZ_MERGE_ROWS
+#define SQZ_MERGE_ROWS 64
+#endif
+constexpr int MERGE_ROWS = SQZ_MERGE_ROWS;  // rows per merge CTA
 __global__ void __launch_bounds__(256) k_merge_cut(AttnArgs a, int npairs) {
     using namespace ws;
     asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ float wgt[8][MERGE_ROWS];  // up to 8 pieces in registers' worth of weights
-    __shared__ int s_last;
     const int tid = threadIdx.x;
-    const int ncut = ldcg(a.cut);
     const int k = blockIdx.x;
-    if (k < ncut) {
-        const int s = ldcg(a.cut + 4 + 3 * k), c0 = ldcg(a.cut + 5 + 3 * k), c1 = ldcg(a.cut + 6 + 3 * k);
+    const int s = ldcg(a.cut + 3 * k);
+    if (s >= 0) {
+        const int c0 = ldcg(a.cut + 3 * k + 1), c1 = ldcg(a.cut + 3 * k + 2);
         const int np = c1 - c0 + 1;
         const int bh = s / npairs, pair = s - bh * npairs;
         const int nrow_seg = min(PR, a.n_q - pair * PR);
@@ -794,16 +798,6 @@ __global__ void __launch_bounds__(256) k_merge_cut(AttnArgs a, int npairs) {
                     reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.O) + orow * D)[ch] = acc;
                 }
             }
-        }
-    }
-    // self-cleaning: the last CTA resets the list counter
-    __syncthreads();
-    if (tid == 0) {
-        const int t = atomicAdd(a.cut + 1, 1);
-        s_last = t == (int)(gridDim.x * gridDim.y) - 1;
-        if (s_last) {
-            a.cut[0] = 0;
-            a.cut[1] = 0;
         }
     }
 }
