@@ -362,6 +362,16 @@ int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t 
         }
         return SQZ_OK;
     }
+    if (idx->levels == 2 && n_q == 1) {
+        // decode: Level 2 expands its slice of the candidate rows from the Level-1
+        // survivors (run-length) in shared memory; no candidate list is written
+        w.l1.exp_list = nullptr;
+        w.l2.rl_list = w.l1.list;
+        w.l2.rl_pref = w.l1.sel_pref;
+        w.l2.rl_off = idx->child_off;
+        w.l2.rl_n = w.l1.n_list;
+        w.l2.rl_c = idx->c1;
+    }
     if (idx->levels == 2) {
         cudaError_t e = launch_lookup_level(s, Q, w.l1, st);
         if (e != cudaSuccess) return cuda_fail(e, "lookup level 1");

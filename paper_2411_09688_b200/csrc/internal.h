@@ -48,6 +48,12 @@ struct LevelArgs {
                           //    logits phase 1 stored, prefill recomputes them)
     float2 *stats_out;    // [B,H,n_q] (m, D) of this shard's rows        (phase 1)
     const float2 *gstat;  // [B,H,n_q] (M, log D) folded over the shards  (phase 2)
+    // decode Level 2: the candidate rows in run-length form (the parent level's
+    // ascending survivor list and its child-count prefix) instead of a
+    // materialised list; the kernel expands its own slice in shared memory
+    const int32_t *rl_list, *rl_pref, *rl_off;  // [B,H,rl_c], [B,H,rl_c], [H,rl_c+1]
+    const int32_t *rl_n;                        // [B,H] survivors
+    int32_t rl_c;
 };
 
 struct LookupShape {

@@ -387,7 +387,57 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         }
     } else {
     // ---- scan: logits of the CTA's rows for the NB queries ----
-    if (ROWLIST) {  // the CTA's row ids in one coalesced pass (not one round trip per batch)
+    if (ROWLIST && lv.rl_list) {
+        // candidate q = r0 + rr is child (q - pref[j]) of survivor j, pref[j] <= q <
+        // pref[j+1]: the slice's survivors (at most nloc, each has >= 1 child) are
+        // staged in s_o0 / s_o1 (free until the scan), then a search per row
+        const size_t pb = ((size_t)b0 * H + h) * lv.rl_c;
+        __shared__ int s_ja, s_ns, s_smp;
+        // last survivor with pref <= r0: 256 samples, then a warp scans the gap
+        // (two memory round trips instead of a serial binary search)
+        const int n = ldcg(lv.rl_n + (size_t)b0 * H + h);
+        if (tid == 0) s_smp = -1;
+        __syncthreads();
+        if (n > 0) {
+            const int ik = (int)((long long)tid * n / NT);
+            if (ldcg(lv.rl_pref + pb + ik) <= r0) atomicMax(&s_smp, tid);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int k = max(s_smp, 0);
+            const int lo = (int)((long long)k * n / NT), hi = (int)((long long)(k + 1) * n / NT);
+            int best = lo;
+            for (int base = lo + 1; base < hi; base += 32) {
+                const int j = base + lane;
+                const bool le = j < hi && ldcg(lv.rl_pref + pb + j) <= r0;
+                const unsigned bal = __ballot_sync(FULL, le);
+                if (bal) best = base + 31 - __clz(bal);
+            }
+            if (lane == 0) {
+                s_ja = best;
+                s_ns = max(0, min(n - best, nloc));
+            }
+        }
+        __syncthreads();
+        const int ja = s_ja, ns = s_ns;
+        const int32_t *po = lv.rl_off + (size_t)h * (lv.rl_c + 1);
+        for (int m = tid; m < ns; m += NT) {
+            s_o0[m] = __ldg(po + ldcg(lv.rl_list + pb + ja + m));  // first child row
+            s_o1[m] = ldcg(lv.rl_pref + pb + ja + m);              // its candidate index
+        }
+        __syncthreads();
+        for (int rr = tid; rr < nloc; rr += NT) {
+            const int q = r0 + rr;
+            int lo = 0, hi = ns - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_o1[mid] <= q) lo = mid;
+                else hi = mid - 1;
+            }
+            s_row[rr] = s_o0[lo] + (q - s_o1[lo]);
+        }
+        __syncthreads();
+    } else if (ROWLIST) {  // the CTA's row ids in one coalesced pass (not one round trip per batch)
         for (int rr = tid; rr < nloc; rr += NT) s_row[rr] = ldcg(rows + r0 + rr);
         __syncthreads();
     }
