@@ -853,7 +853,18 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
 template <typename T, int D, int NB, bool RL>
 static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
                                  int groups, cudaStream_t st) {
-    // 8-CTA clusters while a CTA's rows fit ~72 KB (3 CTAs per SM), else 16
+    // the smallest cluster whose CTAs' rows fit ~72 KB (3 CTAs per SM) while the
+    // grid still has >= 256 CTAs: fewer, longer CTAs amortise the per-CTA phases
+    // (fold, compaction, cluster barriers) when there are many (query group,
+    // head) units, e.g. batched Level-2 lookups
+    const int units = s.H * groups;
+    auto ok = [&](int nc) {
+        return decode_smem_bytes(NB, (rowspace + nc - 1) / nc) <= 72 * 1024 && nc * units >= 256;
+    };
+#ifndef SQZ_NC_FIXED8  // A/B switch (experiments only)
+    if (ok(2)) return launch_decode_nc<T, D, NB, RL, 2>(s, Q, lv, rowspace, groups, st);
+    if (ok(4)) return launch_decode_nc<T, D, NB, RL, 4>(s, Q, lv, rowspace, groups, st);
+#endif
     if (decode_smem_bytes(NB, (rowspace + 7) / 8) <= 72 * 1024)
         return launch_decode_nc<T, D, NB, RL, 8>(s, Q, lv, rowspace, groups, st);
     return launch_decode_nc<T, D, NB, RL, 16>(s, Q, lv, rowspace, groups, st);
