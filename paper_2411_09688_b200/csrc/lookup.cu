@@ -315,7 +315,7 @@ template <int NB> struct DecodeSmem {
     int cnt[NB], keys[NB];
 };
 
-template <typename T, int D, int NB, bool ROWLIST, int NC>
+template <typename T, int D, int NB, bool ROWLIST, int NC, bool SLIM>
 __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T *__restrict__ Q,
                                                       LevelArgs lv, int rpc) {
     namespace cg = cooperative_groups;
@@ -335,20 +335,27 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
     const int32_t *off = lv.off + (size_t)h * (c + 1);
 
     extern __shared__ __align__(16) unsigned char dyn[];
-    // per-row arrays; with one query (NB == 1) the compaction writes its output
-    // in place over the row arrays (output position <= input position, and a
-    // tile's reads precede its writes), 20 B per row instead of 36
+    // per-row arrays.  With one query (NB == 1) the compaction writes its output
+    // in place over them (output position <= input position, and a tile's reads
+    // precede its writes), 20 B per row.  SLIM (one query, large row spaces)
+    // keeps only the logit, row id and off[row] (12 B per row; N and
+    // off[row + 1] are re-read from the tables where needed): selected row ->
+    // s_row, range start -> s_o0, key offset -> s_log, range length =
+    // difference of consecutive key offsets.
+    static_assert(!SLIM || NB == 1, "SLIM layout is for one query");
+    constexpr bool ONEQ = SLIM;
     constexpr int NCMP = NB == 1 ? 0 : NB;                         // separate compaction arrays
     float *s_log = reinterpret_cast<float *>(dyn);                 // [NB][rpc]
     int *s_row = reinterpret_cast<int *>(s_log + NB * rpc);        // [rpc] (ROWLIST)
-    float *s_Nw = reinterpret_cast<float *>(s_row + rpc);          // [rpc] N of the row
-    int *s_o0 = reinterpret_cast<int *>(s_Nw + rpc);               // [rpc] off[row]
-    int *s_o1 = s_o0 + rpc;                                        // [rpc] off[row + 1]
+    int *s_o0 = s_row + rpc;                                       // [rpc] off[row]
+    float *s_Nw = reinterpret_cast<float *>(s_o0 + rpc);           // [rpc] N of the row (NB > 1)
+    int *s_o1 = reinterpret_cast<int *>(s_Nw + rpc);               // [rpc] off[row + 1] (NB > 1)
     int *s_cmp = s_o1 + rpc;                                       // [4][NCMP][rpc]
     int *s_sel = NB == 1 ? s_row : s_cmp;                          // [NB][rpc] selected row ids
     int *s_st = NB == 1 ? s_o0 : s_cmp + NCMP * rpc;               // [NB][rpc] range starts
-    int *s_n = NB == 1 ? s_o1 : s_cmp + 2 * NCMP * rpc;            // [NB][rpc] range lengths
-    int *s_kp = NB == 1 ? reinterpret_cast<int *>(s_Nw) : s_cmp + 3 * NCMP * rpc;  // key offsets
+    int *s_n = ONEQ ? nullptr : NB == 1 ? s_o1 : s_cmp + 2 * NCMP * rpc;  // range lengths
+    int *s_kp = ONEQ ? reinterpret_cast<int *>(s_log)
+                     : NB == 1 ? reinterpret_cast<int *>(s_Nw) : s_cmp + 3 * NCMP * rpc;  // key offsets
     __shared__ DecodeSmem<NB> sh;
     __shared__ float s_M[NB], s_lD[NB];
     __shared__ float s_wm[NW][NB], s_wd[NW][NB];
@@ -373,9 +380,11 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         for (int rr = tid; rr < nloc; rr += NT) {
             const int row = ROWLIST ? ldcg(rows + r0 + rr) : r0 + rr;
             s_row[rr] = row;
-            s_Nw[rr] = (float)__ldg(N + row);
             s_o0[rr] = __ldg(off + row);
-            s_o1[rr] = __ldg(off + row + 1);
+            if (!ONEQ) {
+                s_Nw[rr] = (float)__ldg(N + row);
+                s_o1[rr] = __ldg(off + row + 1);
+            }
             for (int i = 0; i < nb; ++i)
                 s_log[i * rpc + rr] = ldcg(lv.logits + ((size_t)(b0 + i) * H + h) * c + r0 + rr);
         }
@@ -390,7 +399,8 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
     if (ROWLIST && lv.rl_list) {
         // candidate q = r0 + rr is child (q - pref[j]) of survivor j, pref[j] <= q <
         // pref[j+1]: the slice's survivors (at most nloc, each has >= 1 child) are
-        // staged in s_o0 / s_o1 (free until the scan), then a search per row
+        // staged in s_o0 / s_log (free until the scan), then a search per row
+        int *s_sp = reinterpret_cast<int *>(s_log);
         const size_t pb = ((size_t)b0 * H + h) * lv.rl_c;
         __shared__ int s_ja, s_ns, s_smp;
         // last survivor with pref <= r0: 256 samples, then a warp scans the gap
@@ -423,7 +433,7 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         const int32_t *po = lv.rl_off + (size_t)h * (lv.rl_c + 1);
         for (int m = tid; m < ns; m += NT) {
             s_o0[m] = __ldg(po + ldcg(lv.rl_list + pb + ja + m));  // first child row
-            s_o1[m] = ldcg(lv.rl_pref + pb + ja + m);              // its candidate index
+            s_sp[m] = ldcg(lv.rl_pref + pb + ja + m);              // its candidate index
         }
         __syncthreads();
         for (int rr = tid; rr < nloc; rr += NT) {
@@ -431,10 +441,10 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
             int lo = 0, hi = ns - 1;
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if (s_o1[mid] <= q) lo = mid;
+                if (s_sp[mid] <= q) lo = mid;
                 else hi = mid - 1;
             }
-            s_row[rr] = s_o0[lo] + (q - s_o1[lo]);
+            s_row[rr] = s_o0[lo] + (q - s_sp[lo]);
         }
         __syncthreads();
     } else if (ROWLIST) {  // the CTA's row ids in one coalesced pass (not one round trip per batch)
@@ -463,9 +473,11 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         int myrow = -1;
         if (lane < U && myrr < nloc) {
             myrow = ROWLIST ? s_row[myrr] : r0 + myrr;
-            s_Nw[myrr] = (float)__ldg(N + myrow);
             s_o0[myrr] = __ldg(off + myrow);
-            s_o1[myrr] = __ldg(off + myrow + 1);
+            if (!ONEQ) {
+                s_Nw[myrr] = (float)__ldg(N + myrow);
+                s_o1[myrr] = __ldg(off + myrow + 1);
+            }
         }
         typename LaneT::Raw raw[U];
         bool have[U];
@@ -518,7 +530,10 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         for (int w = 0; w < NW; ++w) M = fmaxf(M, s_wm[w][i]);
         float e = 0.f;
         if (M != -INFINITY)
-            for (int rr = tid; rr < nloc; rr += NT) e += s_Nw[rr] * expf(s_log[i * rpc + rr] - M);
+            for (int rr = tid; rr < nloc; rr += NT) {
+                const float nw = ONEQ ? (float)__ldg(N + (ROWLIST ? s_row[rr] : r0 + rr)) : s_Nw[rr];
+                e += nw * expf(s_log[i * rpc + rr] - M);
+            }
         e = warp_sum(e);
         if (lane == 0) s_wd[warp][i] = e;
         __syncthreads();
@@ -579,13 +594,16 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
             if (valid && lv.dbg_S) lv.dbg_S[(size_t)bh * c + row] = expf(x - lD);
             if (valid && lv.bitmap) lv.bitmap[(size_t)bh * c + row] = sel ? 1 : 0;
             int st = 0, n = 0;
-            if (sel) { st = s_o0[rr]; n = s_o1[rr] - st; }
+            if (sel) {
+                st = s_o0[rr];
+                n = (ONEQ ? __ldg(off + row + 1) : s_o1[rr]) - st;
+            }
             int pos, kpre, tc, tk;
             tile_scan(sel, n, pos, kpre, tc, tk);
             if (sel) {
                 s_sel[i * rpc + run + pos] = row;
                 s_st[i * rpc + run + pos] = st;
-                s_n[i * rpc + run + pos] = n;
+                if (!ONEQ) s_n[i * rpc + run + pos] = n;
                 s_kp[i * rpc + run + pos] = runk + kpre;
             }
             run += tc;
@@ -637,7 +655,8 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         }
         if (exp_list)
         for (int j = warp; j < mine; j += NW) {
-            const int st = s_st[i * rpc + j], n = s_n[i * rpc + j], kp = s_kp[i * rpc + j];
+            const int st = s_st[i * rpc + j], kp = s_kp[i * rpc + j];
+            const int n = ONEQ ? (j + 1 < mine ? s_kp[i * rpc + j + 1] : sh.keys[i]) - kp : s_n[i * rpc + j];
             for (int t = lane; t < n; t += 32) exp_list[kp + t] = st + t;
         }
     }
@@ -675,8 +694,8 @@ cudaError_t launch_fold_stats(int P, const float2 *stats_in, int64_t n, float2 *
     return cudaGetLastError();
 }
 
-static size_t decode_smem_bytes(int NB, int rpc) {
-    return (size_t)rpc * 4 * (NB + 4 + (NB == 1 ? 0 : 4 * NB)) + 16;
+static size_t decode_smem_bytes(int NB, int rpc, bool slim = false) {
+    return (size_t)rpc * 4 * (slim ? 3 : NB == 1 ? 5 : NB + 4 + 4 * NB) + 16;
 }
 
 // --------------------------------------------------------------------------
@@ -811,13 +830,13 @@ static bool decode_fits(int NB, int rowspace, int nc) {
     return decode_smem_bytes(NB, (rowspace + nc - 1) / nc) <= DECODE_SMEM_MAX;
 }
 
-template <typename T, int D, int NB, bool RL, int NC>
+template <typename T, int D, int NB, bool RL, int NC, bool SLIM = false>
 static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
                                     int groups, cudaStream_t st) {
     const int rpc = (rowspace + NC - 1) / NC;
-    const size_t smem = decode_smem_bytes(NB, rpc);
+    const size_t smem = decode_smem_bytes(NB, rpc, SLIM);
     if (smem > DECODE_SMEM_MAX) return cudaErrorInvalidValue;
-    auto kern = k_lookup_decode<T, D, NB, RL, NC>;
+    auto kern = k_lookup_decode<T, D, NB, RL, NC, SLIM>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -853,20 +872,22 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
 template <typename T, int D, int NB, bool RL>
 static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
                                  int groups, cudaStream_t st) {
-    // the smallest cluster whose CTAs' rows fit ~72 KB (3 CTAs per SM) while the
-    // grid still has >= 256 CTAs: fewer, longer CTAs amortise the per-CTA phases
-    // (fold, compaction, cluster barriers) when there are many (query group,
-    // head) units, e.g. batched Level-2 lookups
+    // the smallest cluster whose CTAs' rows fit 110 KB (2 CTAs per SM, which is
+    // also the register limit) while the grid keeps >= 256 CTAs (one wave):
+    // fewer, longer CTAs amortise the per-CTA phases (fold, compaction, cluster
+    // barriers), e.g. 2-CTA clusters for batched Level-2 lookups
     const int units = s.H * groups;
     auto ok = [&](int nc) {
-        return decode_smem_bytes(NB, (rowspace + nc - 1) / nc) <= 72 * 1024 && nc * units >= 256;
+        return decode_smem_bytes(NB, (rowspace + nc - 1) / nc) <= 110 * 1024 && nc * units >= 256;
     };
-#ifndef SQZ_NC_FIXED8  // A/B switch (experiments only)
     if (ok(2)) return launch_decode_nc<T, D, NB, RL, 2>(s, Q, lv, rowspace, groups, st);
     if (ok(4)) return launch_decode_nc<T, D, NB, RL, 4>(s, Q, lv, rowspace, groups, st);
-#endif
-    if (decode_smem_bytes(NB, (rowspace + 7) / 8) <= 72 * 1024)
+    if (ok(8) || decode_smem_bytes(NB, (rowspace + 7) / 8) <= 110 * 1024)
         return launch_decode_nc<T, D, NB, RL, 8>(s, Q, lv, rowspace, groups, st);
+    if constexpr (NB == 1) {  // one query, large row space: 12 B/row keeps 8-CTA clusters (one wave)
+        if (decode_smem_bytes(1, (rowspace + 7) / 8, true) <= 110 * 1024)
+            return launch_decode_nc<T, D, NB, RL, 8, true>(s, Q, lv, rowspace, groups, st);
+    }
     return launch_decode_nc<T, D, NB, RL, 16>(s, Q, lv, rowspace, groups, st);
 }
 
