@@ -182,3 +182,29 @@ def test_cfg4_hier_decode_fullsize():
     torch.cuda.synchronize()
     assert torch.equal(sel_dbg.n_keys, sel.n_keys)
     _check(idx, sel_dbg, O, LSE, T, T1, scale, heads, Q, K, V, Ku, Vu, False)
+
+
+def test_slim_layout_large_level2():
+    """A Level-2 table large enough (47K rows) that the one-query decode lookup
+    takes the 12-byte-per-row SLIM layout in 8-CTA clusters (cfg5's case), checked
+    against the oracle on every head."""
+    sqz = _sqz()
+    H, L, d, c2, c1 = 2, 49152, 128, 47000, 9400
+    fc = synth.fixed_context(H, L, d, c2, seed=1109, G1=c1)
+    K, V = sqz.to_device(fc.K), sqz.to_device(fc.V)
+    init2 = torch.from_numpy(synth.kmeans_init(H, L, c2, seed=2109)).cuda()
+    init1 = torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=2209)).cuda()
+    Qc = sqz.to_device(synth.decode_queries(fc.mix, 16, seed=3109))
+    Q = sqz.to_device(synth.decode_queries(fc.mix, 1, seed=4109))
+    Ku, Vu = (sqz.to_device(a) for a in synth.user_kv(fc.mix, 1, 64, seed=5109))
+    idx, Kp, Vp, _ = sqz.cluster_keys(K, V, c2, init2, c1, init1, max_iters=3)
+    scale = 1.0 / np.sqrt(d)
+    s = sqz.centroid_lookup(idx, Qc, scale, 0.0, 0.0, debug=True)
+    T1 = calib.distributed_threshold(s.dbg_S1, idx.N1[None], 0.5, float(16 * idx.N1.sum()))
+    s = sqz.centroid_lookup(idx, Qc, scale, 0.0, T1, debug=True)
+    T = calib.distributed_threshold(s.dbg_S, idx.N2[None], 0.1, float(16 * H * L))
+    sel = sqz.centroid_lookup(idx, Q, scale, T, T1, debug=True)
+    O, LSE = sqz.sparse_attention(Q, Kp, Vp, idx, sel, Ku, Vu, scale)
+    torch.cuda.synchronize()
+    assert int(sel.n_keys.min()) > 0
+    _check(idx, sel, O, LSE, T, T1, scale, [0, 1], Q, K, V, Ku, Vu, False)
