@@ -29,9 +29,13 @@ sel = sqz.Selection.empty(idx, 1, 1)
 O = torch.empty(1, H, 1, d, dtype=torch.bfloat16, device="cuda")
 LSE = torch.empty(1, H, 1, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+# SQZ_FLUSH=read: after the write flush, read a second 512 MB buffer (L2 left clean)
+rflush = torch.ones(128 << 20, dtype=torch.float32, device="cuda") if os.environ.get("SQZ_FLUSH") == "read" else None
 lib = sqz.lib()
 for it in range(6):
     flush.zero_()  # no sync: the host runs ahead as in bench.py
+    if rflush is not None:
+        rflush.sum()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     sqz.centroid_lookup(idx, Q, 1 / np.sqrt(d), T, sel=sel)
@@ -53,8 +57,40 @@ def st(name, v):
 for i, n in enumerate(["lookup start", "lookup scan done", "lookup cluster.sync 1", "lookup cluster.sync 2",
                        "lookup writes done", "lookup end"]):
     st(n, tl[:, i])
-for i, n in enumerate(["attn entry", "attn after griddep wait", "attn prologue done",
-                       "attn first stage ready", "attn streaming done (last seg)", "attn end"]):
+for i, n in [(0, "attn entry"), (1, "attn after griddep wait"), (2, "attn prologue done"),
+             (6, "attn first segment done"), (4, "attn streaming done (last seg)"), (5, "attn end")]:
     col = ta[:, i]
     if (col > 0).any():
         st(n, col[col > 0])
+# per-CTA attribution of the tail: segments, merges, keys, SM
+info = ta[:, 3].astype(np.uint64)
+nseg = (info & 0xff).astype(int)
+nmer = ((info >> 8) & 0xff).astype(int)
+keys = (info >> 16).astype(int)
+smid = ta[:, 7].astype(int)
+done = (ta[:, 4] - t0) / 1e3
+end = (ta[:, 5] - t0) / 1e3
+start = (ta[:, 2] - t0) / 1e3
+print(f"  CTAs {len(ta)}; keys/CTA min {keys.min()} max {keys.max()}")
+for k in sorted(set(nseg)):
+    m = nseg == k
+    print(f"  nseg={k}: {m.sum():4d} CTAs, done med {np.median(done[m]):.2f} max {done[m].max():.2f}; "
+          f"end med {np.median(end[m]):.2f} max {end[m].max():.2f}")
+for k in sorted(set(nmer)):
+    m = nmer == k
+    print(f"  merges={k}: {m.sum():4d} CTAs, end med {np.median(end[m]):.2f} max {end[m].max():.2f}")
+rate = keys / np.maximum(done - start, 1e-3)  # keys per us
+for lo, hi in [(0, 74), (74, 148)]:
+    m = (smid >= lo) & (smid < hi)
+    print(f"  SM {lo}-{hi - 1}: {m.sum()} CTAs, keys/us med {np.median(rate[m]):.1f}, done med {np.median(done[m]):.2f} max {done[m].max():.2f}")
+per_sm = {}
+for s_, d_ in zip(smid, done):
+    per_sm.setdefault(s_, []).append(d_)
+sm_max = np.array([max(v) for v in per_sm.values()])
+sm_spread = np.array([max(v) - min(v) for v in per_sm.values()])
+print(f"  per-SM last done: min {sm_max.min():.2f} med {np.median(sm_max):.2f} max {sm_max.max():.2f}; "
+      f"within-SM spread med {np.median(sm_spread):.2f}")
+order = np.argsort(-done)[:12]
+print("  slowest CTAs (cta, sm, nseg, merges, keys, start, done, end):")
+for i in order:
+    print(f"    {i:4d} {smid[i]:4d} {nseg[i]} {nmer[i]} {keys[i]:5d} {start[i]:6.2f} {done[i]:6.2f} {end[i]:6.2f}")

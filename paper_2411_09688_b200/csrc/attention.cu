@@ -36,6 +36,15 @@ constexpr int NCT = NCW * 32;           // threads per CTA
 constexpr int KR = 16;                  // keys per warp round
 constexpr int MAX_PERSIST_CTAS = 1184;  // 148 SMs x 8
 constexpr int MIN_KEYS = 256;           // minimum keys per persistent CTA
+// Partition cost of a decode segment: its keys plus SEG_KW keys' worth for the
+// segment's setup and epilogue (q load, position prefetch, pipeline refill,
+// partial write + ticket), so a CTA whose range straddles a row boundary gets
+// fewer keys (measured: ~2.3 us per extra segment at ~25 keys/us per CTA;
+// 128 was the best of 0 / 64 / 128 on cfg2).
+#ifndef SQZ_DEC_SEG_KW
+#define SQZ_DEC_SEG_KW 128
+#endif
+constexpr int SEG_KW = SQZ_DEC_SEG_KW;
 
 int attention_kch(int n_q) { return n_q == 1 ? 256 : 1024; }
 int attention_max_parts(int64_t L, int n_u, int n_q) {
@@ -116,57 +125,51 @@ struct Seg {
 };
 
 // Merge of one row's partials by the CTA: O = sum_p e^(lse_p - M) o_p / L,
-// LSE = M + log L.
+// LSE = M + log L.  Thread k < D owns output column k; the
+// partials are read 16 at a time (their lse values and o columns in the same
+// memory round trip) with an online rescale, so the merge is one pass without
+// block barriers.  Every thread forms the same weights in the same order (the
+// result does not depend on which CTA merges or when).
 template <int D>
-__device__ void merge_row(const AttnArgs &a, int row, int P, float *s_w, float *s_red) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+__device__ void merge_row(const AttnArgs &a, int row, int P) {
+    constexpr int MB = 16;
+    const int tid = threadIdx.x;
+    if (tid >= D) return;
     const float *lse = a.part_lse + (size_t)row * a.max_chunks;
-    float acc = 0.f, lsum = 0.f;
-    float M = -INFINITY;
-    for (int p0 = 0; p0 < P; p0 += NCT) {
-        // one tile of <= NCT partials: lse values once, block max, weights in
-        // smem, then the o rows with independent (unrolled) loads
-        const int p = p0 + tid;
-        const float lv = p < P ? ldcg(lse + p) : -INFINITY;
-        const float mx = warp_max(lv);
-        if (lane == 0) s_red[warp] = mx;
-        __syncthreads();
-        float Mt = -INFINITY;
-        for (int w = 0; w < NCW; ++w) Mt = fmaxf(Mt, s_red[w]);
-        const float Mn = fmaxf(M, Mt);
-        const float corr = (M == -INFINITY) ? 0.f : expf(M - Mn);  // rescale earlier tiles
-        acc *= corr;
-        lsum *= corr;
-        M = Mn;
-        const float w = (lv == -INFINITY) ? 0.f : expf(lv - M);
-        s_w[tid] = w;
-        lsum += w;
-        __syncthreads();
-        const int np = min(NCT, P - p0);
-        if (tid < D) {
-            const float *op = a.part_o + ((size_t)row * a.max_chunks + p0) * D + tid;
-#pragma unroll 16
-            for (int j = 0; j < np; ++j) acc = fmaf(s_w[j], ldcg(op + (size_t)j * D), acc);
+    const float *op = a.part_o + (size_t)row * a.max_chunks * D + tid;
+    float M = -INFINITY, L = 0.f, acc = 0.f;
+    for (int p0 = 0; p0 < P; p0 += MB) {
+        float lv[MB], ov[MB];
+#pragma unroll
+        for (int j = 0; j < MB; ++j) {
+            const bool in = p0 + j < P;
+            lv[j] = in ? ldcg(lse + p0 + j) : -INFINITY;
+            ov[j] = in ? ldcg(op + (size_t)(p0 + j) * D) : 0.f;
         }
-        __syncthreads();
+        float mt = M;
+#pragma unroll
+        for (int j = 0; j < MB; ++j) mt = fmaxf(mt, lv[j]);
+        if (mt == -INFINITY) continue;
+        const float corr = expf(M - mt);  // M = -inf -> 0
+        L *= corr;
+        acc *= corr;
+#pragma unroll
+        for (int j = 0; j < MB; ++j) {
+            const float w = expf(lv[j] - mt);  // lse = -inf -> 0
+            L += w;
+            acc = fmaf(w, ov[j], acc);
+        }
+        M = mt;
     }
-    lsum = warp_sum(lsum);
-    if (lane == 0) s_red[warp] = lsum;
-    __syncthreads();
-    float L = 0.f;
-    for (int w = 0; w < NCW; ++w) L += s_red[w];
-    if (tid < D) {
-        const float v = (M == -INFINITY) ? 0.f : acc / L;
-        if (a.out_dtype == SQZ_BF16)
-            reinterpret_cast<__nv_bfloat16 *>(a.O)[(size_t)row * D + tid] = __float2bfloat16_rn(v);
-        else
-            reinterpret_cast<float *>(a.O)[(size_t)row * D + tid] = v;
-    }
+    const float v = (M == -INFINITY) ? 0.f : acc / L;
+    if (a.out_dtype == SQZ_BF16)
+        reinterpret_cast<__nv_bfloat16 *>(a.O)[(size_t)row * D + tid] = __float2bfloat16_rn(v);
+    else
+        reinterpret_cast<float *>(a.O)[(size_t)row * D + tid] = v;
     if (tid == 0) {
         a.LSE[row] = (M == -INFINITY) ? -INFINITY : M + logf(L);
         if (M == -INFINITY && !a.partial) atomicOr(a.status, 1);
     }
-    __syncthreads();
 }
 
 // Rows with no key at all (no selected fixed key, no visible user key) get the
@@ -188,7 +191,7 @@ __device__ void empty_row(const AttnArgs &a, int row) {
 // Iterates the segments of this CTA.
 template <bool PERSIST> struct SegIter {
     const AttnArgs *a;
-    const int *pref;  // PERSIST: exclusive prefix of row stream lengths, [rows + 1]
+    const int *pref;  // PERSIST: exclusive prefix of row partition costs, [rows + 1]
     int rows, r;
     long long ks, ke, K;
     int G;
@@ -202,7 +205,9 @@ template <bool PERSIST> struct SegIter {
         rows = nrows;
         done = false;
         if (PERSIST) {
-            // at least MIN_KEYS keys per CTA: small problems use fewer CTAs
+            // the CTAs split the cost space (row r: SEG_KW setup units, then one
+            // unit per key) into equal ranges; at least MIN_KEYS units per CTA,
+            // so small problems use fewer CTAs and no range lies inside a setup gap
             K = pref[rows];
             G = (int)min((long long)gridDim.x, max(1LL, (K + MIN_KEYS - 1) / MIN_KEYS));
             if ((int)blockIdx.x >= G || K == 0) { r = rows; ke = 0; return; }
@@ -219,9 +224,10 @@ template <bool PERSIST> struct SegIter {
     __device__ bool next(Seg &s) {
         if (PERSIST) {
             while (r < rows && pref[r] < ke) {
-                const long long rs = pref[r], re = pref[r + 1];
+                const long long cs = pref[r], re = pref[r + 1];
                 const int row = r++;
-                if (re <= ks || re == rs) continue;
+                const long long rs = cs + SEG_KW;  // cost unit of the row's first key
+                if (re <= ks || re == cs || ke <= rs) continue;
                 s.row = row;
                 s.a0 = (int)(max(ks, rs) - rs);
                 s.a1 = (int)(min(ke, re) - rs);
@@ -257,7 +263,7 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
     extern __shared__ __align__(16) int dyn_i[];
     int *s_pref = dyn_i;             // [rows + 1] (persistent)
     int *s_nkf = dyn_i + rows + 1;   // [rows]     (persistent)
-    __shared__ float s_m[NCW], s_l[NCW], s_o[NCW * D], s_w[NCT], s_red[NCW];
+    __shared__ float s_m[NCW], s_l[NCW], s_o[NCW * D];
     __shared__ int s_last;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
             int len = 0;
             if (r < rows) {
                 const RowInfo ri = row_info(a, r);
-                len = ri.total();
+                len = ri.total() > 0 ? ri.total() + SEG_KW : 0;
                 s_nkf[r] = ri.nkf;
             }
             int inc = len;
@@ -308,7 +314,14 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
     Seg sg;
     const int g = lane / G, sub = lane % G;
     const int myslot = sub >> (LG_G - LG_NS);
+#ifdef SQZ_TRACE
+    int tr_nseg = 0, tr_nmerge = 0, tr_keys = 0;
+#endif
     while (it.next(sg)) {
+#ifdef SQZ_TRACE
+        ++tr_nseg;
+        tr_keys += sg.a1 - sg.a0;
+#endif
         const RowInfo ri = row_info(a, sg.row, PERSIST ? s_nkf[sg.row] : -1);
         const T *Kf = reinterpret_cast<const T *>(a.Kp) + (size_t)ri.h * a.L * D;
         const T *Vf = reinterpret_cast<const T *>(a.Vp) + (size_t)ri.h * a.L * D;
@@ -407,6 +420,9 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
             m_run = m_new;
         }
         SQZ_TRACE_AT(g_trace_attn, 4);
+#ifdef SQZ_TRACE
+        if (tr_nseg == 1) SQZ_TRACE_AT(g_trace_attn, 6);
+#endif
         // ---- segment epilogue: fold key groups, then the warps ----
 #pragma unroll
         for (int s2 = G; s2 < 32; s2 <<= 1)
@@ -432,10 +448,11 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
             a.part_o[slot * D + tid] = L > 0.f ? O / L : 0.f;
             if (tid == 0) a.part_lse[slot] = L > 0.f ? (M + log2f(L)) * LN2 : -INFINITY;
         }
-        // the CTA that completes a row's last segment merges its partials
-        __threadfence();
+        // the CTA that completes a row's last segment merges its partials (the
+        // barrier orders the CTA's partial stores before thread 0's release fence)
         __syncthreads();
         if (tid == 0) {
+            __threadfence();
             const int t = atomicAdd(a.row_cnt + sg.row, 1);
             s_last = (t == sg.nparts - 1);
             if (s_last) a.row_cnt[sg.row] = 0;
@@ -443,10 +460,23 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
         __syncthreads();
         if (s_last) {
             __threadfence();
-            merge_row<D>(a, sg.row, sg.nparts, s_w, s_red);
+            merge_row<D>(a, sg.row, sg.nparts);
+            __syncthreads();
+#ifdef SQZ_TRACE
+            ++tr_nmerge;
+#endif
         }
     }
     SQZ_TRACE_AT(g_trace_attn, 5);
+#ifdef SQZ_TRACE
+    {
+        unsigned smid_;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));
+        SQZ_TRACE_VAL(g_trace_attn, 3, (unsigned long long)tr_nseg | ((unsigned long long)tr_nmerge << 8) |
+                                           ((unsigned long long)tr_keys << 16));
+        SQZ_TRACE_VAL(g_trace_attn, 7, smid_);
+    }
+#endif
 }
 
 template <typename T, int D>

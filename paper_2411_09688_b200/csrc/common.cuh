@@ -157,6 +157,11 @@ __device__ __forceinline__ int runwin_pos(const RunWin &w, int k) {
             name[lin_ * 8 + (slot)] = t_;                                                 \
         }                                                                                 \
     } while (0)
+#define SQZ_TRACE_VAL(name, slot, val)                                                    \
+    do {                                                                                  \
+        const unsigned lin_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+        if (threadIdx.x == 0 && lin_ < 2048) name[lin_ * 8 + (slot)] = (unsigned long long)(val); \
+    } while (0)
 #define SQZ_TRACE_EXPORT(name, fn)                                                        \
     extern "C" int fn(void *host, size_t bytes) {                                         \
         return (int)cudaMemcpyFromSymbol(host, name, bytes < sizeof(name) ? bytes : sizeof(name)); \
@@ -164,5 +169,6 @@ __device__ __forceinline__ int runwin_pos(const RunWin &w, int k) {
 #else
 #define SQZ_TRACE_DECL(name)
 #define SQZ_TRACE_AT(name, slot) do { } while (0)
+#define SQZ_TRACE_VAL(name, slot, val) do { } while (0)
 #define SQZ_TRACE_EXPORT(name, fn)
 #endif
