@@ -78,6 +78,13 @@ template <> struct Lane<__nv_bfloat16, 128> {
     static __device__ __forceinline__ Raw load_raw(const __nv_bfloat16 *row, int lane) {
         return __ldg(reinterpret_cast<const uint2 *>(row) + lane);
     }
+    // a load the compiler keeps where it is written (not hoisted out of a loop)
+    static __device__ __forceinline__ Raw load_raw_pinned(const __nv_bfloat16 *row, int lane) {
+        Raw u;
+        asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(u.x), "=r"(u.y)
+                     : "l"(reinterpret_cast<const uint2 *>(row) + lane));
+        return u;
+    }
     static __device__ __forceinline__ void cvt(const Raw &u, float (&f)[4]) {
         f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xffff0000u);
         f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xffff0000u);
@@ -91,6 +98,12 @@ template <> struct Lane<__nv_bfloat16, 64> {
     static __device__ __forceinline__ Raw load_raw(const __nv_bfloat16 *row, int lane) {
         return __ldg(reinterpret_cast<const uint32_t *>(row) + lane);
     }
+    static __device__ __forceinline__ Raw load_raw_pinned(const __nv_bfloat16 *row, int lane) {
+        Raw u;
+        asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(u)
+                     : "l"(reinterpret_cast<const uint32_t *>(row) + lane));
+        return u;
+    }
     static __device__ __forceinline__ void cvt(const Raw &u, float (&f)[2]) {
         f[0] = __uint_as_float(u << 16); f[1] = __uint_as_float(u & 0xffff0000u);
     }
@@ -103,6 +116,12 @@ template <> struct Lane<float, 128> {
     static __device__ __forceinline__ Raw load_raw(const float *row, int lane) {
         return __ldg(reinterpret_cast<const float4 *>(row) + lane);
     }
+    static __device__ __forceinline__ Raw load_raw_pinned(const float *row, int lane) {
+        Raw u;
+        asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(u.x), "=f"(u.y), "=f"(u.z), "=f"(u.w)
+                     : "l"(reinterpret_cast<const float4 *>(row) + lane));
+        return u;
+    }
     static __device__ __forceinline__ void cvt(const Raw &u, float (&f)[4]) {
         f[0] = u.x; f[1] = u.y; f[2] = u.z; f[3] = u.w;
     }
@@ -114,6 +133,12 @@ template <> struct Lane<float, 64> {
     using Raw = float2;
     static __device__ __forceinline__ Raw load_raw(const float *row, int lane) {
         return __ldg(reinterpret_cast<const float2 *>(row) + lane);
+    }
+    static __device__ __forceinline__ Raw load_raw_pinned(const float *row, int lane) {
+        Raw u;
+        asm volatile("ld.global.nc.v2.f32 {%0,%1}, [%2];" : "=f"(u.x), "=f"(u.y)
+                     : "l"(reinterpret_cast<const float2 *>(row) + lane));
+        return u;
     }
     static __device__ __forceinline__ void cvt(const Raw &u, float (&f)[2]) {
         f[0] = u.x; f[1] = u.y;
@@ -315,7 +340,12 @@ template <int NB> struct DecodeSmem {
     int cnt[NB], keys[NB];
 };
 
-template <typename T, int D, int NB, bool ROWLIST, int NC, bool SLIM>
+// rows per warp batch: 32 for packed bf16 rows with one or two queries (their
+// raw rows take the registers 16 fp32 rows would), else 16; a CTA whose rows all
+// fit one 16-row batch per warp takes U = 16 (every warp loads, fewer registers)
+template <typename T, int NB> constexpr int decode_u_max() { return (sizeof(T) == 2 && NB <= 2) ? 32 : 16; }
+
+template <typename T, int D, int NB, bool ROWLIST, int NC, bool SLIM, int U>
 __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T *__restrict__ Q,
                                                       LevelArgs lv, int rpc) {
     namespace cg = cooperative_groups;
@@ -451,41 +481,57 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         for (int rr = tid; rr < nloc; rr += NT) s_row[rr] = ldcg(rows + r0 + rr);
         __syncthreads();
     }
-    float q[NB][D / 32];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-        if (i < nb) Lane<T, D>::load(Q + ((size_t)(b0 + i) * H + h) * D, lane, q[i]);
-        else
-#pragma unroll
-            for (int k = 0; k < D / 32; ++k) q[i][k] = 0.f;
-    }
-    // A warp loads U rows at once (one memory round trip; U = 32 for packed bf16
-    // rows with one or two queries, whose raw rows take the registers 16 fp32
-    // rows would), forms the U x NB partial dot products, and reduces them 16 at
-    // a time with the transposed butterfly: value v = row_local * NB + query.
+    // A warp loads U rows at once (one memory round trip), forms the U x NB
+    // partial dot products, and reduces them 16 at a time with the transposed
+    // butterfly: value v = row_local * NB + query.  The row metadata, the
+    // centroid rows and the query of a warp's first batch are all in flight
+    // before any of them is used (one round trip, not three).
     using LaneT = Lane<T, D>;
-    constexpr int U = (sizeof(T) == 2 && NB <= 2) ? 32 : 16;
     constexpr int RPT = 16 / NB;  // rows per 16-value transpose
     for (int rr0 = warp * U; rr0 < nloc; rr0 += NW * U) {
         // lane l < U owns row rr0 + l: its id and its N / key-range metadata are
-        // fetched now, in the same memory round trip as the centroid rows
+        // fetched now, in the same memory round trip as the centroid rows, and
+        // reach shared memory after the row loads are issued
         const int myrr = rr0 + lane;
-        int myrow = -1;
-        if (lane < U && myrr < nloc) {
+        const bool mine = lane < U && myrr < nloc;
+        int myrow = -1, m_o0 = 0, m_N = 0, m_o1 = 0;
+        if (mine) {
             myrow = ROWLIST ? s_row[myrr] : r0 + myrr;
-            s_o0[myrr] = __ldg(off + myrow);
+            m_o0 = __ldg(off + myrow);
             if (!ONEQ) {
-                s_Nw[myrr] = (float)__ldg(N + myrow);
-                s_o1[myrr] = __ldg(off + myrow + 1);
+                m_N = __ldg(N + myrow);
+                m_o1 = __ldg(off + myrow + 1);
             }
         }
         typename LaneT::Raw raw[U];
         bool have[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            // every slot loads (a missing row reads row 0 and is zeroed at use):
+            // a conditional load would be a predicated move that waits for it
             const int rid = __shfl_sync(FULL, myrow, u);
             have[u] = rid >= 0;
-            if (have[u]) raw[u] = LaneT::load_raw(C + (size_t)rid * D, lane);
+            raw[u] = LaneT::load_raw(C + (size_t)max(rid, 0) * D, lane);
+        }
+        if (mine) {
+            s_o0[myrr] = m_o0;
+            if (!ONEQ) {
+                s_Nw[myrr] = (float)m_N;
+                s_o1[myrr] = m_o1;
+            }
+        }
+        // the query row, (re)loaded in the batch's own block (a cache hit after
+        // the first batch) so the compiler does not hoist it, and its wait,
+        // ahead of the row loads
+        float q[NB][D / 32];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            if (i < nb) {
+                LaneT::cvt(LaneT::load_raw_pinned(Q + ((size_t)(b0 + i) * H + h) * D, lane), q[i]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < D / 32; ++k) q[i][k] = 0.f;
+            }
         }
 #pragma unroll
         for (int gq = 0; gq < U / RPT; ++gq) {
@@ -836,7 +882,10 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
     const int rpc = (rowspace + NC - 1) / NC;
     const size_t smem = decode_smem_bytes(NB, rpc, SLIM);
     if (smem > DECODE_SMEM_MAX) return cudaErrorInvalidValue;
-    auto kern = k_lookup_decode<T, D, NB, RL, NC, SLIM>;
+    constexpr int UMAX = decode_u_max<T, NB>();
+    auto kern = k_lookup_decode<T, D, NB, RL, NC, SLIM, UMAX>;
+    if constexpr (UMAX == 32 && !RL)
+        if (rpc <= NW * 16) kern = k_lookup_decode<T, D, NB, RL, NC, SLIM, 16>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
