@@ -54,7 +54,7 @@ print(f"retention {ret}: event step time {e0.elapsed_time(e1) * 1e3:.1f} us; k =
 def st(name, v):
     v = (v - t0) / 1e3
     print(f"  {name:38s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us")
-for i, n in enumerate(["lookup start", "lookup scan done", "lookup cluster.sync 1", "lookup cluster.sync 2",
+for i, n in enumerate(["lookup start", "lookup scan done", "lookup compaction done (pre-barrier)", "lookup cluster.sync 2",
                        "lookup writes done", "lookup end"]):
     st(n, tl[:, i])
 for i, n in [(0, "attn entry"), (1, "attn after griddep wait"), (2, "attn prologue done"),

@@ -40,13 +40,20 @@ tl = np.zeros(2048 * 8, np.uint64)
 sqz.lib().sqz_trace_look(tl.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(tl.nbytes))
 tl = tl.reshape(2048, 8).astype(np.float64)
 tl = tl[tl[:, 0] > 0]
+tl = tl[tl[:, 0] > tl[:, 5].max() - 1e6]  # CTAs of the last launch (stale slots are older)
 t0 = tl[:, 0].min()
 print(f"lookup (both levels) {e0.elapsed_time(e1) * 1e3:.1f} us; L2 CTAs traced {len(tl)}; "
       f"candidates/bh {sel.n_clusters.float().mean().item():.0f} sel, keys {sel.n_keys.float().mean().item():.0f}")
-for i, n in enumerate(["start", "scan done", "cluster.sync 1 (fold)", "compaction + sync 2",
+for i, n in enumerate(["start", "scan done", "compaction done (pre-barrier)", "cluster.sync 2",
                        "writes done", "end"]):
     v = (tl[:, i] - t0) / 1e3
     print(f"  {n:28s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us")
+if (tl[:, 7] > 0).any():
+    v = (tl[:, 7] - t0) / 1e3
+    print(f"  {'SLIM length pass done':28s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us")
+if (tl[:, 6] > 0).any():
+    v = (tl[:, 6] - t0) / 1e3
+    print(f"  {'candidate slice ready':28s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us")
 d_scan = (tl[:, 1] - tl[:, 0]) / 1e3
 d_cmp = (tl[:, 3] - tl[:, 2]) / 1e3
 d_wr = (tl[:, 4] - tl[:, 3]) / 1e3

@@ -477,6 +477,7 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
             s_row[rr] = s_o0[lo] + (q - s_sp[lo]);
         }
         __syncthreads();
+        SQZ_TRACE_AT(g_trace_look, 6);
     } else if (ROWLIST) {  // the CTA's row ids in one coalesced pass (not one round trip per batch)
         for (int rr = tid; rr < nloc; rr += NT) s_row[rr] = ldcg(rows + r0 + rr);
         __syncthreads();
@@ -576,9 +577,18 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         for (int w = 0; w < NW; ++w) M = fmaxf(M, s_wm[w][i]);
         float e = 0.f;
         if (M != -INFINITY)
-            for (int rr = tid; rr < nloc; rr += NT) {
-                const float nw = ONEQ ? (float)__ldg(N + (ROWLIST ? s_row[rr] : r0 + rr)) : s_Nw[rr];
-                e += nw * expf(s_log[i * rpc + rr] - M);
+            for (int rb = tid; rb < nloc; rb += 4 * NT) {
+                // 4 rows per thread per trip, their cluster sizes loaded together
+                float nw[4], lg[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int rr = rb + u * NT;
+                    const bool in = rr < nloc;
+                    nw[u] = !in ? 0.f : ONEQ ? (float)__ldg(N + (ROWLIST ? s_row[rr] : r0 + rr)) : s_Nw[rr];
+                    lg[u] = in ? s_log[i * rpc + rr] : M;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) e += nw[u] * expf(lg[u] - M);
             }
         e = warp_sum(e);
         if (lane == 0) s_wd[warp][i] = e;
@@ -631,18 +641,44 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         const int bh = (b0 + i) * H + h;
         const float M = s_M[i], lD = s_lD[i], thr = lD + logT;
         int run = 0, runk = 0;
+        if constexpr (ONEQ) {
+            // the selection and the range lengths of all the CTA's rows first, in
+            // one pass of independent loads of off[row + 1] (one memory round trip,
+            // not one per tile): s_log[rr] becomes the length, or -1 if unselected
+            int *s_len = reinterpret_cast<int *>(s_log);
+            for (int rr = tid; rr < nloc; rr += NT) {
+                const int row = ROWLIST ? s_row[rr] : r0 + rr;
+                const float x = s_log[rr] - M;
+                const bool sel = all || x > thr;
+                if (lv.dbg_S) lv.dbg_S[(size_t)bh * c + row] = expf(x - lD);
+                if (lv.bitmap) lv.bitmap[(size_t)bh * c + row] = sel ? 1 : 0;
+                s_len[rr] = sel ? __ldg(off + row + 1) - s_o0[rr] : -1;
+            }
+            __syncthreads();
+            SQZ_TRACE_AT(g_trace_look, 7);
+        }
         for (int base = 0; base < nloc; base += NT) {
             const int rr = base + tid;
             const bool valid = rr < nloc;
             const int row = valid ? (ROWLIST ? s_row[rr] : r0 + rr) : 0;
-            const float x = valid ? s_log[i * rpc + rr] - M : 0.f;
-            const bool sel = valid && (all || x > thr);
-            if (valid && lv.dbg_S) lv.dbg_S[(size_t)bh * c + row] = expf(x - lD);
-            if (valid && lv.bitmap) lv.bitmap[(size_t)bh * c + row] = sel ? 1 : 0;
+            bool sel;
             int st = 0, n = 0;
-            if (sel) {
-                st = s_o0[rr];
-                n = (ONEQ ? __ldg(off + row + 1) : s_o1[rr]) - st;
+            if constexpr (ONEQ) {
+                const int len = valid ? reinterpret_cast<const int *>(s_log)[rr] : -1;
+                sel = len >= 0;
+                if (sel) {
+                    st = s_o0[rr];
+                    n = len;
+                }
+            } else {
+                const float x = valid ? s_log[i * rpc + rr] - M : 0.f;
+                sel = valid && (all || x > thr);
+                if (valid && lv.dbg_S) lv.dbg_S[(size_t)bh * c + row] = expf(x - lD);
+                if (valid && lv.bitmap) lv.bitmap[(size_t)bh * c + row] = sel ? 1 : 0;
+                if (sel) {
+                    st = s_o0[rr];
+                    n = s_o1[rr] - st;
+                }
             }
             int pos, kpre, tc, tk;
             tile_scan(sel, n, pos, kpre, tc, tk);
@@ -657,6 +693,7 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         }
         if (tid == 0) { sh.cnt[i] = run; sh.keys[i] = runk; }
     }
+    SQZ_TRACE_AT(g_trace_look, 2);  // (overwrites the fold time: compaction done, before the barrier)
     cluster.sync();
     SQZ_TRACE_AT(g_trace_look, 3);
     // ---- cluster-wide offsets, then write the lists and expand the ranges ----
