@@ -356,6 +356,11 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
             if (k >= sg.a1) return 0;
             return k < ri.nkf ? ldcg(kidx + k) : -1 - (k - ri.nkf);
         };
+        // lane l (< KR) holds the position of key l of this warp's current round;
+        // the first positions are requested before the query row, so the two
+        // loads share one memory round trip
+        int j0 = sg.a0 + warp * KR;
+        int pos_cur = pos_of(j0, j0 + (lane & (KR - 1)));
         float q[8];
         load8(reinterpret_cast<const T *>(a.Q) + (size_t)sg.row * D + sub * 8, q);
         const float sc = a.scale * LOG2E;
@@ -364,10 +369,6 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
         float m_run = -INFINITY, l_lane = 0.f, o[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) o[k] = 0.f;
-
-        // lane l (< KR) holds the position of key l of this warp's current round
-        int j0 = sg.a0 + warp * KR;
-        int pos_cur = pos_of(j0, j0 + (lane & (KR - 1)));
         for (; j0 < sg.a1; j0 += NCW * KR) {
             const int nk = min(KR, sg.a1 - j0);
             Raw<T> kr[NS], vr[NS];

@@ -725,6 +725,9 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         }
     }
     __syncthreads();
+    // this CTA is done reading its peers' shared memory: arrive now, wait (so
+    // that its own stays alive for the peers' reads) only before exiting
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     for (int i = 0; i < nb; ++i) {
         const int bh = (b0 + i) * H + h;
         const int oc = s_oc[i], ok = s_ok[i];
@@ -744,7 +747,7 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         }
     }
     SQZ_TRACE_AT(g_trace_look, 4);
-    cluster.sync();  // keep this CTA's smem alive until every rank has read it
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     SQZ_TRACE_AT(g_trace_look, 5);
 }
 
