@@ -958,6 +958,9 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
     return cudaLaunchKernelEx(&cfg, kern, s, Q, lv, rpc);
 }
 
+#ifndef SQZ_LOOKUP_MIN_CTAS
+#define SQZ_LOOKUP_MIN_CTAS 256
+#endif
 template <typename T, int D, int NB, bool RL>
 static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
                                  int groups, cudaStream_t st) {
@@ -967,7 +970,7 @@ static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelAr
     // barriers), e.g. 2-CTA clusters for batched Level-2 lookups
     const int units = s.H * groups;
     auto ok = [&](int nc) {
-        return decode_smem_bytes(NB, (rowspace + nc - 1) / nc) <= 110 * 1024 && nc * units >= 256;
+        return decode_smem_bytes(NB, (rowspace + nc - 1) / nc) <= 110 * 1024 && nc * units >= SQZ_LOOKUP_MIN_CTAS;
     };
     if (ok(2)) return launch_decode_nc<T, D, NB, RL, 2>(s, Q, lv, rowspace, groups, st);
     if (ok(4)) return launch_decode_nc<T, D, NB, RL, 4>(s, Q, lv, rowspace, groups, st);
