@@ -64,6 +64,9 @@ extern "C" int sqz_trace_fin(void *host, size_t bytes) {
 constexpr int CH = 128;     // centroid rows per CTA
 constexpr int NT = 256;     // threads per CTA
 constexpr int NW = NT / 32;
+#ifndef SQZ_L2_PDL  // programmatic launch of the Level-2 (candidate-list) lookup
+#define SQZ_L2_PDL 0  // measured: cfg4 -2.5 us, cfg5 +50 us (the attention grid floods in)
+#endif
 constexpr int QT = 64;      // prefill queries per tile (8 warps x 8 queries)
 
 int lookup_chunk_rows() { return CH; }
@@ -353,6 +356,10 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
     // let the dependent attention grid launch now: its CTAs become resident and
     // park at griddepcontrol.wait until this grid has completed
     asm volatile("griddepcontrol.launch_dependents;");
+    // a candidate-list (Level-2) lookup is launched programmatically behind the
+    // kernel that wrote its candidates: it becomes resident as that grid drains
+    // and waits here for its completion
+    if (ROWLIST) asm volatile("griddepcontrol.wait;" ::: "memory");
     SQZ_TRACE_AT(g_trace_look, 0);
     const int rank = (int)cluster.block_rank();
     const int h = blockIdx.y, g = blockIdx.z;
@@ -939,13 +946,15 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = NC;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = RL && SQZ_L2_PDL ? 2 : 1;
 #ifdef SQZ_CARVEOUT_MAX
     {
         static bool done = false;
