@@ -64,6 +64,9 @@ extern "C" int sqz_trace_fin(void *host, size_t bytes) {
 constexpr int CH = 128;     // centroid rows per CTA
 constexpr int NT = 256;     // threads per CTA
 constexpr int NW = NT / 32;
+#ifndef SQZ_L2_LATE_DEP
+#define SQZ_L2_LATE_DEP 1
+#endif
 #ifndef SQZ_L2_PDL  // programmatic launch of the Level-2 (candidate-list) lookup
 #define SQZ_L2_PDL 0  // measured: cfg4 -2.5 us, cfg5 +50 us (the attention grid floods in)
 #endif
@@ -354,8 +357,10 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     // let the dependent attention grid launch now: its CTAs become resident and
-    // park at griddepcontrol.wait until this grid has completed
-    asm volatile("griddepcontrol.launch_dependents;");
+    // park at griddepcontrol.wait until this grid has completed.  A Level-2
+    // lookup that may run in more than one wave leaves the trigger to its CTAs'
+    // exits (parked attention CTAs would take the slots its later clusters need)
+    if (!ROWLIST || !SQZ_L2_LATE_DEP) asm volatile("griddepcontrol.launch_dependents;");
     // a candidate-list (Level-2) lookup is launched programmatically behind the
     // kernel that wrote its candidates: it becomes resident as that grid drains
     // and waits here for its completion
