@@ -149,6 +149,11 @@ DECODE_CASES = [
     ("hier_fp32_B8", 2, 3000, 64, 150, 30, synth.F32, 8, 0, 0.15),
     # B >= 4: Level 2 scans the whole table with per-query parent masks
     ("hier_bf16_B5", 3, 4000, 128, 200, 40, synth.BF16, 5, 20, 0.1),
+    # many rows whose streams are shorter than the decode partition's per-segment
+    # setup allowance (fewer CTAs than the grid, ranges mostly inside setup units)
+    ("bf16_many_short_rows", 16, 640, 128, 40, 0, synth.BF16, 12, 3, 0.05),
+    # no user keys and a very sparse selection: rows with no key at all
+    ("bf16_d64_sparse_nu0", 8, 700, 64, 50, 0, synth.BF16, 16, 0, 0.03),
 ]
 
 
