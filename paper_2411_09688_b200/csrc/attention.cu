@@ -40,7 +40,7 @@ constexpr int MIN_KEYS = 256;           // minimum keys per persistent CTA
 // segment's setup and epilogue (q load, position prefetch, pipeline refill,
 // partial write + ticket), so a CTA whose range straddles a row boundary gets
 // fewer keys (measured: ~2.3 us per extra segment at ~25 keys/us per CTA;
-// 128 was the best of 0 / 64 / 128 on cfg2).
+// 128 was the best of 0 / 64 / 128 on cfg2 and of 0 / 128 / 256 / 512 on cfg4).
 #ifndef SQZ_DEC_SEG_KW
 #define SQZ_DEC_SEG_KW 128
 #endif
