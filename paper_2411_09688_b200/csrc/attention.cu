@@ -33,7 +33,11 @@ SQZ_TRACE_DECL(g_trace_attn)
 
 constexpr int NCW = 4;                  // warps per CTA
 constexpr int NCT = NCW * 32;           // threads per CTA
-constexpr int KR = 16;                  // keys per warp round
+#ifndef SQZ_ATT_KR_BF16
+#define SQZ_ATT_KR_BF16 16
+#endif
+// keys per warp round (bf16 rows: tuning knob; fp32 rows take twice the registers)
+template <typename T> constexpr int keys_per_round() { return sizeof(T) == 2 ? SQZ_ATT_KR_BF16 : 16; }
 constexpr int MAX_PERSIST_CTAS = 1184;  // 148 SMs x 8
 constexpr int MIN_KEYS = 256;           // minimum keys per persistent CTA
 // Partition cost of a decode segment: its keys plus SEG_KW keys' worth for the
@@ -255,10 +259,11 @@ template <typename T, int D, bool PERSIST>
 __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
     constexpr int G = D / 8;          // lanes per key row (8 elements each)
     constexpr int KPW = 32 / G;       // key rows per warp instruction
+    constexpr int KR = keys_per_round<T>();
     constexpr int NS = KR / KPW;      // key slots per lane per round
     constexpr int LPS = G / NS;       // lanes holding each reduced key
     constexpr int LG_G = G == 16 ? 4 : 3;
-    constexpr int LG_NS = NS == 8 ? 3 : NS == 4 ? 2 : NS == 2 ? 1 : 0;
+    constexpr int LG_NS = NS == 16 ? 4 : NS == 8 ? 3 : NS == 4 ? 2 : NS == 2 ? 1 : 0;
 
     extern __shared__ __align__(16) int dyn_i[];
     int *s_pref = dyn_i;             // [rows + 1] (persistent)
