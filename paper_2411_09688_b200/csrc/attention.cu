@@ -33,6 +33,9 @@ SQZ_TRACE_DECL(g_trace_attn)
 
 constexpr int NCW = 4;                  // warps per CTA
 constexpr int NCT = NCW * 32;           // threads per CTA
+#ifndef SQZ_ATT_L2PF  // L2::256B prefetch hint on the K/V row loads (tuning knob)
+#define SQZ_ATT_L2PF 0
+#endif
 #ifndef SQZ_ATT_KR_BF16
 #define SQZ_ATT_KR_BF16 16
 #endif
@@ -60,9 +63,15 @@ int attention_max_parts(int64_t L, int n_u, int n_q) {
 template <typename T> struct Raw { uint4 v[sizeof(T) == 2 ? 1 : 2]; };
 __device__ __forceinline__ uint4 ld_nc_v4(const void *p) {
     uint4 u;
+#if SQZ_ATT_L2PF
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+                 : "l"(p));
+#else
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
                  : "l"(p));
+#endif
     return u;
 }
 template <typename T> __device__ __forceinline__ void ld_raw(Raw<T> &r, const T *p) {
