@@ -473,9 +473,7 @@ __global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
 #if SQZ_ATT_ACQREL
             // one acquire-release atomic: releases the CTA's partial (ordered before
             // it by the barrier), and acquires the other segments' partials for the merge
-            int t;
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                         : "=r"(t) : "l"(a.row_cnt + sg.row) : "memory");
+            const int t = ticket_acq_rel(a.row_cnt + sg.row);
 #else
             __threadfence();
             const int t = atomicAdd(a.row_cnt + sg.row, 1);

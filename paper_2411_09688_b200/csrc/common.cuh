@@ -143,6 +143,16 @@ __device__ __forceinline__ int runwin_pos(const RunWin &w, int k) {
     return (m < 32 ? t0 : t1) + (k - (m < 32 ? q0 : q1));
 }
 
+// Ticket of a "last CTA finishes the job" reduction, taken by ONE thread after a
+// block barrier: the acquire-release atomic publishes the CTA's earlier global
+// writes (ordered before it by the barrier) and, for the last CTA, makes every
+// other CTA's writes visible to the reads that follow the next barrier.
+__device__ __forceinline__ int ticket_acq_rel(int *p) {
+    int t;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(p) : "memory");
+    return t;
+}
+
 }  // namespace sqz
 
 // ---- optional device-side timeline tracing (experiments only: -DSQZ_TRACE) ----

@@ -909,16 +909,14 @@ __global__ void __launch_bounds__(NT) k_prefill_colsum(LookupShape s, const T *_
         }
     }
     __shared__ int s_last;
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-        const int t = atomicAdd(lv.tick + bh, 1);
+        const int t = ticket_acq_rel(lv.tick + bh);
         s_last = (t == (int)(gridDim.x * gridDim.y) - 1);
         if (s_last) lv.tick[bh] = 0;
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     finalize_colpart<ROWLIST>(lv, bh, h, nrows, nqt, s.B * s.H, 1.0f / (float)s.n_q);
 }
 
@@ -1309,17 +1307,15 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
         return;
     }
     // ---- the last CTA of this (b,h) averages the tiles and thresholds ----
-    __threadfence();
     __syncthreads();
     if (tid == 0) {
-        const int t = atomicAdd(lv.tick + bh, 1);
+        const int t = ticket_acq_rel(lv.tick + bh);
         s_last = (t == (int)gridDim.x - 1);
         if (s_last) lv.tick[bh] = 0;
     }
     __syncthreads();
     if (!s_last) return;
     SQZ_TRACE_AT(g_trace_pl, 4);
-    __threadfence();
     finalize_colpart<ROWLIST>(lv, bh, h, nrows, gridDim.x, s.B * s.H, 1.0f / (float)s.n_q);
     SQZ_TRACE_AT(g_trace_pl, 5);
 }
