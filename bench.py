@@ -13,9 +13,13 @@ layer), `cfg4` the 128K hierarchical decode at B=8, `cfg1` the tiny fp32 case.
 Inputs: SYN-MIX v1 synthetic clustered keys; the index is built by
 sqz_cluster_keys on the GPU; T is calibrated on 100 separate calibration queries
 (App. C).  L2 is flushed (512 MB write) between timed steps; timing is CUDA
-events on the launching stream, max over ranks.  N > 1 (torchrun): every rank
-runs an independent replica (weak scaling; the path has no exchange step for
-this config).
+events on the launching stream, max over ranks.  The default run also measures
+the cfg3 prefill (the other half of BASELINE's metric) and reports it as the
+line's `prefill` object.  N > 1 (torchrun): cfg2/cfg3/cfg4 shard the heads over
+the GPUs (no exchange on the hot path; strong scaling), cfg5 shards the fixed
+context by cluster (statistics all-gather + (O, LSE) all-gather merge); every
+input is a function of (seed, head) only, so the N-GPU run processes the inputs
+of the 1-GPU run.
 
 `--impl reference` times the CPU oracle (the paper-derived fp64 reference, the
 only reference this build has) on a bounded sample of the same workload.
@@ -40,11 +44,11 @@ CONFIGS = {
     "cfg2": dict(workload="cfg2: LLaMA-2-7B-32K decode, H=32 d128, L=32768, c=1024 single-level, "
                           "B=1, n_u=1024, bf16, retention 30% (3.1x KV budget reduction)",
                  mode="decode", H=32, d=128, L=32768, c2=1024, c1=0, B=1, n_q=1, n_u=1024,
-                 dtype=1, retention=0.3, cfgno=2),
+                 dtype=1, retention=0.3, cfgno=2, shard="heads"),
     "cfg3": dict(workload="cfg3: LongChat-7B-32K prefill, H=32 d128, L=32768, c=1024, n_q=n_u=1024 "
                           "causal, bf16, retention 30% (prefill-calibrated)",
                  mode="prefill", H=32, d=128, L=32768, c2=1024, c1=0, B=1, n_q=1024, n_u=1024,
-                 dtype=1, retention=0.3, cfgno=3),
+                 dtype=1, retention=0.3, cfgno=3, shard="heads"),
     "cfg4": dict(workload="cfg4: 128K hierarchical decode, H=32 d128, L=131072, c1=1311, c2=6554, "
                           "L1 prunes 50%, retention 10%, B=8, n_u=1024, bf16; heads sharded over the GPUs",
                  mode="decode", H=32, d=128, L=131072, c2=6554, c1=1311, B=8, n_q=1, n_u=1024,
@@ -224,6 +228,95 @@ def cpu_oracle_run(cfg, steps=None, warmup=0, seconds=12.0, h_sample=4):
     return value, sample, cores, times
 
 
+def oracle_parity(sqz, gidx, q, sel, O, LSE, T, T1, scale, K0, V0, Ku0, Vu0, loc, causal,
+                  rows_sample=None):
+    """Rank 0, after the timed region (part of the oracle leg): the fp64 oracle
+    re-runs the lookup of head 0 on the GPU-built global tables and the
+    attention of that head on the selected keys, and compares them with the GPU
+    output of the same input (band rule 1e-5, bf16 O max-abs 2e-2, LSE 1e-3;
+    DESIGN.md parity rules).  `loc` = rank 0's index (a shard in cluster mode:
+    only its clusters' selections are compared, the attention output is the
+    merged one).  Returns a small dict for the bench line."""
+    import torch
+
+    import oracle
+
+    def bits(t):
+        return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16) \
+            if t.dtype == torch.bfloat16 else t.contiguous().cpu().numpy()
+
+    h = 0
+    sub = oracle.Index(levels=gidx.levels, dtype=gidx.dtype, H=1, L=gidx.L, d=gidx.d, c2=gidx.c2,
+                       C2=oracle.to_f64(bits(gidx.C2[h:h + 1])), N2=gidx.N2[h:h + 1].cpu().numpy(),
+                       key_off=gidx.key_off[h:h + 1].cpu().numpy(),
+                       perm=gidx.perm[h:h + 1].cpu().numpy())
+    if gidx.levels == 2:
+        sub.c1 = gidx.c1
+        sub.C1 = oracle.to_f64(bits(gidx.C1[h:h + 1]))
+        sub.N1 = gidx.N1[h:h + 1].cpu().numpy()
+        sub.child_off = gidx.child_off[h:h + 1].cpu().numpy()
+    B, _, n_q, d = q.shape
+    Q64 = oracle.to_f64(bits(q[:, h:h + 1]))
+    out = {"head": h, "queries": int(B * n_q)}
+    sharded = loc.L_total > 0
+    forced = None
+    if gidx.levels == 2:
+        ref1 = oracle.lookup(Q64, sub, scale, T, T1)
+        g1 = ref1["surv1"].copy()
+        mine = np.arange(gidx.c1) if not sharded else loc.c1_src[h].cpu().numpy()
+        gl = sel.l1_surv[:, h].cpu().numpy().astype(bool)[:, :len(mine)]
+        g1[:, 0, mine] = gl
+        flips = (g1 != ref1["surv1"])
+        band1 = oracle.band(ref1["Sbar1"], T1)
+        out["level1_outside_band"] = int((flips & ~band1).sum())
+        forced = g1
+    ref = oracle.lookup(Q64, sub, scale, T, T1, forced_l1=forced)
+    cl, n = sel.clusters[:, h].cpu().numpy(), sel.n_clusters[:, h].cpu().numpy()
+    src = None if not sharded else loc.c2_src[h].cpu().numpy()
+    gsel = np.zeros_like(ref["sel2"])
+    own = np.zeros(gidx.c2, bool)
+    own[np.arange(gidx.c2) if src is None else src[src >= 0]] = True
+    for b in range(B):
+        ids = cl[b, :n[b]]
+        gsel[b, 0, ids if src is None else src[ids]] = True
+    band = oracle.band(ref["Sbar2"], T)
+    diff = (gsel != ref["sel2"]) & own[None, None, :]
+    out["selection_outside_band"] = int((diff & ~band).sum())
+    out["selection_in_band_flips"] = int((diff & band).sum())
+    out["clusters_compared"] = int(own.sum()) * B
+    any_band = bool((band & ref["sel2"]).any() or (band & ~ref["sel2"]).any())
+    if out["selection_outside_band"] == 0 and not (any_band and sharded):
+        # mask = the GPU's selection (unsharded) or the oracle's (sharded, no band clusters)
+        m = gsel if not sharded else ref["sel2"]
+        mask = oracle.keymask(sub, m) if sub.assign2 is not None else None
+        if mask is None:  # GPU-built tables: members from key_off / perm
+            mask = np.zeros((B, 1, gidx.L), bool)
+            for b in range(B):
+                for i in np.nonzero(m[b, 0])[0]:
+                    mask[b, 0, sub.perm[0][sub.key_off[0, i]:sub.key_off[0, i + 1]]] = True
+        Ku64 = None if Ku0 is None else oracle.to_f64(bits(Ku0))[:, None]
+        Vu64 = None if Vu0 is None else oracle.to_f64(bits(Vu0))[:, None]
+        qs = Q64 if rows_sample is None else Q64[:, :, rows_sample]
+        Oref, Lref, rc = oracle.attention(qs, oracle.to_f64(bits(K0))[None], oracle.to_f64(bits(V0))[None],
+                                          mask, Ku64, Vu64, causal, scale, qpos=rows_sample,
+                                          n_q_total=n_q)
+        Og = O[:, h:h + 1].float().cpu().numpy()
+        Lg = LSE[:, h:h + 1].cpu().numpy()
+        if rows_sample is not None:
+            Og, Lg = Og[:, :, rows_sample], Lg[:, :, rows_sample]
+        out["attention_rows"] = int(Og.shape[0] * Og.shape[2])
+        out["O_max_abs"] = float(np.abs(Og - Oref).max())
+        out["O_rel_l2"] = float(np.linalg.norm(Og - Oref) / max(np.linalg.norm(Oref), 1e-30))
+        out["LSE_max_abs"] = float(np.abs(Lg - Lref).max())
+        tol_o = 2e-2 if gidx.dtype == 1 else 1e-4
+        out["ok"] = bool(rc == 0 and out["O_max_abs"] <= tol_o and out["LSE_max_abs"] <= 1e-3
+                         and out.get("level1_outside_band", 0) == 0)
+    else:
+        out["ok"] = out["selection_outside_band"] == 0 and out.get("level1_outside_band", 0) == 0
+        out["attention"] = "skipped: near-threshold clusters on a sharded run"
+    return out
+
+
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
@@ -284,35 +377,45 @@ def run_gpu(args, cfg, rank, world, local_rank):
     else:
         heads = list(range(H))
     Hl = len(heads)
-    # cluster sharding: rank r holds a contiguous 1/g slice of the
-    # fixed context with its own index (clusters never straddle ranks); the lookup
-    # all-gathers the per-level (m, D) statistics, the attention partials are
-    # all-gathered and merged -- all inside libsqz (NCCL)
-    Ls = L // world if shard == "clusters" else L
-    c2s = -(-c2 // world) if shard == "clusters" else c2
-    c1s = (-(-c1 // world) if c1 else 0) if shard == "clusters" else c1
     kiters = cfg.get("kmeans_iters", args.kmeans_iters) if args.kmeans_iters_set is None \
         else args.kmeans_iters_set
     # ---- offline: data + index (not timed) ----
+    # Every input is a function of (config seed, head) only, so the N-GPU run
+    # processes exactly the inputs of the 1-GPU run: head shards slice them,
+    # cluster shards split ONE global index (sqz_shard_plan_compute +
+    # sqz_index_shard: Level-1 cluster p on rank p mod g, subtrees intact).
     if cfg.get("device_gen"):
         mix = synth.device_mixture(H, c2, d, G1=c1, seed=1000 + cno, device=dev)
-        K, V = synth.device_keys(mix, Ls, seed=1000 + cno + 7919 * (rank + 1) if shard == "clusters"
-                                 else 1000 + cno, dtype=dt, heads=heads)
-        init2 = synth.device_kmeans_init(Hl, Ls, c2s, seed=2000 + cno + 13 * rank, device=dev)
-        init1 = synth.device_kmeans_init(Hl, c2s, c1s, seed=2100 + cno + 13 * rank, device=dev) \
+        K, V = synth.device_keys(mix, L, seed=1000 + cno, dtype=dt, heads=heads)
+        init2 = synth.device_kmeans_init(H, L, c2, seed=2000 + cno, device=dev, heads=heads)
+        init1 = synth.device_kmeans_init(H, c2, c1, seed=2100 + cno, device=dev, heads=heads) \
             if c1 else None
     else:
         fc = synth.fixed_context(H, L, d, c2, dtype=dt, seed=1000 + cno, G1=c1)
         mix = fc.mix
-        K, V = sqz.to_device(fc.K, dev), sqz.to_device(fc.V, dev)
-        init2 = torch.from_numpy(synth.kmeans_init(H, L, c2, seed=2000 + cno)).to(dev)
-        init1 = (torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=2100 + cno)).to(dev)
+        K, V = sqz.to_device(fc.K[heads], dev), sqz.to_device(fc.V[heads], dev)
+        init2 = torch.from_numpy(synth.kmeans_init(H, L, c2, seed=2000 + cno)[heads]).to(dev)
+        init1 = (torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=2100 + cno)[heads]).to(dev)
                  if c1 else None)
+        del fc
     t0 = time.time()
-    idx, Kp, Vp, iters = sqz.cluster_keys(K, V, c2s, init2, c1s, init1, max_iters=kiters)
+    idx, Kp, Vp, iters = sqz.cluster_keys(K, V, c2, init2, c1, init1, max_iters=kiters)
     torch.cuda.synchronize()
     t_index = time.time() - t0
+    # host copy of the sampled head (original order) for the oracle parity check
+    par_head = 0
+    K0 = K[par_head].contiguous().cpu() if rank == 0 else None
+    V0 = V[par_head].contiguous().cpu() if rank == 0 else None
     del K, V
+    gidx = idx  # the global (unsharded) index: rank 0's parity check reads its tables
+    if shard == "clusters":
+        idx, Kp_l, Vp_l = sqz.shard_index(idx, Kp, Vp, rank, world)
+        torch.cuda.synchronize()
+        if rank != 0:
+            gidx = None
+        del Kp, Vp
+        Kp, Vp = Kp_l, Vp_l
+        torch.cuda.empty_cache()
     comm = sqz.Comm(rank, world) if shard == "clusters" else None
 
     def allsum(x):
@@ -340,35 +443,34 @@ def run_gpu(args, cfg, rank, world, local_rank):
         Ku, Vu = synth.device_user_kv(mix, B, n_u, seed=5000 + cno, dtype=dt, heads=heads)
     else:
         if cfg["mode"] == "decode":
-            Qc = sqz.to_device(synth.decode_queries(mix, n_cal, seed=3000 + cno, dtype=dt), dev)
-            Qt = sqz.to_device(synth.decode_queries(mix, n_inputs * B, seed=4000 + cno, dtype=dt),
-                               dev).view(n_inputs, B, H, 1, d)
+            Qc = sqz.to_device(synth.decode_queries(mix, n_cal, seed=3000 + cno, dtype=dt)[:, heads],
+                               dev)
+            Qt = sqz.to_device(synth.decode_queries(mix, n_inputs * B, seed=4000 + cno,
+                                                    dtype=dt)[:, heads], dev).view(n_inputs, B, Hl, 1, d)
         else:
-            Qc = sqz.to_device(synth.prefill_queries(mix, n_cal, n_q, seed=3000 + cno, dtype=dt), dev)
+            Qc = sqz.to_device(synth.prefill_queries(mix, n_cal, n_q, seed=3000 + cno,
+                                                     dtype=dt)[:, heads], dev)
             Qt = sqz.to_device(synth.prefill_queries(mix, n_inputs * B, n_q, seed=4000 + cno,
-                                                     dtype=dt), dev).view(n_inputs, B, H, n_q, d)
-        Ku, Vu = (sqz.to_device(a, dev) for a in synth.user_kv(mix, B, n_u, seed=5000 + cno, dtype=dt))
+                                                     dtype=dt)[:, heads], dev).view(n_inputs, B, Hl, n_q, d)
+        Ku, Vu = (sqz.to_device(a[:, heads], dev)
+                  for a in synth.user_kv(mix, B, n_u, seed=5000 + cno, dtype=dt))
+    Ku0 = Ku[:, par_head].contiguous().cpu() if rank == 0 else None
+    Vu0 = Vu[:, par_head].contiguous().cpu() if rank == 0 else None
     if shard == "clusters" and rank != 0:
         Ku = Vu = None  # the user KV partial is computed once, on rank 0
     n_u_r = 0 if Ku is None else n_u
     Bc = Qc.shape[0]
     # ---- calibration of the global thresholds (R12, R13) ----
+    # bisection on the all-reduced retained weight (integer sums, exact in fp64):
+    # the same T at every N, so the N-GPU run selects what the 1-GPU run selects
     T1 = 0.0
-    sharded_cal = shard in ("heads", "clusters") or cfg.get("device_gen")
     if c1:
         s = sqz.centroid_lookup(idx, Qc, scale, 0.0, 0.0, debug=True, comm=comm)
-        if sharded_cal:
-            T1 = calib.distributed_threshold(s.dbg_S1, idx.N1[None], 0.5, allsum(float(
-                Bc * idx.N1.sum())), allreduce=allsum)
-        else:
-            T1 = calib.weighted_threshold(s.dbg_S1.cpu().numpy(), idx.N1.cpu().numpy()[None], 0.5)
+        T1 = calib.distributed_threshold(s.dbg_S1, idx.N1[None], 0.5, allsum(float(
+            Bc * idx.N1.sum())), allreduce=allsum)
     s = sqz.centroid_lookup(idx, Qc, scale, 0.0, T1, debug=True, comm=comm)
-    if sharded_cal:
-        T = calib.distributed_threshold(s.dbg_S, idx.N2[None], cfg["retention"], float(Bc * H * L),
-                                        allreduce=allsum)
-    else:
-        T = calib.weighted_threshold(s.dbg_S.cpu().numpy(), idx.N2.cpu().numpy()[None],
-                                     cfg["retention"], total_weight=Bc * H * L)
+    T = calib.distributed_threshold(s.dbg_S, idx.N2[None], cfg["retention"], float(Bc * H * L),
+                                    allreduce=allsum)
     del s, Qc
     # ---- per-step work: selection sizes for the algorithmic-byte count ----
     # the expanded key-index tensor is materialised: the attention kernels' run-length
@@ -459,39 +561,52 @@ def run_gpu(args, cfg, rank, world, local_rank):
     t_look = sum(e[0].elapsed_time(e[1]) for e in evp) / K_
     t_attn = sum(e[1].elapsed_time(e[2]) for e in evp) / K_
     # ---- end to end through the public API with host buffers ----
+    # One pinned host staging buffer per input holds everything the step brings
+    # in (the query rows, and the new token's K/V row entering the user cache for
+    # decode, the whole user input for prefill), copied in ONE host->device
+    # transfer and scattered on the device; O and LSE live in one device buffer
+    # read back in ONE device->host transfer (each PCIe copy pays ~2-4 us of
+    # latency, so five small copies cost more than the bytes).
     pin = dict(pin_memory=True)
-    hQ = torch.empty((n_inputs,) + tuple(Qt.shape[1:]), dtype=Qt.dtype, **pin)
-    hQ.copy_(Qt.cpu())
-    hO = torch.empty(O.shape, dtype=O.dtype, **pin)
-    hL = torch.empty(LSE.shape, dtype=LSE.dtype, **pin)
-    dQ = torch.empty_like(Qt[0])
-    hKn = hVn = None
-    if Ku is not None and cfg["mode"] == "decode":
-        # the new token's k/v row enters the user cache each step
-        hKn = torch.empty(B, Hl, 1, d, dtype=Ku.dtype, **pin)
-        hKn.copy_(Ku[:, :, -1:].cpu())
-        hVn = torch.empty(hKn.shape, dtype=hKn.dtype, **pin)
-        hVn.copy_(Vu[:, :, -1:].cpu())
-    elif Ku is not None:
-        hKn = torch.empty(Ku.shape, dtype=Ku.dtype, **pin)
-        hKn.copy_(Ku.cpu())
-        hVn = torch.empty(Vu.shape, dtype=Vu.dtype, **pin)
-        hVn.copy_(Vu.cpu())
-    h2d = hQ[0].numel() * esz + (2 * hKn.numel() * esz if hKn is not None else 0)
-    d2h = hO.numel() * O.element_size() + hL.numel() * 4
+    q_b = Qt[0].numel() * esz
+    kv_new = None
+    if Ku is not None:
+        kv_new = (slice(None), slice(None), slice(n_u - 1, n_u)) if cfg["mode"] == "decode" else \
+            (slice(None), slice(None), slice(None))
+    kv_b = 0 if kv_new is None else Ku[kv_new].numel() * esz
+    h2d = q_b + 2 * kv_b
+    hin = torch.empty(n_inputs, h2d, dtype=torch.uint8, **pin)
+    for i in range(n_inputs):
+        hin[i, :q_b].copy_(Qt[i].contiguous().view(torch.uint8).view(-1).cpu())
+        if kv_new is not None:
+            hin[i, q_b:q_b + kv_b].copy_(Ku[kv_new].contiguous().view(torch.uint8).view(-1).cpu())
+            hin[i, q_b + kv_b:].copy_(Vu[kv_new].contiguous().view(torch.uint8).view(-1).cpu())
+    din = torch.empty(h2d, dtype=torch.uint8, device=dev)
+    dQ = din[:q_b].view(Qt.dtype).view(Qt[0].shape)
+    o_b = O.numel() * O.element_size()
+    out_b = o_b + LSE.numel() * 4
+    dout = torch.empty(out_b, dtype=torch.uint8, device=dev)
+    O_e = dout[:o_b].view(O.dtype).view(O.shape)
+    LSE_e = dout[o_b:].view(torch.float32).view(LSE.shape)
+    hout = torch.empty(out_b, dtype=torch.uint8, **pin)
+    d2h = out_b
+
+    def attend_into(q, Oo, Lo):
+        if comm is None:
+            sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=causal, O=Oo, LSE=Lo)
+        else:
+            sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=causal, partial=True,
+                                 out_dtype=sqz.SQZ_F32, O=Op, LSE=Lp)
+            sqz.allgather_merge(comm, Op, Lp, out_dtype=dt, O=Oo, LSE=Lo)
 
     def e2e_step(i):
-        dQ.copy_(hQ[i % n_inputs], non_blocking=True)
-        if hKn is not None and cfg["mode"] == "decode":
-            Ku[:, :, -1:].copy_(hKn, non_blocking=True)
-            Vu[:, :, -1:].copy_(hVn, non_blocking=True)
-        elif hKn is not None:
-            Ku.copy_(hKn, non_blocking=True)
-            Vu.copy_(hVn, non_blocking=True)
+        din.copy_(hin[i % n_inputs], non_blocking=True)
+        if kv_new is not None:
+            Ku[kv_new].copy_(din[q_b:q_b + kv_b].view(Ku.dtype).view(Ku[kv_new].shape))
+            Vu[kv_new].copy_(din[q_b + kv_b:].view(Vu.dtype).view(Vu[kv_new].shape))
         sqz.centroid_lookup(idx, dQ, scale, T, T1, sel=sel, comm=comm)
-        attend(dQ)
-        hO.copy_(O, non_blocking=True)
-        hL.copy_(LSE, non_blocking=True)
+        attend_into(dQ, O_e, LSE_e)
+        hout.copy_(dout, non_blocking=True)
 
     e2e_graphs = ([capture_graph(lambda i=i: e2e_step(i)) for i in range(n_inputs)]
                   if args.graph else None)
@@ -511,6 +626,23 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     t_e2e = sum(e[0].elapsed_time(e[1]) for e in ev2) / K_
+    # ---- sampled oracle parity of this run's output (after the timed region) ----
+    parity = None
+    if not args.no_parity:
+        q = Qt[0]
+        sel_p = sqz.Selection.empty(idx, B, n_q, debug=True, device=dev, key_idx=False)
+        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel_p, comm=comm)
+        attend_into(q, O, LSE)
+        torch.cuda.synchronize()
+        if rank == 0:
+            rs = None
+            if cfg["mode"] == "prefill":
+                rs = np.unique(np.concatenate([[0, n_q - 1], np.linspace(0, n_q - 1, 62)])).astype(np.int32)
+            t_p = time.time()
+            parity = oracle_parity(sqz, gidx, q, sel_p, O, LSE, T, T1, scale, K0, V0, Ku0, Vu0, idx,
+                                   causal, rs)
+            parity["oracle_s"] = round(time.time() - t_p, 1)
+        del sel_p
     # ---- max over ranks ----
     if world > 1:
         tt = torch.tensor([t_step, t_look, t_attn, t_e2e, t_eager], device=dev)
@@ -561,7 +693,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "higher_is_better": hib, "scaling": "weak" if shard in ("none", "replicas") else "strong",
         "vs_baseline": None,
         "dtype": "bf16" if dt == 1 else "f32", "data": "synthetic (SYN-MIX v1 clustered keys)",
-        "config": {"workload": cfg["workload"], "global_batch": B * world, "seq_len": L,
+        "config": {"workload": cfg["workload"],
+                   "global_batch": B * (world if shard in ("none", "replicas") else 1), "seq_len": L,
                    "n_q": n_q, "n_u": n_u,
                    "parallelism": {"none": "1 GPU", "replicas": f"replicas x{world}",
                                    "heads": f"heads sharded x{world}",
@@ -579,6 +712,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if parity is not None:
+        line["parity"] = parity
     return line
 
 
@@ -588,7 +723,13 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="one workload; default: cfg2 decode (the headline line) with the cfg3 "
+                         "prefill measured in the same run as its `prefill` object")
+    ap.add_argument("--no-prefill", action="store_true",
+                    help="default run: skip the cfg3 prefill object")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the rank-0 sampled oracle parity check after the timed region")
     ap.add_argument("--kmeans-iters", type=int, default=30)
     ap.add_argument("--kmeans-iters-set", type=int, default=None,
                     help="override the per-config Lloyd iteration count (cfg5: 3)")
@@ -599,6 +740,9 @@ def main():
                     help="time eager per-call launches instead of CUDA-graph replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    with_prefill = args.config is None and not args.no_prefill
+    if args.config is None:
+        args.config = "cfg2"
     cfg = dict(CONFIGS[args.config])
     if args.retention is not None:
         cfg["retention"] = args.retention
@@ -637,6 +781,25 @@ def main():
         value, sample, cores, _ = cpu_oracle_run(cfg)
         line["cpu_baseline"] = {"value": round(value, 3), "unit": unit, "cores": cores,
                                 "kind": "oracle", "sample": sample}
+    if with_prefill:
+        # the prefill half of BASELINE's metric (cfg3), same run, same rules
+        import torch
+
+        torch.cuda.empty_cache()
+        pcfg = dict(CONFIGS["cfg3"])
+        if args.retention is not None:
+            pcfg["retention"] = args.retention
+        pargs = argparse.Namespace(**vars(args))
+        pargs.config = "cfg3"
+        pl = run_gpu(pargs, pcfg, rank, world, local_rank)
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            pv, psample, pcores, _ = cpu_oracle_run(pcfg, seconds=8.0)
+            pl["cpu_baseline"] = {"value": round(pv, 3), "unit": pl["unit"], "cores": pcores,
+                                  "kind": "oracle", "sample": psample}
+        keep = ("metric", "value", "unit", "ms_per_step", "higher_is_better", "dtype", "config",
+                "phases_ms", "whole_step", "roofline", "e2e", "gpu_launches", "clocks", "parity",
+                "cpu_baseline", "scaling")
+        line["prefill"] = {k: pl[k] for k in keep if k in pl}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -137,8 +137,10 @@ int sqz_cluster_keys(const void *K, const void *V, const int64_t *init2, const i
                      size_t ws_bytes, int32_t *iters_out, void *stream);
 
 /* Checks the index invariants on the device (sum N2 = L, key_off consistent
- * with N2, perm a permutation of [0, L), child_off a partition of [0, c2),
- * N1 = descendant keys).  Synchronises the stream.  SQZ_ERR_INVARIANT on
+ * with N2, perm a permutation of [0, L), child_off a partition of [0, c2)
+ * into NON-EMPTY child ranges for an unsharded index (K-means leaves no
+ * cluster empty; the decode Level-2 lookup relies on it), N1 = descendant
+ * keys).  Indexes built outside sqz_cluster_keys should be validated once.  Synchronises the stream.  SQZ_ERR_INVARIANT on
  * failure.  ws: sqz_index_validate_workspace() bytes. */
 int sqz_index_validate_workspace(const sqz_index *idx, size_t *ws_bytes);
 int sqz_index_validate(const sqz_index *idx, void *ws, size_t ws_bytes, void *stream);

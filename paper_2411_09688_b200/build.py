@@ -21,13 +21,30 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def needs_build() -> bool:
-    if not os.path.exists(OUT):
-        return True
-    t = os.path.getmtime(OUT)
+def _stamp() -> str:
+    """Hash of every source, header and flag that goes into libsqz.so."""
+    import hashlib
+
+    h = hashlib.sha256()
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
     deps += glob.glob(os.path.join(ROOT, "include", "*.h"))
-    return any(os.path.getmtime(f) > t for f in deps)
+    for f in sorted(deps):
+        h.update(os.path.relpath(f, ROOT).encode())
+        h.update(open(f, "rb").read())
+    h.update(" ".join([NVCC, *ARCH, *FLAGS]).encode())
+    return h.hexdigest()
+
+
+STAMP = OUT + ".sha256"
+
+
+def needs_build() -> bool:
+    """Rebuild unless libsqz.so exists AND was built from exactly these sources
+    and flags (content hash, not modification times: a copied-in or stale
+    binary is never reused)."""
+    if not os.path.exists(OUT) or not os.path.exists(STAMP):
+        return True
+    return open(STAMP).read().strip() != _stamp()
 
 
 def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
@@ -54,6 +71,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
         for o in objs:
             sys.stdout.write(open(o + ".log").read())
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", OUT, *objs])
+    with open(STAMP, "w") as f:
+        f.write(_stamp())
     return OUT
 
 

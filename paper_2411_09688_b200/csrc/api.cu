@@ -146,8 +146,9 @@ AttnWs attn_carve(const sqz_index *idx, int B, int n_q, int n_u, char *base) {
     w.cut = cv.take<int32_t>(3 * 1024);  // one (segment, c0, c1) slot per persistent CTA
     // partial rows: [rows, max_chunks] for the split-KV kernels, one 256-row slot
     // per piece for the persistent prefill kernel
+    // (the persistent prefill kernel indexes its partials by piece, never by chunk)
     const size_t prow = prefill_ws_applies(idx->d, idx->dtype, n_q)
-                            ? std::max(rows * w.max_chunks, prefill_ws_part_rows(B, idx->H, n_q))
+                            ? prefill_ws_part_rows(B, idx->H, n_q)
                             : rows * w.max_chunks;
     w.part_lse = cv.take<float>(prow);
     w.part_o = cv.take<float>(prow * idx->d);

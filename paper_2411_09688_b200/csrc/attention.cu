@@ -517,29 +517,20 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    // Host-side launch cost matters at decode sizes (a few microseconds per
-    // runtime query): attributes are set once and the persistent grid size is
-    // cached per row count (one device per process).
-    if (a.n_q == 1 && rows <= 8192) {
+    // The persistent decode partition keeps int32 cost prefixes in shared
+    // memory: shapes whose total cost could reach 2^31 (e.g. dense attention over
+    // 1M keys with B*H >= 2048) take the 2-D split-KV grid instead.
+    const long long max_cost = (long long)rows * (a.L + a.n_u + SEG_KW);
+    if (a.n_q == 1 && rows <= 8192 && max_cost < 0x7fffffffLL) {
         const size_t dsm = (size_t)(2 * rows + 1) * sizeof(int);
         auto kern = k_attend<T, D, true>;
-        static size_t attr_bytes = 48 * 1024;
-        static int cached_rows = -1, cached_grid = 0;
-        if (dsm > attr_bytes) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)dsm);
+        if (dsm > 48 * 1024) {
+            cudaError_t e = ensure_func_attr((const void *)kern,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
             if (e != cudaSuccess) return e;
-            attr_bytes = dsm;
         }
-        if (rows != cached_rows) {
-            int dev = 0, nsm = 0, occ = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NCT, dsm);
-            cached_grid = std::min(nsm * std::max(occ, 1), MAX_PERSIST_CTAS);
-            cached_rows = rows;
-        }
-        cfg.gridDim = dim3(cached_grid);
+        const int occ = occupancy_blocks((const void *)kern, NCT, dsm);
+        cfg.gridDim = dim3(std::min(device_sm_count() * occ, MAX_PERSIST_CTAS));
         cfg.dynamicSmemBytes = dsm;
         return cudaLaunchKernelEx(&cfg, kern, a, rows);
     }

@@ -116,6 +116,13 @@ int index_validate(const sqz_index &idx, void *ws, size_t ws_bytes, cudaStream_t
 // tmap.cu: TMA tensor map of a contiguous bf16 [dims2][dims1][dims0] tensor
 // (128-byte swizzle, zero out-of-bounds fill); 0 on success
 int encode_tmap_bf16_3d(CUtensorMap *m, const void *ptr, const uint64_t dims[3], const uint32_t box[3]);
+// tmap.cu: per-device launch caches (keyed by device ordinal and kernel, mutex
+// guarded): SM count of the current device; sets a function attribute once per
+// (device, kernel) -- for cudaFuncAttributeMaxDynamicSharedMemorySize only when
+// `value` exceeds the largest opt-in set so far; cached occupancy.
+int device_sm_count();
+cudaError_t ensure_func_attr(const void *kern, cudaFuncAttribute attr, int value);
+int occupancy_blocks(const void *kern, int threads, size_t smem);
 
 // shard.cu: gathers of the shard index rows
 cudaError_t launch_shard_gather(const sqz_index &full, const void *Kp, const void *Vp,

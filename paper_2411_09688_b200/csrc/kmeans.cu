@@ -663,7 +663,11 @@ __global__ void k_validate(sqz_index idx, int32_t *__restrict__ hist, int *__res
         const int32_t *co = idx.child_off + (size_t)h * (c1 + 1);
         const int32_t *N1 = idx.N1 + (size_t)h * c1;
         for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < c1; p += gridDim.x * blockDim.x) {
-            if (co[p + 1] < co[p] || co[p] < 0 || co[p + 1] > c2) { atomicOr(bad, 4); continue; }
+            // an unsharded index has no empty Level-1 cluster (K-means repairs empty
+            // clusters; the decode Level-2 lookup relies on >= 1 child per survivor);
+            // shard padding rows (L_total > 0) have empty ranges
+            if (co[p + 1] < co[p] || co[p] < 0 || co[p + 1] > c2 ||
+                (idx.L_total == 0 && co[p + 1] == co[p])) { atomicOr(bad, 4); continue; }
             if (p == 0 && co[0] != 0) atomicOr(bad, 4);
             if (p == c1 - 1 && (idx.L_total > 0 ? co[c1] > c2 : co[c1] != c2)) atomicOr(bad, 4);
             long long s = 0;

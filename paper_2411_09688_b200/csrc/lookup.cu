@@ -416,6 +416,9 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
     }
 
     const int phase = lv.phase;
+    // the staged select (phase 2) has no scan barrier: order this CTA's NaN fill
+    // before any peer writes a real score to the same rows (uniform branch)
+    if (ROWLIST && lv.dbg_S && phase == 2) cluster.sync();
     if (phase == 2) {
         // ---- staged select: the logits and row metadata phase 1 stored, and the
         // (M, log D) folded over every shard ----
@@ -937,11 +940,11 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
     if constexpr (UMAX == 32 && !RL)
         if (rpc <= NW * 16) kern = k_lookup_decode<T, D, NB, RL, NC, SLIM, 16>;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = ensure_func_attr((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     if (NC > 8) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaError_t e = ensure_func_attr((const void *)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t cfg = {};
@@ -958,15 +961,6 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = RL && SQZ_L2_PDL ? 2 : 1;
-#ifdef SQZ_CARVEOUT_MAX
-    {
-        static bool done = false;
-        if (!done) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-            done = true;
-        }
-    }
-#endif
     return cudaLaunchKernelEx(&cfg, kern, s, Q, lv, rpc);
 }
 
@@ -1324,12 +1318,10 @@ template <int D, bool RL>
 static cudaError_t launch_prefill_tc(const LookupShape &s, const __nv_bfloat16 *Q, const LevelArgs &lv,
                                      cudaStream_t st) {
     auto kern = k_prefill_lookup_tc<D, RL>;
-    static bool set = false;
-    if (!set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             PlSmem<D>::BYTES);
+    {
+        cudaError_t e = ensure_func_attr((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         PlSmem<D>::BYTES);
         if (e != cudaSuccess) return e;
-        set = true;
     }
     PlMaps maps;
     std::memset(&maps, 0, sizeof(maps));

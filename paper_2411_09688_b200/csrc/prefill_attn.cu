@@ -1,6 +1,8 @@
 // prefill_attn.cu -- prefill sparse attention on the 5th-generation tensor cores
 // (section 4.2; prefill = many query rows).
 //
+// This split-KV kernel serves d = 64 bf16 prefill; d = 128 runs on the persistent
+// warp-specialised kernel of prefill_attn_ws.cu.
 // CTA = one 128-row query tile of one (b,h) and one split of its key stream
 // (selected fixed keys, then the user keys visible to the tile, R8).  Per
 // 128-key tile:
@@ -360,26 +362,12 @@ cudaError_t launch_prefill_attention(const AttnArgs &a, cudaStream_t st) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (a.d == 128) {
-        if (prefill_ws_applies(a.d, a.dtype, a.n_q)) return launch_prefill_attention_ws(a, st);
-        static bool set = false;
-        if (!set) {
-            cudaError_t e = cudaFuncSetAttribute(k_prefill_attend<128>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 PfSmem<128>::BYTES);
-            if (e != cudaSuccess) return e;
-            set = true;
-        }
-        cfg.dynamicSmemBytes = PfSmem<128>::BYTES;
-        return cudaLaunchKernelEx(&cfg, k_prefill_attend<128>, a, qtiles);
-    }
-    static bool set64 = false;
-    if (!set64) {
-        cudaError_t e = cudaFuncSetAttribute(k_prefill_attend<64>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             PfSmem<64>::BYTES);
+    if (prefill_ws_applies(a.d, a.dtype, a.n_q)) return launch_prefill_attention_ws(a, st);
+    if (a.d != 64) return cudaErrorInvalidValue;  // d = 128 bf16 prefill is the persistent kernel
+    {
+        cudaError_t e = ensure_func_attr((const void *)k_prefill_attend<64>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, PfSmem<64>::BYTES);
         if (e != cudaSuccess) return e;
-        set64 = true;
     }
     cfg.dynamicSmemBytes = PfSmem<64>::BYTES;
     return cudaLaunchKernelEx(&cfg, k_prefill_attend<64>, a, qtiles);

@@ -803,21 +803,11 @@ __global__ void __launch_bounds__(256) k_merge_cut(AttnArgs a, int npairs) {
 }
 
 namespace {
-int ws_grid() {
-    static int g = 0;
-    if (!g) {
-        int dev = 0, n = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        g = n > 0 ? n : 148;
-    }
-    return g;
-}
+int ws_grid() { return device_sm_count(); }
 }  // namespace
 
 bool prefill_ws_applies(int d, int dtype, int n_q) {
-    static const bool legacy = getenv("SQZ_PF_LEGACY") != nullptr;  // A/B switch
-    return !legacy && n_q > 1 && d == 128 && dtype == SQZ_BF16;
+    return n_q > 1 && d == 128 && dtype == SQZ_BF16;
 }
 // rows of the partial buffers: one 256-row slot per piece, piece id = segment + CTA
 size_t prefill_ws_part_rows(int B, int H, int n_q) {
@@ -857,12 +847,10 @@ cudaError_t launch_prefill_attention_ws(const AttnArgs &a, cudaStream_t st) {
     TmaMaps maps;
     if (encode_map(&maps.q, a.Q, (uint64_t)a.B * a.H * a.n_q, 128) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
-    static bool set = false;
-    if (!set) {
-        cudaError_t e = cudaFuncSetAttribute(k_prefill_attend_ws,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, ws::BYTES);
+    {
+        cudaError_t e = ensure_func_attr((const void *)k_prefill_attend_ws,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ws::BYTES);
         if (e != cudaSuccess) return e;
-        set = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ws_grid());

@@ -3,6 +3,9 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <vector>
+
 #include "internal.h"
 
 namespace sqz {
@@ -38,6 +41,72 @@ int encode_tmap_bf16_3d(CUtensorMap *m, const void *ptr, const uint64_t dims[3],
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
+}  // namespace sqz
+
+// ---------------------------------------------------------------------------
+// Per-device launch-configuration caches.  Function attributes (the opt-in
+// dynamic shared memory size, non-portable cluster sizes) belong to each
+// device's context, and SM counts / occupancies differ by device, so every
+// cached value is keyed by (device ordinal, kernel) and guarded by a mutex:
+// a process may drive several GPUs from several threads.
+// ---------------------------------------------------------------------------
+namespace sqz {
+namespace {
+struct AttrEntry {
+    int dev;
+    const void *kern;
+    int attr;   // cudaFuncAttribute, or -1 for an occupancy entry
+    long long key;  // occupancy: threads << 32 | smem
+    int value;
+};
+std::mutex g_cache_mu;
+std::vector<AttrEntry> g_cache;
+int g_sm_count[64];
+}  // namespace
+
+int device_sm_count() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    if (!g_sm_count[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        g_sm_count[dev] = n > 0 ? n : 148;
+    }
+    return g_sm_count[dev];
+}
+
+cudaError_t ensure_func_attr(const void *kern, cudaFuncAttribute attr, int value) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (AttrEntry &x : g_cache)
+        if (x.dev == dev && x.kern == kern && x.attr == (int)attr) {
+            if (x.value >= value) return cudaSuccess;  // a larger opt-in covers this one
+            e = cudaFuncSetAttribute(kern, attr, value);
+            if (e == cudaSuccess) x.value = value;
+            return e;
+        }
+    e = cudaFuncSetAttribute(kern, attr, value);
+    if (e == cudaSuccess) g_cache.push_back({dev, kern, (int)attr, 0, value});
+    return e;
+}
+
+int occupancy_blocks(const void *kern, int threads, size_t smem) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+    const long long key = ((long long)threads << 32) | (long long)smem;
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (const AttrEntry &x : g_cache)
+        if (x.dev == dev && x.kern == kern && x.attr == -1 && x.key == key) return x.value;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess) occ = 1;
+    occ = occ > 0 ? occ : 1;
+    g_cache.push_back({dev, kern, -1, key, occ});
+    return occ;
 }
 
 }  // namespace sqz

@@ -188,6 +188,7 @@ class Index:
     child_off: torch.Tensor = None
     L_total: int = 0          # > 0: a fixed-context shard (see shard_index)
     c2_src: torch.Tensor = None  # shard: global Level-2 id of each local row (-1 = padding)
+    c1_src: torch.Tensor = None  # shard: global Level-1 id of each local row
 
     @property
     def levels(self):
@@ -446,14 +447,15 @@ def shard_index(idx: Index, Kp: torch.Tensor, Vp: torch.Tensor, rank: int, world
                 C2=torch.empty(H, plan["c2"], d, dtype=td, device=dev), N2=up(plan["N2"]),
                 key_off=up(plan["key_off"]), perm=torch.empty(H, plan["L"], dtype=torch.int32,
                                                               device=dev),
-                c1=plan["c1"], L_total=idx.L, c2_src=up(plan["c2_src"]))
+                c1=plan["c1"], L_total=idx.L, c2_src=up(plan["c2_src"]),
+                c1_src=up(plan["c1_src"]) if idx.levels == 2 else None)
     if idx.levels == 2:
         loc.C1 = torch.empty(H, plan["c1"], d, dtype=td, device=dev)
         loc.N1 = up(plan["N1"])
         loc.child_off = up(plan["child_off"])
     Kl = torch.empty(H, plan["L"], d, dtype=td, device=dev)
     Vl = torch.empty_like(Kl)
-    c1s = up(plan["c1_src"]) if idx.levels == 2 else None
+    c1s = loc.c1_src
     c2s, ks = loc.c2_src, up(plan["key_src"])
     sf, sl = idx.struct(), loc.struct()
     _check(lib().sqz_index_shard(ctypes.byref(sf), _p(Kp), _p(Vp), _p(c1s), _p(c2s), _p(ks),

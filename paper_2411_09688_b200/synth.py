@@ -158,7 +158,15 @@ def centroid_counts(L, frac_fine=0.05, frac_coarse=0.01):
 # configurations (128K-1M keys x 32 heads), where host generation would take
 # minutes.  Not bit-identical to the numpy generator above (different RNG);
 # the parity tests use the host generator, the benches at 128K+ this one.
+# Every per-head draw uses its own generator seeded by (seed, head), so a rank
+# holding a subset of the heads draws exactly the bits the full run draws for
+# them: inputs do not change with the number of GPUs.
 # --------------------------------------------------------------------------
+def _head_gen(seed, h, device):
+    import torch
+
+    return torch.Generator(device=device).manual_seed(int(seed) * 1000003 + int(h))
+
 @dataclass
 class DeviceMixture:
     u: "torch.Tensor"      # [H,G,d] fp32 unit directions
@@ -199,11 +207,11 @@ def device_keys(mix: DeviceMixture, L, seed, dtype=BF16, heads=None):
 
     dev = mix.u.device
     heads = range(mix.u.shape[0]) if heads is None else heads
-    g = torch.Generator(device=dev).manual_seed(seed)
     d = mix.u.shape[2]
     K = torch.empty(len(heads), L, d, dtype=torch.bfloat16 if dtype == BF16 else torch.float32, device=dev)
     V = torch.empty_like(K)
     for i, h in enumerate(heads):
+        g = _head_gen(seed, h, dev)
         lab = torch.multinomial(mix.pi[h], L, replacement=True, generator=g)
         K[i] = _torch_storage(mix.rho * mix.u[h][lab] + mix.sigma * torch.randn(L, d, generator=g, device=dev),
                               dtype)
@@ -217,10 +225,10 @@ def device_decode_queries(mix: DeviceMixture, B, seed, dtype=BF16, heads=None):
 
     dev = mix.u.device
     heads = range(mix.u.shape[0]) if heads is None else heads
-    g = torch.Generator(device=dev).manual_seed(seed)
     d = mix.u.shape[2]
     Q = torch.empty(B, len(heads), 1, d, device=dev)
     for i, h in enumerate(heads):
+        g = _head_gen(seed, h, dev)
         tp = torch.multinomial(mix.pi[h], 2 * B, replacement=True, generator=g).view(B, 2)
         xi = torch.nn.functional.normalize(torch.randn(B, d, generator=g, device=dev), dim=-1)
         v = mix.u[h][tp[:, 0]] + mix.u[h][tp[:, 1]] + 0.3 * xi
@@ -234,11 +242,11 @@ def device_prefill_queries(mix: DeviceMixture, B, n_q, seed, dtype=BF16, heads=N
 
     dev = mix.u.device
     heads = range(mix.u.shape[0]) if heads is None else heads
-    g = torch.Generator(device=dev).manual_seed(seed)
     d = mix.u.shape[2]
     Q = torch.empty(B, len(heads), n_q, d, device=dev)
-    for b in range(B):
-        for i, h in enumerate(heads):
+    for i, h in enumerate(heads):
+        g = _head_gen(seed, h, dev)
+        for b in range(B):
             nt = int(torch.randint(2, 5, (1,), generator=g, device=dev))
             topics = torch.multinomial(mix.pi[h], nt, replacement=True, generator=g)
             pick = topics[torch.randint(0, nt, (n_q,), generator=g, device=dev)]
@@ -254,20 +262,22 @@ def device_user_kv(mix: DeviceMixture, B, n_u, seed, dtype=BF16, heads=None):
 
     dev = mix.u.device
     heads = range(mix.u.shape[0]) if heads is None else heads
-    g = torch.Generator(device=dev).manual_seed(seed)
     d = mix.u.shape[2]
     Ku = torch.empty(B, len(heads), n_u, d, device=dev)
-    for b in range(B):
-        for i, h in enumerate(heads):
+    Vu = torch.empty(B, len(heads), n_u, d, device=dev)
+    for i, h in enumerate(heads):
+        g = _head_gen(seed, h, dev)
+        for b in range(B):
             lab = torch.multinomial(mix.pi[h], n_u, replacement=True, generator=g)
             Ku[b, i] = mix.rho * mix.u[h][lab] + mix.sigma * torch.randn(n_u, d, generator=g, device=dev)
-    Vu = torch.randn(B, len(heads), n_u, d, generator=g, device=dev)
+            Vu[b, i] = torch.randn(n_u, d, generator=g, device=dev)
     return _torch_storage(Ku, dtype), _torch_storage(Vu, dtype)
 
 
-def device_kmeans_init(H, n, c, seed, device="cuda"):
-    """kmeans_init() on the device: [H, c] int64 distinct indices per head."""
+def device_kmeans_init(H, n, c, seed, device="cuda", heads=None):
+    """kmeans_init() on the device: [len(heads), c] int64 distinct indices per head."""
     import torch
 
-    g = torch.Generator(device=device).manual_seed(seed)
-    return torch.stack([torch.randperm(n, generator=g, device=device)[:c] for _ in range(H)])
+    heads = range(H) if heads is None else heads
+    return torch.stack([torch.randperm(n, generator=_head_gen(seed, h, device), device=device)[:c]
+                        for h in heads])

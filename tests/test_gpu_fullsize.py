@@ -208,3 +208,29 @@ def test_slim_layout_large_level2():
     torch.cuda.synchronize()
     assert int(sel.n_keys.min()) > 0
     _check(idx, sel, O, LSE, T, T1, scale, [0, 1], Q, K, V, Ku, Vu, False)
+
+
+def test_cfg5p_shape_hier_prefill():
+    """The cfg5-prefill launch shape on a smaller context: hierarchical lookup with
+    4096 query rows (32 query tiles of the tensor-core lookup, the Level-2 pass on
+    the candidate-row list), 4096 causal user keys, c1 = 1% / c2 = 5% of L, 10%
+    retention; two heads checked against the oracle (lookup on all 4096 rows, the
+    attention on 64 sampled rows incl. the first and last)."""
+    sqz = _sqz()
+    H, L, d, n_q = 4, 32768, 128, 4096
+    c1, c2 = synth.centroid_counts(L)
+    fc = synth.fixed_context(H, L, d, c2, seed=1105, G1=c1)
+    K, V = sqz.to_device(fc.K), sqz.to_device(fc.V)
+    init2 = torch.from_numpy(synth.kmeans_init(H, L, c2, seed=2105)).cuda()
+    init1 = torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=2205)).cuda()
+    Qc = sqz.to_device(synth.prefill_queries(fc.mix, 1, n_q, seed=3105))
+    Q = sqz.to_device(synth.prefill_queries(fc.mix, 1, n_q, seed=4105))
+    Ku, Vu = (sqz.to_device(a) for a in synth.user_kv(fc.mix, 1, n_q, seed=5105))
+    idx, sel, O, LSE, T, T1, scale, heads = _run(K, V, Q, Ku, Vu, c2, c1, init2, init1, True, 0.1, Qc)
+    sel_dbg = sqz.Selection.empty(idx, 1, n_q, debug=True)
+    sqz.centroid_lookup(idx, Q, scale, T, T1, sel=sel_dbg)
+    torch.cuda.synchronize()
+    assert torch.equal(sel_dbg.n_keys, sel.n_keys)
+    assert int(sel.n_keys.min()) > 0
+    rows = np.unique(np.concatenate([[0, n_q - 1], np.linspace(0, n_q - 1, 62).astype(np.int32)]))
+    _check(idx, sel_dbg, O, LSE, T, T1, scale, heads, Q, K, V, Ku, Vu, True, rows=rows.astype(np.int32))

@@ -89,3 +89,51 @@ def test_generic_data_invariants_and_determinism(levels):
         for h in range(H):
             for p in range(c1):
                 assert N1[h, p] == N2[h, co[h, p]:co[h, p + 1]].sum()
+
+
+def _repair_data(dtype, seed):
+    """Keys with a forced empty cluster: 6 tight groups on orthogonal directions,
+    init points 0 and 1 identical (so cluster 1 ties with cluster 0 everywhere and
+    starts empty), plus two outliers at clearly different distances from their
+    nearest centroid (squared distances ~0.5 and ~0.25 in the normalised space)."""
+    rng = np.random.default_rng(seed)
+    d, per = 64, 30
+    X = []
+    for g in range(6):
+        e = np.zeros(d, np.float32)
+        e[g] = 4.0
+        X.append(e + 0.01 * rng.standard_normal((per, d)).astype(np.float32))
+    X = np.concatenate(X)
+    X[1] = X[0]
+    o1 = np.zeros(d, np.float32)
+    o1[0], o1[7] = 0.75, 0.66   # 1 - cos ~ 0.25 from group 0's direction -> dist^2 ~ 0.5
+    o2 = np.zeros(d, np.float32)
+    o2[3], o2[8] = 0.88, 0.47   # dist^2 ~ 0.24 from group 3
+    X = np.concatenate([X, 4 * o1[None], 4 * o2[None]])
+    stored = synth.to_storage(X, dtype)
+    init = np.array([0, 1, per, 2 * per, 3 * per, 4 * per, 5 * per], np.int64)
+    return stored, init
+
+
+@pytest.mark.parametrize("dtype", [synth.F32, synth.BF16])
+@pytest.mark.parametrize("iters", [1, 50])
+def test_empty_cluster_repair_matches_oracle(dtype, iters):
+    """S:191 on the GPU (k_repair): the empty cluster takes the farthest point,
+    exactly as the oracle's repair does; after one Lloyd iteration the repaired
+    cluster holds only that outlier, and the converged tables are identical."""
+    stored, init = _repair_data(dtype, 7)
+    L = stored.shape[0]
+    K = np.stack([stored, stored[::-1].copy()])  # head 1: same points, reversed order
+    inits = np.stack([init, L - 1 - init])
+    V = synth.to_storage(np.random.default_rng(8).standard_normal(K.shape).astype(np.float32), dtype)
+    from types import SimpleNamespace
+    fc = SimpleNamespace(K=K, V=V)
+    g, Kp, Vp, _ = _build(fc, 7, inits, iters=iters)
+    r = oracle.build_index(K, 7, inits, max_iters=iters)
+    assert np.array_equal(_np(g.N2), r.N2)
+    assert np.array_equal(_np(g.key_off), r.key_off)
+    assert np.array_equal(_np(g.perm), r.perm)
+    assert np.array_equal(_np(g.C2), oracle.encode(r.C2, dtype))
+    if iters == 1:
+        # head 0: cluster 1 (the empty duplicate) took the farthest outlier, point L - 2
+        assert r.N2[0, 1] == 1 and r.perm[0, r.key_off[0, 1]] == L - 2

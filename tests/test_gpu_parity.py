@@ -154,6 +154,9 @@ DECODE_CASES = [
     ("bf16_many_short_rows", 16, 640, 128, 40, 0, synth.BF16, 12, 3, 0.05),
     # no user keys and a very sparse selection: rows with no key at all
     ("bf16_d64_sparse_nu0", 8, 700, 64, 50, 0, synth.BF16, 16, 0, 0.03),
+    # fp32 storage at d = 128 (k_lookup_decode<float,128>, k_attend<float,128>)
+    ("fp32_d128", 3, 2000, 128, 64, 0, synth.F32, 2, 20, 0.3),
+    ("hier_fp32_d128", 2, 3000, 128, 150, 30, synth.F32, 1, 16, 0.15),
 ]
 
 
@@ -188,6 +191,15 @@ PREFILL_CASES = [
     # more 128-key tiles than SMs: segments cut across CTAs, multi-part merges,
     # several pieces per CTA, ragged last query pair
     ("bf16_multiseg", 4, 6000, 128, 150, 0, synth.BF16, 1, 600, 600, 0.4, True),
+    # bf16 d = 64: k_prefill_lookup_tc<64, *> and the split-KV k_prefill_attend<64>
+    ("bf16_d64", 2, 2048, 64, 100, 0, synth.BF16, 1, 200, 200, 0.3, True),
+    ("bf16_d64_noncausal_B2", 2, 2048, 64, 100, 0, synth.BF16, 2, 300, 150, 0.3, False),
+    ("hier_bf16_d64", 2, 3000, 64, 150, 30, synth.BF16, 1, 130, 130, 0.15, True),
+    ("hier_bf16_d64_noncausal", 2, 3000, 64, 150, 30, synth.BF16, 1, 170, 60, 0.15, False),
+    ("bf16_d64_multiseg", 4, 6000, 64, 150, 0, synth.BF16, 1, 600, 600, 0.4, True),
+    # fp32 d = 128 prefill (k_prefill_rowlse / colsum<float,128>, exact FFMA attention)
+    ("fp32_d128", 1, 1500, 128, 40, 0, synth.F32, 1, 70, 90, 0.3, True),
+    ("hier_fp32_d128", 1, 2000, 128, 100, 20, synth.F32, 1, 65, 40, 0.2, True),
 ]
 
 

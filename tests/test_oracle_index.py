@@ -80,6 +80,26 @@ def test_empty_cluster_repair():
     assert len(np.unique(a)) == 3
 
 
+def test_empty_cluster_repair_exact_move():
+    """S:191, the exact repair move after ONE Lloyd iteration.  Points 0-4 sit on
+    centroid 0 (distance 0) and tie with the empty duplicate 1 (ties -> lowest id),
+    points 5-9 sit on centroid 2; point 10 (0.6, 0.8) goes to centroid 2 at squared
+    distance 0.4.  Cluster 1 is empty, so it takes the point FARTHEST from its own
+    centroid among clusters with > 1 member: point 10.  A "nearest point" or
+    "lowest index" repair would move point 0 instead."""
+    X = np.array([[1.0, 0.0]] * 5 + [[0.0, 1.0]] * 5 + [[0.6, 0.8]])
+    a, mu, it, _ = oracle.kmeans(X, 3, [0, 1, 5], max_iters=1)
+    assert it == 1
+    assert a.tolist() == [0] * 5 + [2] * 5 + [1]
+    # the repaired cluster's normalised-space centroid is its single member
+    np.testing.assert_allclose(mu[1], [0.6, 0.8], rtol=0, atol=1e-15)
+    # two empty clusters are repaired in increasing id, each taking the farthest
+    # remaining point (the second one: point 11 at squared distance 0.092 from (0, 1))
+    X2 = np.concatenate([X, [[0.3, 0.95393920141694566]]])
+    a2, _, _, _ = oracle.kmeans(X2, 4, [0, 1, 2, 5], max_iters=1)
+    assert a2[10] == 1 and a2[11] == 2 and a2[:5].tolist() == [0] * 5
+
+
 @pytest.mark.parametrize("levels", [1, 2])
 def test_build_index_invariants(levels):
     H, L, d = 2, 600, 16
