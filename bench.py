@@ -498,21 +498,55 @@ def run_gpu(args, cfg, rank, world, local_rank):
     LSE = torch.empty(B, Hl, n_q, dtype=torch.float32, device=dev)
     Op = torch.empty(B, Hl, n_q, d, dtype=torch.float32, device=dev) if comm else None
     Lp = torch.empty(B, Hl, n_q, dtype=torch.float32, device=dev) if comm else None
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    # L2 flush between timed steps: a 512 MB write (4x the 126 MB L2).  The write
+    # leaves the L2 full of DIRTY lines whose write-back (~126 MB of DRAM writes)
+    # would otherwise land inside the next timed step; with --flush write+read a
+    # 512 MB read follows (untimed), so the timed step starts from an L2 holding
+    # clean, unrelated lines -- the inputs are cold either way.
+    flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    rflush_buf = (torch.ones(128 << 20, dtype=torch.float32, device=dev)
+                  if args.flush == "write+read" else None)
+
+    class _Flush:
+        @staticmethod
+        def zero_():
+            flush_buf.zero_()
+            if rflush_buf is not None:
+                rflush_buf.amax()
+    flush = _Flush()
     causal = cfg["mode"] == "prefill"
 
-    def attend(q):
+    def attend_into(q, Oo, Lo, sl=None):
+        sl = sel if sl is None else sl
         if comm is None:
-            sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=causal, O=O, LSE=LSE)
+            sqz.sparse_attention(q, Kp, Vp, idx, sl, Ku, Vu, scale, causal=causal, O=Oo, LSE=Lo)
         else:  # partial over this shard, then the all-gather merge (P:361-363 across GPUs)
-            sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=causal, partial=True,
+            sqz.sparse_attention(q, Kp, Vp, idx, sl, Ku, Vu, scale, causal=causal, partial=True,
                                  out_dtype=sqz.SQZ_F32, O=Op, LSE=Lp)
-            sqz.allgather_merge(comm, Op, Lp, out_dtype=dt, O=O, LSE=LSE)
+            sqz.allgather_merge(comm, Op, Lp, out_dtype=dt, O=Oo, LSE=Lo)
+
+    def attend(q):
+        attend_into(q, O, LSE)
+
+    # decode through sqz_decode_step (one call; the fused single-level kernel)
+    # unless the fixed context is sharded (the exchange needs the two calls)
+    use_step = cfg["mode"] == "decode" and comm is None and args.decode_path == "step"
+    step_ws = None
+    if use_step:
+        nb = sqz.ctypes.c_size_t(0)
+        sqz._check(sqz.lib().sqz_decode_step_workspace(sqz.ctypes.byref(idx.struct()), B, n_u_r,
+                                                       sqz.ctypes.byref(nb)))
+        step_ws = sqz.workspace(nb.value, dev)
+
+    def step_into(q, Oo, Lo):
+        if use_step:
+            sqz.decode_step(idx, q, Kp, Vp, Ku, Vu, scale, T, T1, sel=sel, O=Oo, LSE=Lo, ws=step_ws)
+        else:
+            sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel, comm=comm)
+            attend_into(q, Oo, Lo)
 
     def step(i):
-        q = Qt[i % n_inputs]
-        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel, comm=comm)
-        attend(q)
+        step_into(Qt[i % n_inputs], O, LSE)
 
     for i in range(args.warmup):
         step(i)
@@ -591,21 +625,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
     hout = torch.empty(out_b, dtype=torch.uint8, **pin)
     d2h = out_b
 
-    def attend_into(q, Oo, Lo):
-        if comm is None:
-            sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=causal, O=Oo, LSE=Lo)
-        else:
-            sqz.sparse_attention(q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=causal, partial=True,
-                                 out_dtype=sqz.SQZ_F32, O=Op, LSE=Lp)
-            sqz.allgather_merge(comm, Op, Lp, out_dtype=dt, O=Oo, LSE=Lo)
-
     def e2e_step(i):
         din.copy_(hin[i % n_inputs], non_blocking=True)
         if kv_new is not None:
             Ku[kv_new].copy_(din[q_b:q_b + kv_b].view(Ku.dtype).view(Ku[kv_new].shape))
             Vu[kv_new].copy_(din[q_b + kv_b:].view(Vu.dtype).view(Vu[kv_new].shape))
-        sqz.centroid_lookup(idx, dQ, scale, T, T1, sel=sel, comm=comm)
-        attend_into(dQ, O_e, LSE_e)
+        step_into(dQ, O_e, LSE_e)
         hout.copy_(dout, non_blocking=True)
 
     e2e_graphs = ([capture_graph(lambda i=i: e2e_step(i)) for i in range(n_inputs)]
@@ -632,7 +657,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         q = Qt[0]
         sel_p = sqz.Selection.empty(idx, B, n_q, debug=True, device=dev, key_idx=False)
         sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel_p, comm=comm)
-        attend_into(q, O, LSE)
+        attend_into(q, O, LSE, sel_p)
         torch.cuda.synchronize()
         if rank == 0:
             rs = None
@@ -655,14 +680,26 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if cfg["mode"] == "decode":
         value = t_step * 1e3 / tokens
         e2e_v = t_e2e * 1e3 / tokens
-        ach = bytes_attn / (t_attn * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4),
-                "traffic": traffic_for(args.config, "sparse_attention"),
-                "kernel": "k_attend (persistent split-KV over equal key ranges + fused merge)",
-                "peak_kind": f"{peak_kind} copy bandwidth",
-                "bytes_per_launch": int(bytes_attn)}
         step_bytes = bytes_lookup + bytes_attn
+        if use_step and idx.levels == 1:
+            # the fused kernel IS the step: its algorithmic bytes over the
+            # graph-replayed step time (which also holds the ~6 us event/launch floor)
+            ach = step_bytes / (t_step * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(ach / hbm, 4),
+                    "traffic": traffic_for(args.config, "decode_step"),
+                    "kernel": "k_decode_step (fused lookup + threshold + sparse attention, one "
+                              "persistent cooperative launch)",
+                    "peak_kind": f"{peak_kind} copy bandwidth",
+                    "bytes_per_launch": int(step_bytes)}
+        else:
+            ach = bytes_attn / (t_attn * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                    "frac": round(ach / hbm, 4),
+                    "traffic": traffic_for(args.config, "sparse_attention"),
+                    "kernel": "k_attend (persistent split-KV over equal key ranges + fused merge)",
+                    "peak_kind": f"{peak_kind} copy bandwidth",
+                    "bytes_per_launch": int(bytes_attn)}
         whole = {"bytes_per_step": int(step_bytes),
                  "achieved_GBps": round(step_bytes / (t_step * 1e-3) / 1e9, 1),
                  "frac_hbm": round(step_bytes / (t_step * 1e-3) / 1e9 / hbm, 4)}
@@ -686,6 +723,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     else:  # stats, then per level: fold + select (+ next level's stats)
         n_look = 1 + levels * (1 + per_select) + (levels - 1)
     launches = K_ * (n_look + 1 + (1 if comm else 0))
+    if use_step and idx.levels == 1:
+        launches = K_  # one k_decode_step per step
     metric, unit, hib = metric_of(cfg)
     line = {
         "metric": metric, "value": round(value, 3), "unit": unit, "n_gpus": world,
@@ -699,12 +738,19 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    "parallelism": {"none": "1 GPU", "replicas": f"replicas x{world}",
                                    "heads": f"heads sharded x{world}",
                                    "clusters": f"fixed context sharded by cluster x{world}"}[shard],
-                   "l2": "flushed (512 MB write) between timed steps",
+                   "l2": {"write": "flushed (512 MB write) between timed steps",
+                          "write+read": "flushed between timed steps: 512 MB write, then a 512 MB "
+                                        "read of another buffer (untimed), so the step starts from "
+                                        "a cold L2 of clean lines"}[args.flush],
                    "T": T, "T1": T1, "mean_selected_keys_per_step": k_glob,
                    "retention_realized": k_glob / (B * H * L), "kmeans_iters": list(iters),
                    "index_build_s": round(t_index, 2)},
         "phases_ms": {"lookup": round(t_look, 5), "sparse_attention": round(t_attn, 5),
-                      "eager_step": round(t_eager, 5), "graph_replay": bool(args.graph)},
+                      "phases_of": "the two-call path (sqz_centroid_lookup, sqz_sparse_attention), "
+                                   "separate events",
+                      "eager_step": round(t_eager, 5), "graph_replay": bool(args.graph),
+                      "decode_path": ("sqz_decode_step" if use_step else "two calls")
+                      if cfg["mode"] == "decode" else "two calls"},
         "whole_step": whole,
         "roofline": roof,
         "e2e": {"value": round(e2e_v, 3), "unit": unit, "h2d_bytes_per_step": int(h2d),
@@ -728,6 +774,11 @@ def main():
                          "prefill measured in the same run as its `prefill` object")
     ap.add_argument("--no-prefill", action="store_true",
                     help="default run: skip the cfg3 prefill object")
+    ap.add_argument("--decode-path", default="step", choices=["step", "calls"],
+                    help="decode: one sqz_decode_step call (fused kernel for single-level "
+                         "indexes) or the two calls (lookup, then sparse attention)")
+    ap.add_argument("--flush", default="write", choices=["write", "write+read"],
+                    help="L2 flush between timed steps (see run_gpu)")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the rank-0 sampled oracle parity check after the timed region")
     ap.add_argument("--kmeans-iters", type=int, default=30)

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQZ_ABI_VERSION 3
+#define SQZ_ABI_VERSION 4
 
 enum {
     SQZ_OK = 0,
@@ -257,6 +257,31 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
                          const sqz_index *idx, const sqz_selection *sel, const void *Ku,
                          const void *Vu, int32_t n_u, const sqz_attn_params *p, void *O,
                          float *LSE, void *ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* One decode step: lookup + sparse attention in one call                    */
+/* ---------------------------------------------------------------------- */
+/* sqz_decode_step(Q [B,H,1,d]) computes exactly what sqz_centroid_lookup
+ * (n_q = 1) followed by sqz_sparse_attention computes -- the same selection
+ * rule and the same attended set (selected fixed keys + all n_u
+ * user keys) -- and writes the same outputs: `sel` (clusters,
+ * n_clusters, n_keys, key_pref required; key_idx optional) and O, LSE.
+ * For a single-level index without debug outputs it runs as ONE persistent
+ * cooperative kernel (scan, threshold, compaction and attention separated by
+ * grid barriers; the selection-independent user KV is streamed while the
+ * lookup's reductions are in flight).  Hierarchical indexes, debug outputs
+ * (dbg_*, l1_surv) and shapes outside the fused kernel's limits run the two
+ * calls internally.  ap->causal is ignored (decode sees all n_u user keys, R8).
+ * The selection may differ from the two-call path only for clusters inside
+ * the 1e-5 near-threshold band (Eq. 1's denominator is reduced in another
+ * order).  ws: sqz_decode_step_workspace bytes, zeroed once
+ * (sqz_workspace_init); empty rows with ap->partial == 0 are reported by
+ * sqz_attention_status(ws) as for sqz_sparse_attention. */
+int sqz_decode_step_workspace(const sqz_index *idx, int32_t B, int32_t n_u, size_t *ws_bytes);
+int sqz_decode_step(const sqz_index *idx, const void *Q, int32_t B, const void *Kp, const void *Vp,
+                    const void *Ku, const void *Vu, int32_t n_u, const sqz_lookup_params *lp,
+                    const sqz_attn_params *ap, const sqz_selection *sel, void *O, float *LSE,
+                    void *ws, size_t ws_bytes, void *stream);
 
 /* Synchronises the stream and returns SQZ_ERR_EMPTY if the last non-partial
  * sqz_sparse_attention on this workspace produced a row with no attended key

@@ -462,6 +462,75 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
     return SQZ_OK;
 }
 
+// ------------------------------------------------------------------ decode step
+// workspace regions: [attention | fused step | lookup].  The attention region
+// comes first so that its status word sits where sqz_attention_status(ws)
+// reads it; the fused kernel reports empty rows through the same word.
+static size_t step_region_bytes(const sqz_index *idx, int B, int n_u) {
+    return (decode_step_ws_bytes(B, idx->H, idx->c2, n_u, idx->d) + 255) & ~(size_t)255;
+}
+
+int sqz_decode_step_workspace(const sqz_index *idx, int32_t B, int32_t n_u, size_t *ws_bytes) {
+    int rc = check_index(idx, false);
+    if (rc) return rc;
+    if (B < 1 || n_u < 0) return fail(SQZ_ERR_INVALID_ARG, "B = %d must be >= 1 and n_u = %d >= 0", B, n_u);
+    if (!ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes is NULL");
+    *ws_bytes = 256 + ((attn_carve(idx, B, 1, n_u, nullptr).bytes + 511) & ~(size_t)255) +
+                step_region_bytes(idx, B, n_u) + ((lookup_carve(idx, B, 1, nullptr).bytes + 511) & ~(size_t)255);
+    return SQZ_OK;
+}
+
+int sqz_decode_step(const sqz_index *idx, const void *Q, int32_t B, const void *Kp, const void *Vp,
+                    const void *Ku, const void *Vu, int32_t n_u, const sqz_lookup_params *lp,
+                    const sqz_attn_params *ap, const sqz_selection *sel, void *O, float *LSE,
+                    void *ws, size_t ws_bytes, void *stream) {
+    int rc = lookup_check(idx, Q, B, 1, lp, sel, ws);
+    if (rc) return rc;
+    if (lp->comm) return fail(SQZ_ERR_INVALID_ARG, "sqz_decode_step: lp->comm must be NULL (use the two calls)");
+    if (!ap) return fail(SQZ_ERR_INVALID_ARG, "attention params is NULL");
+    if (!Kp || !Vp || !aligned16(Kp) || !aligned16(Vp))
+        return fail(SQZ_ERR_INVALID_ARG, "Kp, Vp must be non-NULL and 16-byte aligned");
+    if (n_u < 0 || (n_u > 0 && (!Ku || !Vu || !aligned16(Ku) || !aligned16(Vu))))
+        return fail(SQZ_ERR_INVALID_ARG, "n_u = %d: Ku, Vu must be non-NULL and 16-byte aligned", n_u);
+    if (ap->out_dtype != SQZ_F32 && ap->out_dtype != SQZ_BF16)
+        return fail(SQZ_ERR_INVALID_ARG, "out_dtype = %d is not a sqz_dtype", ap->out_dtype);
+    if (!O || !LSE) return fail(SQZ_ERR_INVALID_ARG, "O and LSE must be non-NULL");
+    size_t need = 0;
+    sqz_decode_step_workspace(idx, B, n_u, &need);
+    if (ws_bytes < need) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes = %zu < required %zu", ws_bytes, need);
+    // regions: attention (its status word first, as sqz_attention_status reads
+    // it), fused step, lookup
+    char *base = align_ws(ws);
+    const size_t attn_b = (attn_carve(idx, B, 1, n_u, nullptr).bytes + 511) & ~(size_t)255;
+    char *step_ws = base + attn_b;
+    char *look_ws = step_ws + step_region_bytes(idx, B, n_u);
+    const bool debug = sel->dbg_S || sel->dbg_S1 || sel->dbg_lse || sel->l1_surv;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (idx->levels == 1 && !debug && decode_step_rows_ok(B, idx->H, idx->c2, idx->L) &&
+        idx->L_total == 0) {
+        StepLaunch l;
+        std::memset(&l, 0, sizeof(l));
+        l.Q = Q; l.C = idx->C2; l.Kp = Kp; l.Vp = Vp; l.Ku = Ku; l.Vu = Vu;
+        l.N = idx->N2; l.koff = idx->key_off;
+        l.B = B; l.H = idx->H; l.c = idx->c2; l.n_u = n_u; l.d = idx->d; l.dtype = idx->dtype;
+        l.out_dtype = ap->out_dtype; l.partial = ap->partial ? 1 : 0;
+        l.L = idx->L; l.scale = lp->scale; l.T = lp->T;
+        l.ws = step_ws;
+        l.clusters = sel->clusters; l.key_pref = sel->key_pref; l.n_clusters = sel->n_clusters;
+        l.n_keys = sel->n_keys; l.key_idx = sel->key_idx;
+        l.O = O; l.LSE = LSE;
+        l.status = reinterpret_cast<int32_t *>(base);
+        cudaError_t e = launch_decode_step(l, st);
+        if (e != cudaSuccess) return cuda_fail(e, "decode step launch");
+        return SQZ_OK;
+    }
+    // the two calls, on sub-workspaces of this one
+    const size_t look_b = (lookup_carve(idx, B, 1, nullptr).bytes + 511) & ~(size_t)255;
+    rc = sqz_centroid_lookup(idx, Q, B, 1, lp, sel, look_ws, look_b, stream);
+    if (rc) return rc;
+    return sqz_sparse_attention(Q, B, 1, Kp, Vp, idx, sel, Ku, Vu, n_u, ap, O, LSE, base, attn_b, stream);
+}
+
 int sqz_attention_status(void *ws, size_t ws_bytes, void *stream) {
     if (!ws || ws_bytes < 512) return fail(SQZ_ERR_INVALID_ARG, "ws too small");
     int32_t *status = reinterpret_cast<int32_t *>(align_ws(ws));

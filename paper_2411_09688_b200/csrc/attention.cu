@@ -25,6 +25,7 @@
 // stream serialization; griddepcontrol.wait orders it after the lookup kernel.
 #include "common.cuh"
 #include "internal.h"
+#include "stream.cuh"
 #include "tma.cuh"
 
 namespace sqz {
@@ -36,14 +37,6 @@ constexpr int NCT = NCW * 32;           // threads per CTA
 #ifndef SQZ_ATT_ACQREL  // acquire-release ticket atomic instead of fence + atomic (tuning knob)
 #define SQZ_ATT_ACQREL 1  // cfg2 -0.4 us, cfg4 -0.1 us (same box)
 #endif
-#ifndef SQZ_ATT_L2PF  // L2::256B prefetch hint on the K/V row loads (tuning knob)
-#define SQZ_ATT_L2PF 0
-#endif
-#ifndef SQZ_ATT_KR_BF16
-#define SQZ_ATT_KR_BF16 16
-#endif
-// keys per warp round (bf16 rows: tuning knob; fp32 rows take twice the registers)
-template <typename T> constexpr int keys_per_round() { return sizeof(T) == 2 ? SQZ_ATT_KR_BF16 : 16; }
 constexpr int MAX_PERSIST_CTAS = 1184;  // 148 SMs x 8
 constexpr int MIN_KEYS = 256;           // minimum keys per persistent CTA
 // Partition cost of a decode segment: its keys plus SEG_KW keys' worth for the
@@ -61,61 +54,6 @@ int attention_max_parts(int64_t L, int n_u, int n_q) {
     const int kch = attention_kch(n_q);
     const int grid_parts = (int)((L + n_u + kch - 1) / kch);
     return n_q == 1 ? std::max(grid_parts, MAX_PERSIST_CTAS) : grid_parts;
-}
-
-template <typename T> struct Raw { uint4 v[sizeof(T) == 2 ? 1 : 2]; };
-__device__ __forceinline__ uint4 ld_nc_v4(const void *p) {
-    uint4 u;
-#if SQZ_ATT_L2PF
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
-                 : "l"(p));
-#else
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
-                 : "l"(p));
-#endif
-    return u;
-}
-template <typename T> __device__ __forceinline__ void ld_raw(Raw<T> &r, const T *p) {
-#pragma unroll
-    for (int i = 0; i < (int)(sizeof(r.v) / sizeof(uint4)); ++i)
-        r.v[i] = ld_nc_v4(reinterpret_cast<const uint4 *>(p) + i);
-}
-__device__ __forceinline__ void cvt(const Raw<__nv_bfloat16> &r, float (&f)[8]) {
-    const uint32_t w[4] = {r.v[0].x, r.v[0].y, r.v[0].z, r.v[0].w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        f[2 * i] = __uint_as_float(w[i] << 16);
-        f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-    }
-}
-__device__ __forceinline__ void cvt(const Raw<float> &r, float (&f)[8]) {
-    f[0] = __uint_as_float(r.v[0].x); f[1] = __uint_as_float(r.v[0].y);
-    f[2] = __uint_as_float(r.v[0].z); f[3] = __uint_as_float(r.v[0].w);
-    f[4] = __uint_as_float(r.v[1].x); f[5] = __uint_as_float(r.v[1].y);
-    f[6] = __uint_as_float(r.v[1].z); f[7] = __uint_as_float(r.v[1].w);
-}
-
-// NV values per lane, reduced over aligned groups of G lanes; lane ends with
-// the group sum of value index (sub >> (log2 G - log2 NV)) & (NV - 1).
-template <int NV, int G>
-__device__ __forceinline__ float group_transpose_reduce(float (&v)[NV], int lane) {
-    int stride = G / 2;
-#pragma unroll
-    for (int w = NV; w > 1; w >>= 1) {
-        const bool hi = lane & stride;
-#pragma unroll
-        for (int k = 0; k < w / 2; ++k) {
-            float keep = hi ? v[k + w / 2] : v[k];
-            float send = hi ? v[k] : v[k + w / 2];
-            v[k] = keep + __shfl_xor_sync(FULL, send, stride);
-        }
-        stride >>= 1;
-    }
-#pragma unroll
-    for (; stride >= 1; stride >>= 1) v[0] += __shfl_xor_sync(FULL, v[0], stride);
-    return v[0];
 }
 
 // A row's key stream: nkf selected fixed keys, then nu visible user keys.

@@ -103,6 +103,24 @@ int attention_max_parts(int64_t L, int n_u, int n_q);
 cudaError_t launch_merge(int P, const float *O_parts, const float *LSE_parts, int64_t rows, int d,
                          void *O, float *LSE, int out_dtype, cudaStream_t st);
 
+// decode_step.cu: the fused single-level decode step (lookup + attention in one
+// persistent cooperative launch)
+struct StepLaunch {
+    const void *Q, *C, *Kp, *Vp, *Ku, *Vu;
+    const int32_t *N, *koff;
+    int32_t B, H, c, n_u, d, dtype, out_dtype, partial;
+    int64_t L;
+    float scale, T;
+    void *ws;  // carved by the launcher (decode_step_ws_bytes)
+    int32_t *clusters, *key_pref, *n_clusters, *n_keys, *key_idx;
+    void *O;
+    float *LSE;
+    int32_t *status;  // set to 1 when a final (non-partial) row attended no key
+};
+size_t decode_step_ws_bytes(int B, int H, int c, int n_u, int d);
+int decode_step_rows_ok(int B, int H, int c, long long L);
+cudaError_t launch_decode_step(const StepLaunch &l, cudaStream_t st);
+
 // kmeans.cu
 struct KmeansWs;
 size_t kmeans_workspace_bytes(const sqz_index &idx);

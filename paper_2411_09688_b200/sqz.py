@@ -25,7 +25,7 @@ SO = os.path.join(HERE, "libsqz.so")
 SQZ_F32, SQZ_BF16 = 0, 1
 SQZ_OK, SQZ_ERR_INVALID_ARG, SQZ_ERR_FORMAT, SQZ_ERR_INVARIANT = 0, 2, 3, 4
 SQZ_ERR_CUDA, SQZ_ERR_NCCL, SQZ_ERR_EMPTY, SQZ_ERR_UNSUPPORTED = 5, 6, 7, 8
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 EXPORTS = [
     "sqz_cluster_keys_workspace", "sqz_cluster_keys", "sqz_index_validate_workspace",
@@ -34,7 +34,8 @@ EXPORTS = [
     "sqz_merge_partials", "sqz_workspace_init", "sqz_last_error", "sqz_abi_version",
     "sqz_device_check", "sqz_centroid_lookup_stage", "sqz_shard_plan_compute", "sqz_index_shard",
     "sqz_comm_unique_id", "sqz_comm_init", "sqz_comm_destroy", "sqz_lookup_workspace_comm",
-    "sqz_comm_merge_workspace", "sqz_comm_allgather_merge",
+    "sqz_comm_merge_workspace", "sqz_comm_allgather_merge", "sqz_decode_step_workspace",
+    "sqz_decode_step",
 ]
 
 
@@ -122,6 +123,11 @@ def lib():
         L.sqz_lookup_workspace_comm.argtypes = [ip, i32, i32, i32, szp]
         L.sqz_comm_merge_workspace.argtypes = [i32, i64, i32, szp]
         L.sqz_comm_allgather_merge.argtypes = [vp, vp, vp, i64, i32, vp, vp, i32, vp, sz, vp]
+        L.sqz_decode_step_workspace.argtypes = [ip, i32, i32, szp]
+        L.sqz_decode_step.argtypes = [ip, vp, i32, vp, vp, vp, vp, i32,
+                                      ctypes.POINTER(sqz_lookup_params),
+                                      ctypes.POINTER(sqz_attn_params), ctypes.POINTER(sqz_selection),
+                                      vp, vp, vp, sz, vp]
         if L.sqz_abi_version() != ABI_VERSION:
             raise RuntimeError(f"{SO} has ABI {L.sqz_abi_version()}, binding expects {ABI_VERSION}: "
                                "rebuild with __graft_entry__.build()")
@@ -367,6 +373,37 @@ def sparse_attention(Q, Kp, Vp, idx: Index, sel: Selection, Ku=None, Vu=None, sc
                                       ctypes.byref(ss), _p(Ku), _p(Vu), n_u, ctypes.byref(p),
                                       _p(O), _p(LSE), _p(ws), ws.numel(), _stream()))
     return O, LSE
+
+
+def decode_step(idx: Index, Q, Kp, Vp, Ku, Vu, scale, T, T1=0.0, sel: Selection = None,
+                partial=False, out_dtype=None, O=None, LSE=None, ws=None, debug=False):
+    """sqz_decode_step: the centroid lookup and the sparse attention of one decode
+    step (Q [B,H,1,d]) in one call.  Returns (Selection, O [B,H,1,d], LSE [B,H,1])."""
+    B, H, n_q, d = Q.shape
+    if n_q != 1:
+        raise ValueError("decode_step takes one query row per (b, h)")
+    n_u = 0 if Ku is None else Ku.shape[2]
+    if sel is None:
+        sel = Selection.empty(idx, B, 1, debug, Q.device)
+    if out_dtype is None:
+        out_dtype = idx.dtype
+    if O is None:
+        O = torch.empty(B, H, 1, d, dtype=torch_dtype(out_dtype), device=Q.device)
+    if LSE is None:
+        LSE = torch.empty(B, H, 1, dtype=torch.float32, device=Q.device)
+    s = idx.struct()
+    if ws is None:
+        nb = ctypes.c_size_t(0)
+        _check(lib().sqz_decode_step_workspace(ctypes.byref(s), B, n_u, ctypes.byref(nb)))
+        ws = _WS.get(("step", Q.device, idx.H, idx.L, idx.c1, idx.c2, B, n_u), nb.value, Q.device)
+        _WS.last_attn = ws
+    lp = sqz_lookup_params(scale, T, T1, None)
+    ap = sqz_attn_params(scale, 0, int(partial), out_dtype)
+    ss = sel.struct()
+    _check(lib().sqz_decode_step(ctypes.byref(s), _p(Q), B, _p(Kp), _p(Vp), _p(Ku), _p(Vu), n_u,
+                                 ctypes.byref(lp), ctypes.byref(ap), ctypes.byref(ss), _p(O), _p(LSE),
+                                 _p(ws), ws.numel(), _stream()))
+    return sel, O, LSE
 
 
 def attention_status(ws: torch.Tensor = None):

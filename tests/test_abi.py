@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(lib):
     for name in decl:
         assert hasattr(lib, name), name
     assert sorted(sqz.EXPORTS) == decl
-    assert lib.sqz_abi_version() == sqz.ABI_VERSION == 3
+    assert lib.sqz_abi_version() == sqz.ABI_VERSION == 4
 
 
 def test_struct_layout_matches_header(tmp_path):

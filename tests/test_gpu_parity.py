@@ -180,6 +180,73 @@ def test_decode_lookup_and_attention(case):
     _check_runs(t, sel, O, LSE, scale, T, T1, False, True)
 
 
+@pytest.mark.parametrize("case", DECODE_CASES, ids=lambda c: c[0])
+def test_decode_step(case):
+    """sqz_decode_step (one call: the fused single-level kernel, or the two calls for
+    hierarchical indexes) against the oracle: the selection under the band rule,
+    key_pref / key_idx consistent with it, and the attention on its key set."""
+    sqz = _sqz()
+    _, H, L, d, c2, c1, dt, B, n_u, ret = case
+    P = oracle_problem(H, L, d, c2, c1, dt, seed=zlib.crc32(case[0].encode()) % 1000, B=B, n_u=n_u)
+    scale = 1.0 / np.sqrt(d)
+    T, T1 = _calibrate(P, scale, ret)
+    t = _device(P)
+    idx = P["idx"]
+    for rep in range(2):  # the second call reuses the (self-cleaning) workspace
+        sel = sqz.Selection.empty(t["idx"], B, 1)
+        sel_l1 = sqz.Selection.empty(t["idx"], B, 1, debug=True) if idx.levels == 2 else None
+        sel, O, LSE = sqz.decode_step(t["idx"], t["Q"], t["Kp"], t["Vp"], t["Ku"], t["Vu"], scale, T, T1,
+                                      sel=sel, partial=True)
+        torch.cuda.synchronize()
+        Q64 = oracle.to_f64(P["Q"])
+        forced = None
+        if idx.levels == 2:  # Level-1 survivors of the GPU for the conditional comparison
+            sqz.centroid_lookup(t["idx"], t["Q"], scale, T, T1, sel=sel_l1)
+            torch.cuda.synchronize()
+            forced = sel_l1.l1_surv.cpu().numpy().astype(bool)
+        ref = oracle.lookup(Q64, idx, scale, T, T1, forced_l1=forced)
+        g = gpu_sets(sel, B, H, idx.c2)
+        assert_selection_parity(g, ref["sel2"], ref["Sbar2"], T)
+        nk = sel.n_keys.cpu().numpy()
+        ki = sel.key_idx.cpu().numpy()
+        kp = sel.key_pref.cpu().numpy()
+        for b in range(B):
+            for h in range(H):
+                cl = np.nonzero(g[b, h])[0]
+                assert nk[b, h] == idx.N2[h][cl].sum()
+                assert int(sel.n_clusters[b, h]) == len(cl)
+                exp = np.concatenate([np.arange(idx.key_off[h, i], idx.key_off[h, i + 1]) for i in cl]
+                                     + [np.zeros(0, np.int64)])
+                assert np.array_equal(ki[b, h, :nk[b, h]], exp)
+                pref = np.concatenate([[0], np.cumsum(idx.N2[h][cl])[:-1]]) if len(cl) else np.zeros(0)
+                assert np.array_equal(kp[b, h, :len(cl)], pref)
+        fp32 = dt == synth.F32
+        _check_attention(P, sel, O, LSE, scale, False, B, 1e-4 if fp32 else 2e-2,
+                         None if fp32 else 5e-3)
+
+
+def test_decode_step_empty_rows_and_status():
+    """A threshold no cluster passes: rows attend only their user keys; with no user
+    keys either they are empty (identity partial, or SQZ_ERR_EMPTY when final)."""
+    sqz = _sqz()
+    P = oracle_problem(3, 900, 128, 30, 0, synth.BF16, seed=12, B=2, n_u=5)
+    t = _device(P)
+    scale = 1 / np.sqrt(128)
+    sel, O, LSE = sqz.decode_step(t["idx"], t["Q"], t["Kp"], t["Vp"], t["Ku"], t["Vu"], scale, 1.0)
+    torch.cuda.synchronize()
+    assert int(sel.n_keys.sum()) == 0
+    _check_attention(P, sel, O, LSE, scale, False, 2, 2e-2, 5e-3)
+    sqz.attention_status()
+    sel, O, LSE = sqz.decode_step(t["idx"], t["Q"], t["Kp"], t["Vp"], None, None, scale, 1.0, partial=True)
+    torch.cuda.synchronize()
+    assert torch.isneginf(LSE).all() and (O == 0).all()
+    sqz.attention_status()
+    sqz.decode_step(t["idx"], t["Q"], t["Kp"], t["Vp"], None, None, scale, 1.0, partial=False)
+    with pytest.raises(sqz.SqzError) as e:
+        sqz.attention_status()
+    assert e.value.code == sqz.SQZ_ERR_EMPTY
+
+
 PREFILL_CASES = [
     # id, H, L, d, c2, c1, dtype, B, n_q, n_u, retention, causal
     ("bf16_single", 2, 2048, 128, 100, 0, synth.BF16, 1, 200, 200, 0.3, True),
