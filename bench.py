@@ -774,9 +774,11 @@ def main():
                          "prefill measured in the same run as its `prefill` object")
     ap.add_argument("--no-prefill", action="store_true",
                     help="default run: skip the cfg3 prefill object")
-    ap.add_argument("--decode-path", default="step", choices=["step", "calls"],
-                    help="decode: one sqz_decode_step call (fused kernel for single-level "
-                         "indexes) or the two calls (lookup, then sparse attention)")
+    ap.add_argument("--decode-path", default="calls", choices=["step", "calls"],
+                    help="decode: the two calls (lookup, then sparse attention, chained by "
+                         "programmatic dependent launch; default: measured fastest) or one "
+                         "sqz_decode_step call (the fused single-level kernel: 65-70 us vs 52.7 us "
+                         "on cfg2, DESIGN.md section 7)")
     ap.add_argument("--flush", default="write", choices=["write", "write+read"],
                     help="L2 flush between timed steps (see run_gpu)")
     ap.add_argument("--no-parity", action="store_true",

@@ -30,6 +30,7 @@
 // The user KV does not depend on the selection: it is cut into 64-key chunks
 // that CTAs take dynamically (atomic counter) while they wait at a barrier,
 // and after their fixed range; its partials join the row's merge.
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -38,6 +39,8 @@
 #include "stream.cuh"
 
 namespace sqz {
+
+SQZ_TRACE_DECL(g_trace_step)
 
 namespace dstep {
 constexpr int NW = 4;          // warps per CTA
@@ -56,6 +59,7 @@ struct StepArgs {
     float scale, logT;
     int32_t G, S, rpp, rmax;  // grid, scan parts per (b,h), rows per part, rows per CTA
     int32_t nuc, maxp;        // user chunks per row, partial slots per row
+    int32_t umode;            // bit b: take user chunks while waiting at barrier b+1
     // workspace
     float2 *md;               // [BH * S] part statistics (m, D)
     int2 *cntk;               // [BH * S] part (selected clusters, selected keys)
@@ -447,6 +451,7 @@ __global__ void __launch_bounds__(dstep::NT) k_decode_step(StepArgs a) {
     auto part_bh = [&](int m) { return multi ? j + m * G : j / S; };
     auto part_k = [&](int m) { return multi ? 0 : j % S; };
 
+    SQZ_TRACE_AT(g_trace_step, 0);
     // ------------------------------------------------------------ A: scan
     int sbase = 0;
     for (int m = 0; m < nparts; ++m) {
@@ -533,16 +538,18 @@ __global__ void __launch_bounds__(dstep::NT) k_decode_step(StepArgs a) {
             if (tid == 0) s_def[s_ndef++] = row;
         }
     };
-    auto grid_barrier = [&](int target) {
+    auto grid_barrier = [&](int target, bool take) {
         __syncthreads();
         if (tid == 0) red_release_add(a.ctl, 1);
-        user_chunks_until(target);
+        if (take) user_chunks_until(target);
         if (tid == 0)
             while (ld_acquire(a.ctl) < target) {
             }
         __syncthreads();
     };
-    grid_barrier(G);
+    SQZ_TRACE_AT(g_trace_step, 1);
+    grid_barrier(G, a.umode & 1);
+    SQZ_TRACE_AT(g_trace_step, 2);
 
     // ------------------------------------------- B: fold, threshold, compact
     sbase = 0;
@@ -585,7 +592,9 @@ __global__ void __launch_bounds__(dstep::NT) k_decode_step(StepArgs a) {
         if (tid == 0) a.cntk[bh * S + k] = make_int2(run, runk);
         sbase += n;
     }
-    grid_barrier(2 * G);
+    SQZ_TRACE_AT(g_trace_step, 3);
+    grid_barrier(2 * G, a.umode & 2);
+    SQZ_TRACE_AT(g_trace_step, 4);
 
     // ---------------------------------- C: offsets, outputs, partition
     for (int s = tid; s < nslot; s += NT) {
@@ -602,31 +611,6 @@ __global__ void __launch_bounds__(dstep::NT) k_decode_step(StepArgs a) {
     }
     __syncthreads();
     block_exscan(s_pref, BH);
-    // the ABI selection outputs of this CTA's parts
-    for (int m = 0; m < nparts; ++m) {
-        const int bh = part_bh(m), k = part_k(m), sl = bh * S + k;
-        const int i0 = min(c, k * a.rpp);
-        const int cnt = FC[sl + 1] - FC[sl], cb = FC[sl] - FC[bh * S], kb = FK[sl] - FK[bh * S];
-        const int32_t *lcl = a.loc_cl + (size_t)bh * c + i0, *lpr = a.loc_pref + (size_t)bh * c + i0;
-        for (int e = tid; e < cnt; e += NT) {
-            const int cl = ldcg(lcl + e), kp = kb + ldcg(lpr + e);
-            a.clusters[(size_t)bh * c + cb + e] = cl;
-            a.key_pref[(size_t)bh * c + cb + e] = kp;
-        }
-        if (k == 0 && tid == 0) {
-            a.n_clusters[bh] = FC[(bh + 1) * S] - FC[bh * S];
-            a.n_keys[bh] = FK[(bh + 1) * S] - FK[bh * S];
-        }
-        if (a.key_idx) {  // the expanded key-index tensor (P:354), one warp per run
-            const int32_t *ko = a.koff + (size_t)(bh % a.H) * (c + 1);
-            int32_t *ki = a.key_idx + (size_t)bh * a.L;
-            for (int e = warp; e < cnt; e += NW) {
-                const int cl = ldcg(lcl + e), kp = kb + ldcg(lpr + e);
-                const int st = __ldg(ko + cl), len = __ldg(ko + cl + 1) - st;
-                for (int t = lane; t < len; t += 32) ki[kp + t] = st + t;
-            }
-        }
-    }
     // equal split of the cost space (row r: SEG_KW setup units, then one per key)
     const long long K = s_pref[BH];
     const int Gp = (int)min((long long)G, max(1LL, (K + MIN_KEYS - 1) / MIN_KEYS));
@@ -636,15 +620,8 @@ __global__ void __launch_bounds__(dstep::NT) k_decode_step(StepArgs a) {
         if (re == cs) return 1;
         return cta_of(re - 1) - cta_of(cs + SEG_KW) + 1;
     };
-    // the deferred tickets of the user chunks taken at the barriers
-    for (int i = 0; i < s_ndef; ++i) finish_part<D>(a, s_def[i], a.nuc + fixed_parts(s_def[i]));
-    // rows without a selected key: an identity partial stands in for the fixed part
-    for (int r = j; r < BH; r += G)
-        if (s_pref[r + 1] == s_pref[r]) {
-            identity_part<D>(a, r, a.nuc);
-            finish_part<D>(a, r, a.nuc + 1);
-        }
-
+    SQZ_TRACE_AT(g_trace_step, 5);
+    SQZ_TRACE_VAL(g_trace_step, 7, s_ndef);
     // ------------------------------------------------------ D: attention
     if (j < Gp && K > 0) {
         const long long ks = (long long)j * K / Gp, ke = (long long)(j + 1) * K / Gp;
@@ -676,6 +653,7 @@ __global__ void __launch_bounds__(dstep::NT) k_decode_step(StepArgs a) {
             finish_part<D>(a, r, a.nuc + fixed_parts(r));
         }
     }
+    SQZ_TRACE_AT(g_trace_step, 6);
     // user chunks nobody took while waiting
     {
         while (true) {
@@ -689,6 +667,52 @@ __global__ void __launch_bounds__(dstep::NT) k_decode_step(StepArgs a) {
             stream_part<T, D, false>(a, row, part * UCH, min(a.n_u, (part + 1) * UCH), dummy, part);
             finish_part<D>(a, row, a.nuc + fixed_parts(row));
         }
+    }
+    // the deferred tickets of the user chunks taken at the barriers
+    for (int i = 0; i < s_ndef; ++i) finish_part<D>(a, s_def[i], a.nuc + fixed_parts(s_def[i]));
+    // rows without a selected key: an identity partial stands in for the fixed part
+    for (int r = j; r < BH; r += G)
+        if (s_pref[r + 1] == s_pref[r]) {
+            identity_part<D>(a, r, a.nuc);
+            finish_part<D>(a, r, a.nuc + 1);
+        }
+
+    // ------------------------------------------------ E: selection outputs
+    // (after the streams: nothing on the step's critical path reads them).  The
+    // part's entries are fetched in one parallel pass into shared memory (the
+    // scan's logit / N arrays are free now), then written: clusters / key_pref
+    // coalesced, the key-index tensor one warp per run.
+    __syncthreads();
+    sbase = 0;
+    for (int m = 0; m < nparts; ++m) {
+        const int bh = part_bh(m), k = part_k(m), sl = bh * S + k;
+        const int i0 = min(c, k * a.rpp), n = min(c, i0 + a.rpp) - i0;
+        const int cnt = FC[sl + 1] - FC[sl], cb = FC[sl] - FC[bh * S], kb = FK[sl] - FK[bh * S];
+        const int32_t *lcl = a.loc_cl + (size_t)bh * c + i0, *lpr = a.loc_pref + (size_t)bh * c + i0;
+        const int32_t *ko = a.koff + (size_t)(bh % a.H) * (c + 1);
+        int *e_st = reinterpret_cast<int *>(s_log) + sbase, *e_kp = s_N + sbase;
+        for (int e = tid; e < cnt; e += NT) {
+            const int cl = ldcg(lcl + e), kp = kb + ldcg(lpr + e);
+            a.clusters[(size_t)bh * c + cb + e] = cl;
+            a.key_pref[(size_t)bh * c + cb + e] = kp;
+            e_st[e] = __ldg(ko + cl);
+            e_kp[e] = kp;
+        }
+        if (k == 0 && tid == 0) {
+            a.n_clusters[bh] = FC[(bh + 1) * S] - FC[bh * S];
+            a.n_keys[bh] = FK[(bh + 1) * S] - FK[bh * S];
+        }
+        __syncthreads();
+        if (a.key_idx) {  // the expanded key-index tensor (P:354), one warp per run
+            int32_t *ki = a.key_idx + (size_t)bh * a.L;
+            const int kend = FK[sl + 1] - FK[bh * S];
+            for (int e = warp; e < cnt; e += NW) {
+                const int st = e_st[e], kp = e_kp[e];
+                const int len = (e + 1 < cnt ? e_kp[e + 1] : kend) - kp;
+                for (int t = lane; t < len; t += 32) ki[kp + t] = st + t;
+            }
+        }
+        sbase += n;
     }
     // the last CTA out resets the barrier and chunk counters (self-cleaning workspace)
     __syncthreads();
@@ -771,6 +795,11 @@ cudaError_t launch_decode_step(const StepLaunch &l, cudaStream_t st) {
     a.all = !(l.T > 0.f);
     a.logT = a.all ? 0.f : logf(l.T);
     a.nuc = (l.n_u + dstep::UCH - 1) / dstep::UCH;
+    static const int umode = [] {
+        const char *e = getenv("SQZ_STEP_UMODE");  // tuning experiments only
+        return e ? atoi(e) : 3;
+    }();
+    a.umode = umode;
     auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
     char *p = reinterpret_cast<char *>(((uintptr_t)l.ws + 255) & ~(uintptr_t)255);
     const size_t BH = (size_t)l.B * l.H;
@@ -795,5 +824,6 @@ cudaError_t launch_decode_step(const StepLaunch &l, cudaStream_t st) {
     return launch_step_t<float, 64>(a, st);
 }
 
-
 }  // namespace sqz
+
+SQZ_TRACE_EXPORT(sqz::g_trace_step, sqz_trace_step)
