@@ -71,6 +71,9 @@ def lib():
         L.sqzref_attention.argtypes = [c_int, c_int, c_int, c_int, c_i64, c_int, dp, dp, dp, u8p,
                                        dp, dp, c_int, c_int, ip, c_d, dp, dp]
         L.sqzref_merge.argtypes = [c_int, c_i64, c_int, dp, dp, dp, dp]
+        L.sqzref_diagnostics.restype = c_int
+        L.sqzref_diagnostics.argtypes = [c_int, c_int, c_int, c_i64, dp, dp, u8p, c_d, c_i64, c_d,
+                                         dp, dp, dp, dp, i64p, i64p, dp]
         _lib = L
     return _lib
 
@@ -370,3 +373,41 @@ def budget(k_selected, L, scanned_per_level=()):
     loaded, counting centroid rows (key-only) at half weight:
     k/L + sum_l scanned_l / (2L)."""
     return k_selected / L + sum(scanned_per_level) / (2.0 * L)
+
+
+# --------------------------------------------------------------------------
+# selection diagnostics: App. A skewness, App. D ideal lookup (NEXT-4)
+# --------------------------------------------------------------------------
+
+def top_count(top_frac, L):
+    """n_top = ceil(top_frac * L), at least 1 ("top 1%" of P:710)."""
+    return max(1, int(np.ceil(float(top_frac) * L)))
+
+
+def diagnostics(Q, K, sel, scale, top_frac=0.01, T=0.0):
+    """Per (b,h) of one decode query row: App. A top-`top_frac` cumulative
+    attention score, and the App. D ideal lookup (keys with a_j > T; and the
+    k largest a_j at the centroid selection's budget k) vs the selection.
+    Q[B,H,d] or [B,H,1,d]; K[H,L,d] original order; sel[B,H,L] bool (original
+    order).  Returns a dict of [B,H] arrays (see sqzref_diagnostics)."""
+    Q = _f64(Q)
+    if Q.ndim == 4:
+        Q = np.ascontiguousarray(Q[:, :, 0])
+    B, H, d = Q.shape
+    K = _f64(K)
+    L = K.shape[1]
+    sm = np.ascontiguousarray(sel, dtype=np.uint8)
+    out = {k: np.zeros((B, H)) for k in ("skew", "mass_sel", "mass_ideal", "recall", "mass_T")}
+    ks = np.zeros((B, H), np.int64)
+    nT = np.zeros((B, H), np.int64)
+    rc = lib().sqzref_diagnostics(
+        B, H, d, L, _p(Q, ctypes.c_double), _p(K, ctypes.c_double), _p(sm, ctypes.c_uint8),
+        float(scale), top_count(top_frac, L), float(T), _p(out["skew"], ctypes.c_double),
+        _p(out["mass_sel"], ctypes.c_double), _p(out["mass_ideal"], ctypes.c_double),
+        _p(out["recall"], ctypes.c_double), _p(ks, ctypes.c_int64), _p(nT, ctypes.c_int64),
+        _p(out["mass_T"], ctypes.c_double))
+    if rc:
+        raise ValueError(f"sqzref_diagnostics rc={rc}")
+    out["k"] = ks
+    out["n_T"] = nT
+    return out

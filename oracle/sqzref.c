@@ -471,4 +471,88 @@ void sqzref_merge(int P, int64_t rows, int d, const double *O_parts, const doubl
     }
 }
 
+/* ------------------------------------------------------------------------ */
+/* Selection diagnostics.                               */
+/*                                                                           */
+/* App. A ("cumulative attention scores for the top 1% highest    */
+/* scoring attention values"): per query row, the softmax over ALL fixed     */
+/* keys a_j = exp(z_j - LSE), z_j = scale q.k_j, sorted descending; skew =   */
+/* the sum of the n_top largest a_j ("up to a maximum of 1 ... sharper,      */
+/* more skewed"; n_top = ceil(top_frac L)).                       */
+/*                                                                           */
+/* App. D (the "Ideal" lookup): "compute attention from the ...  */
+/* query tokens to all of the fixed context keys", then "select the keys     */
+/* whose attention scores are above the configured threshold": n_T = #{a_j > */
+/* T}, mass_T = sum of those a_j.  Compared with the centroid selection      */
+/* `sel` (k keys) at MATCHED budget: the ideal k-set = the k largest */
+/* a_j (ties: lower key index first); recall = |sel n ideal_k| / k (1 when   */
+/* k = 0); mass_sel = sum_{j in sel} a_j (the attention mass the centroid    */
+/* selection retrieves); mass_ideal = sum of the k largest a_j (its upper    */
+/* bound, "an upper bound on the attainable accuracy").                */
+/* Q [B,H,d] (one decode query per (b,h)); K [H,L,d] original order; sel     */
+/* [B,H,L] uint8 in original key order.  Outputs are [B,H].                  */
+/* ------------------------------------------------------------------------ */
+typedef struct { double a; int64_t j; } sqzref_rank_t;
+
+static int rank_desc(const void *x, const void *y)
+{
+    const sqzref_rank_t *p = (const sqzref_rank_t *)x, *q = (const sqzref_rank_t *)y;
+    if (p->a > q->a) return -1;
+    if (p->a < q->a) return 1;
+    return (p->j > q->j) - (p->j < q->j);
+}
+
+int sqzref_diagnostics(int B, int H, int d, int64_t L, const double *Q, const double *K,
+                       const uint8_t *sel, double scale, int64_t n_top, double T,
+                       double *skew, double *mass_sel, double *mass_ideal, double *recall,
+                       int64_t *k_out, int64_t *n_T, double *mass_T)
+{
+    if (B < 1 || H < 1 || d < 1 || L < 1 || n_top < 1 || n_top > L || !(T >= 0.0))
+        return SQZREF_ERR_INVALID;
+#pragma omp parallel for schedule(dynamic)
+    for (int64_t bh = 0; bh < (int64_t)B * H; ++bh) {
+        const int h = (int)(bh % H);
+        const double *q = Q + (size_t)bh * d;
+        const double *Kh = K + (size_t)h * L * d;
+        const uint8_t *sl = sel + (size_t)bh * L;
+        sqzref_rank_t *r = (sqzref_rank_t *)malloc((size_t)L * sizeof(sqzref_rank_t));
+        /* z_j and the softmax over all L fixed keys */
+        double m = -INFINITY;
+        for (int64_t j = 0; j < L; ++j) {
+            double z = 0.0;
+            for (int k = 0; k < d; ++k) z += q[k] * Kh[(size_t)j * d + k];
+            r[j].a = scale * z;
+            r[j].j = j;
+            if (r[j].a > m) m = r[j].a;
+        }
+        double l = 0.0;
+        for (int64_t j = 0; j < L; ++j) l += exp(r[j].a - m);
+        const double lse = m + log(l);
+        int64_t k = 0, nt = 0;
+        double ms = 0.0, mt = 0.0;
+        for (int64_t j = 0; j < L; ++j) {
+            r[j].a = exp(r[j].a - lse);
+            if (sl[j]) { ++k; ms += r[j].a; }
+            if (T == 0.0 || r[j].a > T) { ++nt; mt += r[j].a; }   /* T = 0 selects all (R6) */
+        }
+        qsort(r, (size_t)L, sizeof(sqzref_rank_t), rank_desc);
+        double sk = 0.0, mi = 0.0;
+        int64_t hit = 0;
+        for (int64_t t = 0; t < n_top; ++t) sk += r[t].a;
+        for (int64_t t = 0; t < k; ++t) {
+            mi += r[t].a;
+            if (sl[r[t].j]) ++hit;
+        }
+        skew[bh] = sk;
+        mass_sel[bh] = ms;
+        mass_ideal[bh] = mi;
+        recall[bh] = k ? (double)hit / (double)k : 1.0;
+        k_out[bh] = k;
+        n_T[bh] = nt;
+        mass_T[bh] = mt;
+        free(r);
+    }
+    return SQZREF_OK;
+}
+
 int sqzref_version(void) { return 1; }

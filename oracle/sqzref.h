@@ -40,6 +40,10 @@ int sqzref_attention(int B, int H, int n_q, int d, int64_t L, int n_u,
                      const int32_t *qpos, double scale, double *O, double *LSE);
 void sqzref_merge(int P, int64_t rows, int d, const double *O_parts, const double *LSE_parts,
                   double *O, double *LSE);
+int sqzref_diagnostics(int B, int H, int d, int64_t L, const double *Q, const double *K,
+                       const uint8_t *sel, double scale, int64_t n_top, double T,
+                       double *skew, double *mass_sel, double *mass_ideal, double *recall,
+                       int64_t *k_out, int64_t *n_T, double *mass_T);
 int sqzref_version(void);
 
 #ifdef __cplusplus
