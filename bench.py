@@ -320,6 +320,38 @@ def oracle_parity(sqz, gidx, q, sel, O, LSE, T, T1, scale, K0, V0, Ku0, Vu0, loc
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
+def selection_quality(sqz, idx, Qt, Kp, scale, T, T1, n_in, B, dev):
+    """sqz_selection_diagnostics over the first n_in test inputs: App. A's top-1%
+    cumulative attention score per (b,h) and App. D's ideal lookup at
+    the same T against the centroid selection at matched budget."""
+    import torch
+
+    sel = sqz.Selection.empty(idx, B, 1, False, dev, key_idx=False)
+    acc = {k: [] for k in ("skew", "mass_sel", "mass_ideal", "recall", "n_T", "mass_T", "k")}
+    for i in range(n_in):
+        sqz.centroid_lookup(idx, Qt[i], scale, T, T1, sel=sel)
+        out = sqz.selection_diagnostics(idx, Qt[i], Kp, sel, scale, 0.01, T)
+        for k, v in out.items():
+            acc[k].append(v.float().cpu().numpy().ravel())
+        acc["k"].append(sel.n_keys.float().cpu().numpy().ravel())
+    torch.cuda.synchronize()
+    a = {k: np.concatenate(v) for k, v in acc.items()}
+    L = idx.L
+    sk = a["skew"]
+    ret = a["k"] / L
+    corr = float(np.corrcoef(sk, ret)[0, 1]) if sk.std() > 0 and ret.std() > 0 else None
+    r4 = lambda x: round(float(x), 4)
+    return {"rows": int(sk.size), "top_frac": 0.01,
+            "skew_top1pct": {"min": r4(sk.min()), "median": r4(np.median(sk)), "max": r4(sk.max())},
+            "corr_skew_vs_retention": None if corr is None else r4(corr),
+            "mass_retrieved_mean": r4(a["mass_sel"].mean()),
+            "mass_ideal_same_budget_mean": r4(a["mass_ideal"].mean()),
+            "recall_vs_ideal_same_budget_mean": r4(a["recall"].mean()),
+            "ideal_at_T_retention_mean": r4((a["n_T"] / L).mean()),
+            "ideal_at_T_mass_mean": r4(a["mass_T"].mean()),
+            "what": "sqz_selection_diagnostics (App. A skewness; App. D ideal lookup), fixed keys only"}
+
+
 def capture_graph(fn):
     """Capture `fn` (a sequence of libsqz calls on the current stream) into a CUDA
     graph; one eager warm-up call first fills the library's host-side caches."""
@@ -668,6 +700,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                    causal, rs)
             parity["oracle_s"] = round(time.time() - t_p, 1)
         del sel_p
+    # ---- selection quality (App. A skewness, App. D ideal lookup; after the timed region) ----
+    quality = None
+    if cfg["mode"] == "decode" and comm is None and rank == 0 and not args.no_parity:
+        quality = selection_quality(sqz, idx, Qt, Kp, scale, T, T1, min(n_inputs, 8), B, dev)
     # ---- max over ranks ----
     if world > 1:
         tt = torch.tensor([t_step, t_look, t_attn, t_e2e, t_eager], device=dev)
@@ -760,6 +796,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     }
     if parity is not None:
         line["parity"] = parity
+    if quality is not None:
+        line["selection_quality"] = quality
     return line
 
 

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQZ_ABI_VERSION 4
+#define SQZ_ABI_VERSION 5
 
 enum {
     SQZ_OK = 0,
@@ -294,6 +294,45 @@ int sqz_attention_status(void *ws, size_t ws_bytes, void *stream);
  *   LSE = log sum_p exp(LSE_p), O = sum_p exp(LSE_p - LSE) O_p. */
 int sqz_merge_partials(int32_t P, const float *O_parts, const float *LSE_parts, int64_t rows,
                        int32_t d, void *O, float *LSE, int32_t out_dtype, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Selection diagnostics (App. A; App. D; NEXT-4)        */
+/* ---------------------------------------------------------------------- */
+/* For ONE decode query per (b,h) (Q [B,H,1,d]) and the selection `sel` the
+ * lookup produced for it (clusters, n_clusters, n_keys read), with
+ * a_j = exp(z_j - LSE) the softmax of z_j = scale q.k_j over ALL L fixed keys
+ * of the head (Kp, cluster-major; attention is permutation-invariant):
+ *   skew       [B,H] fp32  sum of the n_top largest a_j, n_top = max(1,
+ *                          ceil(top_frac * L)) -- App. A's "cumulative
+ *                          attention scores for the top 1%" (1 = skewed head,
+ *                          ~top_frac = flat head)
+ *   n_T, mass_T [B,H]      App. D's ideal lookup at threshold T: the keys with
+ *                          a_j > T (T == 0: all), their count and mass
+ *   mass_sel   [B,H] fp32  sum of a_j over the selected keys (the attention
+ *                          mass the centroid lookup retrieves)
+ *   mass_ideal [B,H] fp32  sum of the k largest a_j, k = n_keys[b,h] (the
+ *                          ideal selection at MATCHED budget; >= mass_sel)
+ *   recall     [B,H] fp32  |selected n ideal k-set| / k (1 when k = 0)
+ * Logits are fp32 dot products of the stored bits (the logits attention
+ * uses); the oracle ranks fp64 logits, so results can differ only through
+ * fp32 rounding of near-equal logits.  Not an online-path call: three
+ * launches, the last with one CTA per (b,h).  Unsharded indexes only
+ * (L_total == 0).  ws: sqz_selection_diagnostics_workspace bytes (about
+ * 5 B per (b,h) and key; no zeroing needed).  Errors: SQZ_ERR_INVALID_ARG
+ * (NULL pointers, top_frac not in (0, 1], T < 0 or NaN, sharded index). */
+typedef struct {
+    float *skew;
+    float *mass_sel;
+    float *mass_ideal;
+    float *recall;
+    int32_t *n_T;
+    float *mass_T;
+} sqz_diagnostics;
+
+int sqz_selection_diagnostics_workspace(const sqz_index *idx, int32_t B, size_t *ws_bytes);
+int sqz_selection_diagnostics(const sqz_index *idx, const void *Q, int32_t B, const void *Kp,
+                              const sqz_selection *sel, float scale, double top_frac, float T,
+                              const sqz_diagnostics *out, void *ws, size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Multi-GPU: fixed-context sharding by cluster (the paper is    */

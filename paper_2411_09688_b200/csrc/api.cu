@@ -559,4 +559,65 @@ int sqz_merge_partials(int32_t P, const float *O_parts, const float *LSE_parts, 
     return SQZ_OK;
 }
 
+// ------------------------------------------------------------------ diagnostics
+int sqz_selection_diagnostics_workspace(const sqz_index *idx, int32_t B, size_t *ws_bytes) {
+    int rc = check_index(idx, false);
+    if (rc) return rc;
+    if (B < 1) return fail(SQZ_ERR_INVALID_ARG, "B = %d must be >= 1", B);
+    if (!ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes is NULL");
+    *ws_bytes = diag_ws_bytes(B, idx->H, idx->c2, idx->L) + 256;
+    return SQZ_OK;
+}
+
+int sqz_selection_diagnostics(const sqz_index *idx, const void *Q, int32_t B, const void *Kp,
+                              const sqz_selection *sel, float scale, double top_frac, float T,
+                              const sqz_diagnostics *out, void *ws, size_t ws_bytes, void *stream) {
+    int rc = check_index(idx, true);
+    if (rc) return rc;
+    if (idx->L_total != 0) return fail(SQZ_ERR_INVALID_ARG, "diagnostics need an unsharded index");
+    if (!Q || !Kp) return fail(SQZ_ERR_INVALID_ARG, "Q and Kp must be non-NULL");
+    if (!aligned16(Q) || !aligned16(Kp)) return fail(SQZ_ERR_INVALID_ARG, "Q, Kp must be 16-byte aligned");
+    if (B < 1) return fail(SQZ_ERR_INVALID_ARG, "B = %d must be >= 1", B);
+    if (!sel || !sel->clusters || !sel->n_clusters || !sel->n_keys)
+        return fail(SQZ_ERR_INVALID_ARG, "sel->clusters / n_clusters / n_keys required");
+    if (!(top_frac > 0.0 && top_frac <= 1.0))
+        return fail(SQZ_ERR_INVALID_ARG, "top_frac = %g must be in (0, 1]", top_frac);
+    if (!(T >= 0.f) || std::isinf(T))
+        return fail(SQZ_ERR_INVALID_ARG, "T = %g must be finite and >= 0", (double)T);
+    if (!std::isfinite(scale)) return fail(SQZ_ERR_INVALID_ARG, "scale must be finite");
+    if (!out || !out->skew || !out->mass_sel || !out->mass_ideal || !out->recall || !out->n_T ||
+        !out->mass_T)
+        return fail(SQZ_ERR_INVALID_ARG, "every sqz_diagnostics output is required");
+    const size_t need = diag_ws_bytes(B, idx->H, idx->c2, idx->L);
+    if (!ws || ws_bytes < need) return fail(SQZ_ERR_INVALID_ARG, "ws too small (need %zu bytes)", need);
+    DiagLaunch a;
+    std::memset(&a, 0, sizeof(a));
+    a.Q = Q;
+    a.Kp = Kp;
+    a.key_off = idx->key_off;
+    a.clusters = sel->clusters;
+    a.n_clusters = sel->n_clusters;
+    a.n_keys = sel->n_keys;
+    a.B = B;
+    a.H = idx->H;
+    a.c2 = idx->c2;
+    a.d = idx->d;
+    a.dtype = idx->dtype;
+    a.L = idx->L;
+    a.scale = scale;
+    a.T = T;
+    const long long nt = (long long)std::ceil(top_frac * (double)idx->L);
+    a.n_top = nt < 1 ? 1 : (nt > idx->L ? idx->L : nt);
+    a.ws = ws;
+    a.skew = out->skew;
+    a.mass_sel = out->mass_sel;
+    a.mass_ideal = out->mass_ideal;
+    a.recall = out->recall;
+    a.n_T = out->n_T;
+    a.mass_T = out->mass_T;
+    cudaError_t e = launch_diagnostics(a, (cudaStream_t)stream);
+    return e == cudaSuccess ? SQZ_OK : cuda_fail(e, "diagnostics launch");
+}
+
+
 }  // extern "C"

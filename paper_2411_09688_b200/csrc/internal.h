@@ -121,6 +121,21 @@ size_t decode_step_ws_bytes(int B, int H, int c, int n_u, int d);
 int decode_step_rows_ok(int B, int H, int c, long long L);
 cudaError_t launch_decode_step(const StepLaunch &l, cudaStream_t st);
 
+// diag.cu: App. A skewness + App. D ideal-lookup diagnostics (NEXT-4)
+struct DiagLaunch {
+    const void *Q, *Kp;
+    const int32_t *key_off, *clusters, *n_clusters, *n_keys;
+    int32_t B, H, c2, d, dtype;
+    int64_t L;
+    float scale, T;
+    long long n_top;
+    void *ws;
+    float *skew, *mass_sel, *mass_ideal, *recall, *mass_T;
+    int32_t *n_T;
+};
+size_t diag_ws_bytes(int B, int H, int c2, int64_t L);
+cudaError_t launch_diagnostics(const DiagLaunch &a, cudaStream_t st);
+
 // kmeans.cu
 struct KmeansWs;
 size_t kmeans_workspace_bytes(const sqz_index &idx);

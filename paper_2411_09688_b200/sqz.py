@@ -25,7 +25,7 @@ SO = os.path.join(HERE, "libsqz.so")
 SQZ_F32, SQZ_BF16 = 0, 1
 SQZ_OK, SQZ_ERR_INVALID_ARG, SQZ_ERR_FORMAT, SQZ_ERR_INVARIANT = 0, 2, 3, 4
 SQZ_ERR_CUDA, SQZ_ERR_NCCL, SQZ_ERR_EMPTY, SQZ_ERR_UNSUPPORTED = 5, 6, 7, 8
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 EXPORTS = [
     "sqz_cluster_keys_workspace", "sqz_cluster_keys", "sqz_index_validate_workspace",
@@ -35,7 +35,7 @@ EXPORTS = [
     "sqz_device_check", "sqz_centroid_lookup_stage", "sqz_shard_plan_compute", "sqz_index_shard",
     "sqz_comm_unique_id", "sqz_comm_init", "sqz_comm_destroy", "sqz_lookup_workspace_comm",
     "sqz_comm_merge_workspace", "sqz_comm_allgather_merge", "sqz_decode_step_workspace",
-    "sqz_decode_step",
+    "sqz_decode_step", "sqz_selection_diagnostics_workspace", "sqz_selection_diagnostics",
 ]
 
 
@@ -72,6 +72,11 @@ class sqz_selection(ctypes.Structure):
 class sqz_attn_params(ctypes.Structure):
     _fields_ = [("scale", ctypes.c_float), ("causal", ctypes.c_int32), ("partial", ctypes.c_int32),
                 ("out_dtype", ctypes.c_int32)]
+
+
+class sqz_diagnostics(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in
+                ("skew", "mass_sel", "mass_ideal", "recall", "n_T", "mass_T")]
 
 
 class SqzError(RuntimeError):
@@ -128,6 +133,10 @@ def lib():
                                       ctypes.POINTER(sqz_lookup_params),
                                       ctypes.POINTER(sqz_attn_params), ctypes.POINTER(sqz_selection),
                                       vp, vp, vp, sz, vp]
+        L.sqz_selection_diagnostics_workspace.argtypes = [ip, i32, szp]
+        L.sqz_selection_diagnostics.argtypes = [ip, vp, i32, vp, ctypes.POINTER(sqz_selection),
+                                                ctypes.c_float, ctypes.c_double, ctypes.c_float,
+                                                ctypes.POINTER(sqz_diagnostics), vp, sz, vp]
         if L.sqz_abi_version() != ABI_VERSION:
             raise RuntimeError(f"{SO} has ABI {L.sqz_abi_version()}, binding expects {ABI_VERSION}: "
                                "rebuild with __graft_entry__.build()")
@@ -551,3 +560,25 @@ def allgather_merge(comm: Comm, O_part: torch.Tensor, LSE_part: torch.Tensor, ou
     _check(lib().sqz_comm_allgather_merge(comm.handle, _p(O_part), _p(LSE_part), rows, d, _p(O),
                                           _p(LSE), out_dtype, _p(ws), ws.numel(), _stream()))
     return O, LSE
+
+
+def selection_diagnostics(idx: Index, Q: torch.Tensor, Kp: torch.Tensor, sel: Selection, scale: float,
+                          top_frac: float = 0.01, T: float = 0.0):
+    """sqz_selection_diagnostics (App. A skewness, App. D ideal lookup) for one
+    decode query per (b,h), Q [B,H,1,d].  Returns a dict of [B,H] tensors:
+    skew, mass_sel, mass_ideal, recall, n_T, mass_T."""
+    B = Q.shape[0]
+    s = idx.struct()
+    nb = ctypes.c_size_t(0)
+    _check(lib().sqz_selection_diagnostics_workspace(ctypes.byref(s), B, ctypes.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=Q.device)
+    f32 = dict(dtype=torch.float32, device=Q.device)
+    out = {k: torch.empty(B, idx.H, **f32) for k in ("skew", "mass_sel", "mass_ideal", "recall",
+                                                     "mass_T")}
+    out["n_T"] = torch.empty(B, idx.H, dtype=torch.int32, device=Q.device)
+    d = sqz_diagnostics(*[out[k].data_ptr() for k, _ in sqz_diagnostics._fields_])
+    ss = sel.struct()
+    _check(lib().sqz_selection_diagnostics(ctypes.byref(s), _p(Q), B, _p(Kp), ctypes.byref(ss),
+                                           float(scale), float(top_frac), float(T), ctypes.byref(d),
+                                           _p(ws), nb.value, _stream()))
+    return out

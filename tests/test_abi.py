@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(lib):
     for name in decl:
         assert hasattr(lib, name), name
     assert sorted(sqz.EXPORTS) == decl
-    assert lib.sqz_abi_version() == sqz.ABI_VERSION == 4
+    assert lib.sqz_abi_version() == sqz.ABI_VERSION == 5
 
 
 def test_struct_layout_matches_header(tmp_path):
@@ -45,6 +45,7 @@ def test_struct_layout_matches_header(tmp_path):
                     " offsetof(sqz_index, C1), offsetof(sqz_index, perm), sizeof(sqz_selection),"
                     " sizeof(sqz_lookup_params), sizeof(sqz_attn_params), sizeof(sqz_kmeans_params),"
                     " offsetof(sqz_index, L_total), sizeof(sqz_shard_plan), offsetof(sqz_shard_plan, key_off));"
+                    "printf(\"%zu %zu\\n\", sizeof(sqz_diagnostics), offsetof(sqz_diagnostics, n_T));"
                     "return 0;}\n")
     exe = tmp_path / "lay"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)])
@@ -53,7 +54,8 @@ def test_struct_layout_matches_header(tmp_path):
             ctypes.sizeof(sqz.sqz_selection), ctypes.sizeof(sqz.sqz_lookup_params),
             ctypes.sizeof(sqz.sqz_attn_params), ctypes.sizeof(sqz.sqz_kmeans_params),
             sqz.sqz_index.L_total.offset, ctypes.sizeof(sqz.sqz_shard_plan),
-            sqz.sqz_shard_plan.key_off.offset]
+            sqz.sqz_shard_plan.key_off.offset, ctypes.sizeof(sqz.sqz_diagnostics),
+            sqz.sqz_diagnostics.n_T.offset]
     assert got == want
 
 
