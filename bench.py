@@ -509,12 +509,23 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # reader (key_idx=False) measured slower than the lookup's expansion on every config
     sel = sqz.Selection.empty(idx, B, n_q, False, dev, key_idx=True)
     esz = 2 if dt == 1 else 4
-    ks = []
+    ks, kus = [], []
+    c2l = idx.c2
     for i in range(n_inputs):
         sqz.centroid_lookup(idx, Qt[i], scale, T, T1, sel=sel, comm=comm)
         ks.append(int(sel.n_keys.sum()))
+        # keys in the per-head UNION of the B selections (what the batch-shared pass reads)
+        ar = torch.arange(c2l, device=dev)
+        ids = torch.where(ar[None, None, :] < sel.n_clusters[:, :, None], sel.clusters,
+                          torch.full_like(sel.clusters, c2l)).long()
+        um = torch.zeros(B, Hl, c2l + 1, dtype=torch.bool, device=dev)
+        um.scatter_(2, ids, True)
+        kus.append(int((um[:, :, :c2l].any(0) * idx.N2).sum()))
     torch.cuda.synchronize()
     k_mean = float(np.mean(ks))  # this rank's selected keys per step
+    ku_mean = float(np.mean(kus))  # this rank's union keys per step (= k_mean when B = 1)
+    shared_attn = (cfg["mode"] == "decode" and B >= 2 and d == 128 and dt == 1
+                   and not args.attn_per_row)
     k_glob = allsum(k_mean)
     # algorithmic bytes / flops of THIS rank
     c1l, c2l = idx.c1, idx.c2
@@ -523,6 +534,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if c1:
         bytes_lookup += Hl * 0.5 * c2l * (d * esz + 4) * B  # ~50% of L2 rows scanned per query
     bytes_attn = k_mean * 2 * d * esz + B * Hl * n_u_r * 2 * d * esz + 2 * B * Hl * n_q * d * esz
+    bytes_attn_perq = bytes_attn
+    if shared_attn:  # NEXT-1: each selected key is read once for all the queries that chose it
+        bytes_attn = ku_mean * 2 * d * esz + B * Hl * n_u_r * 2 * d * esz + 2 * B * Hl * n_q * d * esz
     flops_attn = 4.0 * n_q * d * k_mean + (4.0 * d * B * Hl * (n_q * n_u_r - n_q * (n_q - 1) / 2)
                                           if n_u_r else 0.0)
     flops_lookup = 2.0 * B * Hl * n_q * lookup_rows * d
@@ -551,10 +565,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
     def attend_into(q, Oo, Lo, sl=None):
         sl = sel if sl is None else sl
         if comm is None:
-            sqz.sparse_attention(q, Kp, Vp, idx, sl, Ku, Vu, scale, causal=causal, O=Oo, LSE=Lo)
+            sqz.sparse_attention(q, Kp, Vp, idx, sl, Ku, Vu, scale, causal=causal, O=Oo, LSE=Lo,
+                                 per_row=args.attn_per_row)
         else:  # partial over this shard, then the all-gather merge (P:361-363 across GPUs)
             sqz.sparse_attention(q, Kp, Vp, idx, sl, Ku, Vu, scale, causal=causal, partial=True,
-                                 out_dtype=sqz.SQZ_F32, O=Op, LSE=Lp)
+                                 out_dtype=sqz.SQZ_F32, O=Op, LSE=Lp, per_row=args.attn_per_row)
             sqz.allgather_merge(comm, Op, Lp, out_dtype=dt, O=Oo, LSE=Lo)
 
     def attend(q):
@@ -733,7 +748,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
             roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                     "frac": round(ach / hbm, 4),
                     "traffic": traffic_for(args.config, "sparse_attention"),
-                    "kernel": "k_attend (persistent split-KV over equal key ranges + fused merge)",
+                    "kernel": ("k_attend_shared (batch-shared union pass, mma.sync tiles, fused merge); "
+                               "bytes = union of the B selections per head" if shared_attn else
+                               "k_attend (persistent split-KV over equal key ranges + fused merge)"),
+                    "bytes_if_streamed_per_query": int(bytes_attn_perq),
                     "peak_kind": f"{peak_kind} copy bandwidth",
                     "bytes_per_launch": int(bytes_attn)}
         whole = {"bytes_per_step": int(step_bytes),
@@ -758,7 +776,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         n_look = levels * per_select
     else:  # stats, then per level: fold + select (+ next level's stats)
         n_look = 1 + levels * (1 + per_select) + (levels - 1)
-    launches = K_ * (n_look + 1 + (1 if comm else 0))
+    launches = K_ * (n_look + 1 + (1 if comm else 0) + (1 if shared_attn else 0))  # + k_union
     if use_step and idx.levels == 1:
         launches = K_  # one k_decode_step per step
     metric, unit, hib = metric_of(cfg)
@@ -779,6 +797,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                         "read of another buffer (untimed), so the step starts from "
                                         "a cold L2 of clean lines"}[args.flush],
                    "T": T, "T1": T1, "mean_selected_keys_per_step": k_glob,
+                   "mean_union_keys_per_step": allsum(ku_mean),
+                   "attention_path": "batch-shared union pass" if shared_attn else "per-(b,h) streams",
                    "retention_realized": k_glob / (B * H * L), "kmeans_iters": list(iters),
                    "index_build_s": round(t_index, 2)},
         "phases_ms": {"lookup": round(t_look, 5), "sparse_attention": round(t_attn, 5),
@@ -827,6 +847,9 @@ def main():
     ap.add_argument("--retention", type=float, default=None,
                     help="override the config's retention target (1.0 = T = 0, dense)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--attn-per-row", action="store_true",
+                    help="decode with B >= 2: stream each (b,h) selection separately instead of "
+                         "the batch-shared union pass (A/B of NEXT-1)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="time eager per-call launches instead of CUDA-graph replay")
     args = ap.parse_args()

@@ -239,6 +239,12 @@ typedef struct {
                        /*    partial for a later merge); 0: such rows are an error,          */
                        /*    reported by sqz_attention_status()                              */
     int32_t out_dtype; /* sqz_dtype of O                                                     */
+    int32_t per_row;   /* decode (n_q == 1) with B >= 2: 0 (default) = the B sequences share  */
+                       /*    the fixed context, so each head streams the UNION of   */
+                       /*    its B selections once, every key applied to the queries whose    */
+                       /*    selection holds it (bf16, d = 128, B <= 16); 1 = one key stream  */
+                       /*    per (b,h).  Same result either way (each query attends exactly   */
+                       /*    its own selection plus its own user KV).                         */
 } sqz_attn_params;
 
 int sqz_attention_workspace(const sqz_index *idx, int32_t B, int32_t n_q, int32_t n_u,

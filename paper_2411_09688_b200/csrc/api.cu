@@ -133,6 +133,7 @@ struct AttnWs {
     float *part_o, *part_lse;
     int32_t *status, *row_cnt, *cut;
     int32_t kch, max_chunks;
+    char *shared;  // batch-shared decode region (B >= 2, n_q == 1)
     size_t bytes;
 };
 AttnWs attn_carve(const sqz_index *idx, int B, int n_q, int n_u, char *base) {
@@ -152,6 +153,9 @@ AttnWs attn_carve(const sqz_index *idx, int B, int n_q, int n_u, char *base) {
                             : rows * w.max_chunks;
     w.part_lse = cv.take<float>(prow);
     w.part_o = cv.take<float>(prow * idx->d);
+    w.shared = shared_attn_applies(B, n_q, idx->d, idx->dtype, idx->c2)
+                   ? cv.take<char>(shared_attn_ws_bytes(B, idx->H, idx->c2))
+                   : nullptr;
     w.bytes = cv.used + 256;
     return w;
 }
@@ -457,7 +461,13 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
     a.sched = w.status + 1;
     a.cut = w.cut;
     a.O = O; a.LSE = LSE;
-    cudaError_t e = launch_attention(a, (cudaStream_t)stream);
+    a.shared_ws = w.shared;
+    a.N2 = idx->N2;
+    cudaError_t e;
+    if (w.shared && !p->per_row && sel->clusters && sel->n_clusters && idx->N2 && idx->key_off)
+        e = launch_attention_shared(a, (cudaStream_t)stream);
+    else
+        e = launch_attention(a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "sparse attention launch");
     return SQZ_OK;
 }

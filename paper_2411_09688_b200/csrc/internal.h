@@ -90,8 +90,16 @@ struct AttnArgs {
     int32_t *cut;     // [3 * 1024] cut-segment slots of the persistent prefill kernel (one per CTA)
     void *O;
     float *LSE;
+    // batch-shared decode (shared_attn.cu): its workspace region and the N2 table
+    void *shared_ws;
+    const int32_t *N2;
 };
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st);
+// shared_attn.cu: batch-shared decode attention over the per-head union of the
+// B selections (NEXT-1)
+bool shared_attn_applies(int B, int n_q, int d, int dtype, int c2);
+size_t shared_attn_ws_bytes(int B, int H, int c2);
+cudaError_t launch_attention_shared(const AttnArgs &a, cudaStream_t st);
 // prefill_attn.cu: tcgen05 path for bf16 prefill (n_q > 1)
 cudaError_t launch_prefill_attention(const AttnArgs &a, cudaStream_t st);
 cudaError_t launch_prefill_attention_ws(const AttnArgs &a, cudaStream_t st);  // d = 128

@@ -71,7 +71,7 @@ class sqz_selection(ctypes.Structure):
 
 class sqz_attn_params(ctypes.Structure):
     _fields_ = [("scale", ctypes.c_float), ("causal", ctypes.c_int32), ("partial", ctypes.c_int32),
-                ("out_dtype", ctypes.c_int32)]
+                ("out_dtype", ctypes.c_int32), ("per_row", ctypes.c_int32)]
 
 
 class sqz_diagnostics(ctypes.Structure):
@@ -359,8 +359,10 @@ def centroid_lookup(idx: Index, Q: torch.Tensor, scale: float, T: float, T1: flo
 
 
 def sparse_attention(Q, Kp, Vp, idx: Index, sel: Selection, Ku=None, Vu=None, scale=None,
-                     causal=False, partial=False, out_dtype=None, O=None, LSE=None, ws=None):
-    """sqz_sparse_attention: returns (O[B,H,n_q,d], LSE[B,H,n_q])."""
+                     causal=False, partial=False, out_dtype=None, O=None, LSE=None, ws=None,
+                     per_row=False):
+    """sqz_sparse_attention: returns (O[B,H,n_q,d], LSE[B,H,n_q]).  per_row=True
+    disables the batch-shared decode pass (one key stream per (b,h))."""
     B, H, n_q, d = Q.shape
     n_u = 0 if Ku is None else Ku.shape[2]
     if scale is None:
@@ -376,7 +378,7 @@ def sparse_attention(Q, Kp, Vp, idx: Index, sel: Selection, Ku=None, Vu=None, sc
         ws = _WS.get(("attn", Q.device, idx.H, idx.L, B, n_q, n_u),
                      attention_workspace_bytes(idx, B, n_q, n_u), Q.device)
         _WS.last_attn = ws
-    p = sqz_attn_params(scale, int(causal), int(partial), out_dtype)
+    p = sqz_attn_params(scale, int(causal), int(partial), out_dtype, int(per_row))
     ss = sel.struct()
     _check(lib().sqz_sparse_attention(_p(Q), B, n_q, _p(Kp), _p(Vp), ctypes.byref(s),
                                       ctypes.byref(ss), _p(Ku), _p(Vu), n_u, ctypes.byref(p),

@@ -180,6 +180,42 @@ def test_decode_lookup_and_attention(case):
     _check_runs(t, sel, O, LSE, scale, T, T1, False, True)
 
 
+SHARED_CASES = [
+    # batch-shared decode (NEXT-1): B queries per head over one fixed context; the
+    # union pass must give every query exactly its own selection's attention
+    ("shared_B8", 4, 5000, 128, 120, 0, synth.BF16, 8, 64, 0.15),
+    ("shared_B16_hier", 3, 6000, 128, 240, 40, synth.BF16, 16, 33, 0.1),
+    ("shared_B2_nu0", 2, 3000, 128, 90, 0, synth.BF16, 2, 0, 0.3),
+    ("shared_B5_dense", 2, 2100, 128, 50, 0, synth.BF16, 5, 17, 1.0),
+]
+
+
+@pytest.mark.parametrize("case", SHARED_CASES, ids=lambda c: c[0])
+def test_decode_batch_shared(case):
+    sqz = _sqz()
+    name, H, L, d, c2, c1, dt, B, n_u, ret = case
+    P = oracle_problem(H, L, d, c2, c1, dt, seed=zlib.crc32(name.encode()) % 1000, B=B, n_u=n_u)
+    scale = 1.0 / np.sqrt(d)
+    if ret >= 1.0:
+        T, T1 = 0.0, 0.0
+    else:
+        T, T1 = _calibrate(P, scale, ret)
+    t = _device(P)
+    sel = sqz.centroid_lookup(t["idx"], t["Q"], scale, T, T1, debug=True)
+    O, LSE = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, t["Ku"], t["Vu"], scale)
+    Or, Lr = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, t["Ku"], t["Vu"], scale,
+                                  per_row=True)
+    torch.cuda.synchronize()
+    _check_attention(P, sel, O, LSE, scale, False, B, 2e-2, 5e-3)
+    # the two paths compute the same rows (different summation order only)
+    assert (O.float() - Or.float()).abs().max().item() <= 2e-2
+    assert (LSE - Lr).abs().max().item() <= 1e-3
+    # repeated calls reuse the self-cleaning workspace
+    O2, L2 = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, t["Ku"], t["Vu"], scale)
+    torch.cuda.synchronize()
+    assert torch.equal(O, O2) and torch.equal(LSE, L2)
+
+
 @pytest.mark.parametrize("case", DECODE_CASES, ids=lambda c: c[0])
 def test_decode_step(case):
     """sqz_decode_step (one call: the fused single-level kernel, or the two calls for
