@@ -507,7 +507,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # ---- per-step work: selection sizes for the algorithmic-byte count ----
     # the expanded key-index tensor is materialised: the attention kernels' run-length
     # reader (key_idx=False) measured slower than the lookup's expansion on every config
-    sel = sqz.Selection.empty(idx, B, n_q, False, dev, key_idx=True)
+    # the batch-shared pass reads the run-length selection (clusters + key_pref) only
+    shared_attn = (cfg["mode"] == "decode" and B >= 2 and d == 128 and dt == 1
+                   and not args.attn_per_row)
+    sel = sqz.Selection.empty(idx, B, n_q, False, dev, key_idx=not (args.sel_runs or shared_attn))
     esz = 2 if dt == 1 else 4
     ks, kus = [], []
     c2l = idx.c2
@@ -524,8 +527,6 @@ def run_gpu(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     k_mean = float(np.mean(ks))  # this rank's selected keys per step
     ku_mean = float(np.mean(kus))  # this rank's union keys per step (= k_mean when B = 1)
-    shared_attn = (cfg["mode"] == "decode" and B >= 2 and d == 128 and dt == 1
-                   and not args.attn_per_row)
     k_glob = allsum(k_mean)
     # algorithmic bytes / flops of THIS rank
     c1l, c2l = idx.c1, idx.c2
@@ -847,6 +848,9 @@ def main():
     ap.add_argument("--retention", type=float, default=None,
                     help="override the config's retention target (1.0 = T = 0, dense)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sel-runs", action="store_true",
+                    help="keep the selection in run-length form (no key_idx expansion in the lookup; "
+                         "the attention reads the runs)")
     ap.add_argument("--attn-per-row", action="store_true",
                     help="decode with B >= 2: stream each (b,h) selection separately instead of "
                          "the batch-shared union pass (A/B of NEXT-1)")

@@ -1,0 +1,7 @@
+python -m paper_2411_09688_b200.build > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest -q -x tests/test_gpu_parity.py -k "shared or decode" > gpurun_out/test_shared.log 2>&1
+for v in "" "--sel-runs"; do
+  timeout 600 python bench.py --config cfg4 --no-cpu-baseline --steps 30 --no-parity $v > gpurun_out/bench_cfg4_shared$v.log 2>&1
+  timeout 600 python bench.py --config cfg4 --no-cpu-baseline --steps 30 --no-parity --attn-per-row $v > gpurun_out/bench_cfg4_perrow$v.log 2>&1
+  timeout 300 python bench.py --no-prefill --no-cpu-baseline --no-parity $v > gpurun_out/bench_cfg2$v.log 2>&1
+done

@@ -117,8 +117,15 @@ __device__ __forceinline__ int run_of(const RunList &r, int k) {
 // make the window hold the runs of stream keys [kmin, kmax] (warp-uniform,
 // kmin <= kmax < nkf; at most 64 runs apart)
 __device__ __forceinline__ void runwin_cover(RunWin &w, const RunList &r, int kmin, int kmax, int lane) {
-    const int first = __shfl_sync(FULL, w.p0, 0);
+    int first = __shfl_sync(FULL, w.p0, 0);
     if (kmin >= first && kmax < w.end) return;
+    // a warp advances by a fixed stride, so the next key usually lies just past the
+    // window: try the following 64 runs (one round trip) before a full search
+    if (w.end >= 0 && kmin >= w.end && w.J + 64 < r.n) {
+        runwin_load(w, r, w.J + 64, lane);
+        first = __shfl_sync(FULL, w.p0, 0);
+        if (kmax < w.end) return;
+    }
     int J;
     if (kmin >= first && kmin < w.end) {  // slide: the run of kmin is in the window
         const unsigned b0 = __ballot_sync(FULL, w.p0 <= kmin), b1 = __ballot_sync(FULL, w.p1 <= kmin);

@@ -145,8 +145,13 @@ __device__ __forceinline__ void vwin_load(RunWin &w, const VRun &r, int J, int l
     }
 }
 __device__ __forceinline__ void vwin_cover(RunWin &w, const VRun &r, int kmin, int kmax, int lane) {
-    const int first = __shfl_sync(FULL, w.p0, 0);
+    int first = __shfl_sync(FULL, w.p0, 0);
     if (kmin >= first && kmax < w.end) return;
+    if (w.end >= 0 && kmin >= w.end && w.J + 64 < r.n) {  // usually just past the window
+        vwin_load(w, r, w.J + 64, lane);
+        first = __shfl_sync(FULL, w.p0, 0);
+        if (kmax < w.end) return;
+    }
     int J;
     if (kmin >= first && kmin < w.end) {
         const unsigned b0 = __ballot_sync(FULL, w.p0 <= kmin), b1 = __ballot_sync(FULL, w.p1 <= kmin);

@@ -10,7 +10,7 @@
 //                  selected it) and the key prefix of the union;
 //   k_attend_shared persistent CTAs over equal-cost ranges of the per-head
 //                  streams [union fixed keys | user KV of b = 0 .. B-1] (the
-//                  user keys of b carry the mask {b}); a warp takes 16-key
+//                  user keys of b carry the mask {b}); a warp takes 32-key
 //                  tiles (cp.async, 3-stage ring per warp, XOR-swizzled rows)
 //                  and runs S = Q K^T and O += P V on the tensor cores
 //                  (mma.sync m16n8k16 bf16: M = the up-to-16 queries of the
@@ -33,15 +33,29 @@ namespace sqz {
 
 namespace shd {
 constexpr int D = 128;
-constexpr int NW = 8;              // warps per CTA (one CTA per SM)
+// measured on cfg4 (same box): 32-key tiles x 4 warps 240 us, 16 x 8 warps 245 us,
+// 16 x 6 warps x 4 stages 254 us, 16 x 4 warps x 6 stages 291 us
+#ifndef SQZ_SHD_NW
+#define SQZ_SHD_NW 4
+#endif
+#ifndef SQZ_SHD_TK
+#define SQZ_SHD_TK 32
+#endif
+#ifndef SQZ_SHD_NST
+#define SQZ_SHD_NST 3
+#endif
+constexpr int NW = SQZ_SHD_NW;     // warps per CTA (one CTA per SM)
 constexpr int NT = NW * 32;
-constexpr int TK = 16;             // keys per warp tile
-constexpr int NST = 3;             // ring stages per warp
+constexpr int TK = SQZ_SHD_TK;     // keys per warp tile (16 or 32)
+constexpr int NST = SQZ_SHD_NST;   // ring stages per warp
+constexpr int NB8 = TK / 8;        // n8 key tiles of S per warp tile
+static_assert(TK == 16 || TK == 32, "tile of 16 or 32 keys");
 constexpr int ROWB = D * 2;        // 256 B per bf16 row
 constexpr int TILEB = TK * ROWB;   // 4 KB: one K or V tile
 constexpr int STAGEB = 2 * TILEB;  // K then V
 constexpr int WARPB = NST * STAGEB;
-constexpr int SMEM = NW * WARPB;   // 192 KB
+constexpr int SMEM = NW * WARPB;   // 192 KB by default
+static_assert(SMEM <= 200 * 1024 && SMEM >= NW * 16 * 128 * 4, "ring holds the merge buffer");
 constexpr int SEG_KW = 256;        // partition cost of a segment's setup
 constexpr int MIN_KEYS = 1024;     // minimum cost units per CTA
 constexpr int MAXB = 16;
@@ -119,8 +133,15 @@ __device__ __forceinline__ void mwin_load(MWin &w, const UList &r, int J, int la
     w.s1 = j1 < r.n ? __ldg(r.koff + c1) : 0;
 }
 __device__ __forceinline__ void mwin_cover(MWin &w, const UList &r, int kmin, int kmax, int lane) {
-    const int first = __shfl_sync(FULL, w.p0, 0);
+    int first = __shfl_sync(FULL, w.p0, 0);
     if (kmin >= first && kmax < w.end) return;
+    // a warp's tiles advance by NW * TK keys, so the next key usually lies just past
+    // the window: try the following 64 runs (one round trip) before a full search
+    if (w.end >= 0 && kmin >= w.end && w.J + 64 < r.n) {
+        mwin_load(w, r, w.J + 64, lane);
+        first = __shfl_sync(FULL, w.p0, 0);
+        if (kmax < w.end) return;
+    }
     int J;
     if (kmin >= first && kmin < w.end) {
         const unsigned b0 = __ballot_sync(FULL, w.p0 <= kmin), b1 = __ballot_sync(FULL, w.p1 <= kmin);
@@ -374,7 +395,7 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
         auto issue = [&](int i, int st) {
             const int k0 = a0 + (warp + i * NW) * TK;
             const int kl = min(k0 + TK, a1) - 1;  // last valid key of the tile
-            const int myk = min(k0 + (lane & 15), kl);
+            const int myk = min(k0 + (lane & (TK - 1)), kl);
             if (k0 < KU) mwin_cover(win, ul, k0, min(kl, KU - 1), lane);
             int pos = 0, msk = 0;
             if (k0 < KU) mwin_get(win, min(myk, KU - 1), pos, msk);
@@ -388,7 +409,7 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
                 kr = a.Ku + (((size_t)b * H + h) * a.n_u + uu) * D;
                 vr = a.Vu + (((size_t)b * H + h) * a.n_u + uu) * D;
             }
-            if (k0 + (lane & 15) > kl) msk = 0;  // past the segment end: masked for every query
+            if (k0 + (lane & (TK - 1)) > kl) msk = 0;  // past the segment end: masked for every query
             if (lane < TK) s_tm[warp][st][lane] = msk;
             const uint32_t sK = wbase + st * STAGEB, sV = sK + TILEB;
             const int c = lane & 15;
@@ -415,49 +436,66 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
             cp_wait<NST - 1>();
             __syncwarp();
             const uint32_t sK = wbase + st * STAGEB, sV = sK + TILEB;
-            // ---- S = Q K^T: two n8 tiles (keys 0-7, 8-15) ----
-            float s[2][4];
+            // ---- S = Q K^T: NB8 n8 tiles of keys ----
+            // two accumulator sets (even / odd k-steps) halve the dependent HMMA chain
+            float s[NB8][4], s2[NB8][4];
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+            for (int nt = 0; nt < NB8; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) s[nt][e] = s2[nt][e] = 0.f;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-                // matrices: (keys 0-7, dims lo), (keys 0-7, dims hi), (keys 8-15, lo), (8-15, hi)
-                const int mi = lane >> 3, r = (mi >> 1) * 8 + (lane & 7), c = kk * 2 + (mi & 1);
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4(sK + swz(r, c), b0, b1, b2, b3);
-                mma16816(s[0], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
-                mma16816(s[1], qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b2, b3);
+#pragma unroll
+                for (int pr = 0; pr < NB8 / 2; ++pr) {
+                    // matrices: (keys 16pr+0-7, dims lo), (same keys, dims hi), (keys 16pr+8-15, lo), (hi)
+                    const int mi = lane >> 3, r = pr * 16 + (mi >> 1) * 8 + (lane & 7), c = kk * 2 + (mi & 1);
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(sK + swz(r, c), b0, b1, b2, b3);
+                    float(&d0)[4] = (kk & 1) ? s2[2 * pr] : s[2 * pr];
+                    float(&d1)[4] = (kk & 1) ? s2[2 * pr + 1] : s[2 * pr + 1];
+                    mma16816(d0, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
+                    mma16816(d1, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b2, b3);
+                }
             }
-            // ---- mask, online softmax (rows g, g + 8; keys 2t4, 2t4+1, 8+2t4, 9+2t4) ----
-            int mk[4];
-            mk[0] = s_tm[warp][st][2 * t4];
-            mk[1] = s_tm[warp][st][2 * t4 + 1];
-            mk[2] = s_tm[warp][st][8 + 2 * t4];
-            mk[3] = s_tm[warp][st][9 + 2 * t4];
-            float p[2][4];
+#pragma unroll
+            for (int nt = 0; nt < NB8; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) s[nt][e] += s2[nt][e];
+            // ---- mask, online softmax (rows g, g + 8; keys 8j + 2t4, 8j + 2t4 + 1) ----
+            int mk[NB8][2];
+#pragma unroll
+            for (int jt = 0; jt < NB8; ++jt) {
+                mk[jt][0] = s_tm[warp][st][jt * 8 + 2 * t4];
+                mk[jt][1] = s_tm[warp][st][jt * 8 + 2 * t4 + 1];
+            }
+            float p[NB8][4];
 #pragma unroll
             for (int rr = 0; rr < 2; ++rr) {
                 const int q = g + rr * 8;
-                float v[4];
-                v[0] = ((mk[0] >> q) & 1) ? s[0][rr * 2] * sl2 : -INFINITY;
-                v[1] = ((mk[1] >> q) & 1) ? s[0][rr * 2 + 1] * sl2 : -INFINITY;
-                v[2] = ((mk[2] >> q) & 1) ? s[1][rr * 2] * sl2 : -INFINITY;
-                v[3] = ((mk[3] >> q) & 1) ? s[1][rr * 2 + 1] * sl2 : -INFINITY;
-                float mx = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+                float v[NB8][2];
+                float mx = -INFINITY;
+#pragma unroll
+                for (int jt = 0; jt < NB8; ++jt) {
+                    v[jt][0] = ((mk[jt][0] >> q) & 1) ? s[jt][rr * 2] * sl2 : -INFINITY;
+                    v[jt][1] = ((mk[jt][1] >> q) & 1) ? s[jt][rr * 2 + 1] * sl2 : -INFINITY;
+                    mx = fmaxf(mx, fmaxf(v[jt][0], v[jt][1]));
+                }
                 mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 1));
                 mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 2));
                 const float mn = fmaxf(m_r[rr], mx);
-                float alpha = 1.f;
-                if (mn == -INFINITY) {
-                    p[0][rr * 2] = p[0][rr * 2 + 1] = p[1][rr * 2] = p[1][rr * 2 + 1] = 0.f;
-                } else {
-                    alpha = fast_exp2(m_r[rr] - mn);  // exp2(-inf) = 0 for a first key
-                    p[0][rr * 2] = fast_exp2(v[0] - mn);
-                    p[0][rr * 2 + 1] = fast_exp2(v[1] - mn);
-                    p[1][rr * 2] = fast_exp2(v[2] - mn);
-                    p[1][rr * 2 + 1] = fast_exp2(v[3] - mn);
+                float alpha = 1.f, ps = 0.f;
+#pragma unroll
+                for (int jt = 0; jt < NB8; ++jt) {
+                    if (mn == -INFINITY) {
+                        p[jt][rr * 2] = p[jt][rr * 2 + 1] = 0.f;
+                    } else {
+                        p[jt][rr * 2] = fast_exp2(v[jt][0] - mn);
+                        p[jt][rr * 2 + 1] = fast_exp2(v[jt][1] - mn);
+                    }
+                    ps += p[jt][rr * 2] + p[jt][rr * 2 + 1];
                 }
-                l_r[rr] = l_r[rr] * alpha + (p[0][rr * 2] + p[0][rr * 2 + 1] + p[1][rr * 2] + p[1][rr * 2 + 1]);
+                if (mn != -INFINITY) alpha = fast_exp2(m_r[rr] - mn);  // exp2(-inf) = 0 for a first key
+                l_r[rr] = l_r[rr] * alpha + ps;
                 m_r[rr] = mn;
 #pragma unroll
                 for (int n = 0; n < 16; ++n) {
@@ -465,17 +503,22 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
                     o[n][rr * 2 + 1] *= alpha;
                 }
             }
-            // ---- O += P V: A = P (rows g, g+8; keys), B = V via ldmatrix.trans ----
-            const uint32_t pa0 = pack_bf16(p[0][0], p[0][1]), pa1 = pack_bf16(p[0][2], p[0][3]);
-            const uint32_t pa2 = pack_bf16(p[1][0], p[1][1]), pa3 = pack_bf16(p[1][2], p[1][3]);
+            // ---- O += P V: A = P (rows g, g+8; 16 keys per k-step), B = V via ldmatrix.trans ----
 #pragma unroll
-            for (int n2 = 0; n2 < 8; ++n2) {
-                // matrices: (keys 0-7, dims 16n2..+7), (keys 8-15, same), (keys 0-7, +8..), (8-15, +8..)
-                const int mi = lane >> 3, r = (mi & 1) * 8 + (lane & 7), c = n2 * 2 + (mi >> 1);
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(sV + swz(r, c), b0, b1, b2, b3);
-                mma16816(o[2 * n2], pa0, pa1, pa2, pa3, b0, b1);
-                mma16816(o[2 * n2 + 1], pa0, pa1, pa2, pa3, b2, b3);
+            for (int kc = 0; kc < TK / 16; ++kc) {
+                const uint32_t pa0 = pack_bf16(p[2 * kc][0], p[2 * kc][1]);
+                const uint32_t pa1 = pack_bf16(p[2 * kc][2], p[2 * kc][3]);
+                const uint32_t pa2 = pack_bf16(p[2 * kc + 1][0], p[2 * kc + 1][1]);
+                const uint32_t pa3 = pack_bf16(p[2 * kc + 1][2], p[2 * kc + 1][3]);
+#pragma unroll
+                for (int n2 = 0; n2 < 8; ++n2) {
+                    // matrices: (keys 16kc+0-7, dims 16n2..+7), (keys +8-15, same), (0-7, +8..), (8-15, +8..)
+                    const int mi = lane >> 3, r = kc * 16 + (mi & 1) * 8 + (lane & 7), c = n2 * 2 + (mi >> 1);
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_t(sV + swz(r, c), b0, b1, b2, b3);
+                    mma16816(o[2 * n2], pa0, pa1, pa2, pa3, b0, b1);
+                    mma16816(o[2 * n2 + 1], pa0, pa1, pa2, pa3, b2, b3);
+                }
             }
             __syncwarp();  // the stage is refilled by the next issue
         }
