@@ -106,9 +106,16 @@ typedef struct {
 /* Offline: K-means key clustering (section 3.1; section 3.3       */
 /* P:244-247; Fig. 2)                                            */
 /* ---------------------------------------------------------------------- */
+enum { SQZ_KMEANS_AUTO = 0, SQZ_KMEANS_EXACT = 1, SQZ_KMEANS_TENSOR = 2 };
 typedef struct {
-    int32_t max_iters; /* Lloyd iterations per level (e.g. 50)                       */
-    float tol;         /* stop when the max centroid shift < tol (e.g. 1e-4)         */
+    int32_t max_iters;   /* Lloyd iterations per level (e.g. 50)                       */
+    float tol;           /* stop when the max centroid shift < tol (e.g. 1e-4)         */
+    int32_t assign_mode; /* assignment step: SQZ_KMEANS_EXACT = fp32 FFMA scores;       */
+                         /* SQZ_KMEANS_TENSOR = tcgen05 GEMM on split-bf16 operands     */
+                         /* (x_h.mu_h + x_h.mu_l + x_l.mu_h, fp32 accumulation, ~fp32   */
+                         /* FFMA accuracy) with an exact fp32 re-rank of every key     */
+                         /* whose two best scores are within 2e-4; SQZ_KMEANS_AUTO (0) */
+                         /* = TENSOR when keys x clusters >= 2^26 (d = 64 or 128)      */
 } sqz_kmeans_params;
 
 /* Workspace bytes for sqz_cluster_keys with the index geometry in *idx. */

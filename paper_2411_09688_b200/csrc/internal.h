@@ -144,6 +144,29 @@ struct DiagLaunch {
 size_t diag_ws_bytes(int B, int H, int c2, int64_t L);
 cudaError_t launch_diagnostics(const DiagLaunch &a, cudaStream_t st);
 
+// kmeans_tc.cu: tensor-core assignment step of the Lloyd iterations (NEXT-3)
+struct KmeansTcWs {
+    int *amb_n;     // ambiguous-key count
+    float *xx;      // [H, n] ||x^||^2 (sequential FMA)
+    int4 *amb;      // [H * n] (h, key, best, second) of the keys re-ranked exactly
+    void *Xs, *Ms;  // [H, n, 2d], [H, c, 2d] bf16 splits [hi | lo]
+};
+struct KmeansTc {
+    int H, n, c, d;
+    const float *Xh, *mu, *musq;
+    const int *done;
+    int32_t *assign;
+    float *pdist;
+    int *changed;
+    float margin;
+    KmeansTcWs w;
+};
+size_t kmeans_tc_ws_bytes(int H, int64_t n, int64_t c, int d);
+bool kmeans_tc_applies(int mode, int d, int64_t n, int64_t c);
+KmeansTcWs kmeans_tc_carve(void *ws, int H, int64_t n, int d);
+cudaError_t kmeans_tc_split_x(const float *Xh, int H, int n, int d, const KmeansTcWs &w, cudaStream_t st);
+cudaError_t kmeans_tc_assign(const KmeansTc &k, cudaStream_t st);
+
 // kmeans.cu
 struct KmeansWs;
 size_t kmeans_workspace_bytes(const sqz_index &idx);

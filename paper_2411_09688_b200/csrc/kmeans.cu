@@ -422,6 +422,7 @@ struct Ws {
     int32_t *N2old, *parent;
     void *cub;
     size_t cub_b;
+    void *tc;  // tensor-core assignment region (kmeans_tc.cu)
 };
 
 Ws carve(const sqz_index &idx, char *base, size_t *total) {
@@ -454,6 +455,7 @@ Ws carve(const sqz_index &idx, char *base, size_t *total) {
     w.parent = cv.take<int32_t>(H * c);
     w.cub_b = cub_bytes(H * n);
     w.cub = cv.take<char>(w.cub_b);
+    w.tc = cv.take<char>(kmeans_tc_ws_bytes((int)H, n, c, (int)d));
     *total = cv.used + 256;
     return w;
 }
@@ -476,6 +478,17 @@ int lloyd(Ws &w, int H, int n, int c, int d, const int64_t *init, const sqz_kmea
     CK(cudaGetLastError());
     const size_t smem = (size_t)2 * KT * (d + 1) * sizeof(float);
     CK(cudaFuncSetAttribute(k_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // the tensor-core assignment (NEXT-3): split the normalised keys once per run
+    const bool tc = kmeans_tc_applies(p.assign_mode, d, n, c);
+    KmeansTc ktc;
+    if (tc) {
+        ktc.H = H; ktc.n = n; ktc.c = c; ktc.d = d;
+        ktc.Xh = w.Xh; ktc.mu = w.mu; ktc.musq = w.musq; ktc.done = w.done;
+        ktc.assign = w.assign; ktc.pdist = w.pdist; ktc.changed = w.changed;
+        ktc.margin = 2e-4f;
+        ktc.w = kmeans_tc_carve(w.tc, H, n, d);
+        CK(kmeans_tc_split_x(w.Xh, H, n, d, ktc.w, st));
+    }
     std::vector<int32_t> changed(H), done(H, 0);
     std::vector<unsigned> shift(H);
     *iters = 0;
@@ -485,8 +498,11 @@ int lloyd(Ws &w, int H, int n, int c, int d, const int64_t *init, const sqz_kmea
         CK(cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * (size_t)H * c, st));
         CK(cudaMemsetAsync(w.sums, 0, sizeof(unsigned long long) * (size_t)H * c * d, st));
         k_musq<<<dim3((c + 7) / 8, H), 256, 0, st>>>(w.mu, c, d, w.done, w.musq);
-        k_assign<<<dim3((n + KT - 1) / KT, H), 256, smem, st>>>(w.Xh, n, c, d, w.mu, w.musq, w.done,
-                                                               w.assign, w.pdist, w.changed);
+        if (tc)
+            CK(kmeans_tc_assign(ktc, st));
+        else
+            k_assign<<<dim3((n + KT - 1) / KT, H), 256, smem, st>>>(w.Xh, n, c, d, w.mu, w.musq, w.done,
+                                                                   w.assign, w.pdist, w.changed);
         k_counts<<<dim3(std::min(1024, (n + 255) / 256), H), 256, 0, st>>>(w.assign, n, c, w.done,
                                                                           w.counts);
         k_repair<<<H, 1024, 0, st>>>(w.assign, w.pdist, n, c, w.done, w.counts, w.changed);

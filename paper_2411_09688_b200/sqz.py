@@ -55,7 +55,10 @@ class sqz_shard_plan(ctypes.Structure):
 
 
 class sqz_kmeans_params(ctypes.Structure):
-    _fields_ = [("max_iters", ctypes.c_int32), ("tol", ctypes.c_float)]
+    _fields_ = [("max_iters", ctypes.c_int32), ("tol", ctypes.c_float), ("assign_mode", ctypes.c_int32)]
+
+
+KMEANS_AUTO, KMEANS_EXACT, KMEANS_TENSOR = 0, 1, 2
 
 
 class sqz_lookup_params(ctypes.Structure):
@@ -233,8 +236,11 @@ class Index:
 
 
 def cluster_keys(K: torch.Tensor, V: torch.Tensor, c2: int, init2: torch.Tensor, c1: int = 0,
-                 init1: torch.Tensor = None, max_iters: int = 50, tol: float = 1e-4):
-    """sqz_cluster_keys: returns (Index, Kp, Vp, (iters_level2, iters_level1))."""
+                 init1: torch.Tensor = None, max_iters: int = 50, tol: float = 1e-4,
+                 assign_mode: int = KMEANS_AUTO):
+    """sqz_cluster_keys: returns (Index, Kp, Vp, (iters_level2, iters_level1)).
+    assign_mode: KMEANS_EXACT (fp32 FFMA scores), KMEANS_TENSOR (split-bf16
+    tcgen05 GEMM + exact re-rank of near ties) or KMEANS_AUTO."""
     H, L, d = K.shape
     idx = Index.empty(H, d, L, c2, c1, sqz_dtype(K), K.device)
     s = idx.struct()
@@ -244,7 +250,7 @@ def cluster_keys(K: torch.Tensor, V: torch.Tensor, c2: int, init2: torch.Tensor,
     Kp = torch.empty_like(K)
     Vp = torch.empty_like(V)
     it = (ctypes.c_int32 * 2)()
-    p = sqz_kmeans_params(max_iters, tol)
+    p = sqz_kmeans_params(max_iters, tol, assign_mode)
     i2 = init2.to(device=K.device, dtype=torch.int64).contiguous()
     i1 = None if init1 is None else init1.to(device=K.device, dtype=torch.int64).contiguous()
     _check(lib().sqz_cluster_keys(_p(K), _p(V), _p(i2), _p(i1), ctypes.byref(s), _p(Kp), _p(Vp),

@@ -137,3 +137,88 @@ def test_empty_cluster_repair_matches_oracle(dtype, iters):
     if iters == 1:
         # head 0: cluster 1 (the empty duplicate) took the farthest outlier, point L - 2
         assert r.N2[0, 1] == 1 and r.perm[0, r.key_off[0, 1]] == L - 2
+
+
+def _assign_of(g, H, L):
+    """Cluster id of every ORIGINAL key, from the cluster-major tables."""
+    perm, ko = _np(g.perm), _np(g.key_off)
+    a = np.zeros((H, L), np.int64)
+    for h in range(H):
+        a[h, perm[h]] = np.repeat(np.arange(ko.shape[1] - 1), np.diff(ko[h]))
+    return a
+
+
+def _build_mode(fc, c2, init2, iters, mode, c1=0, init1=None):
+    from paper_2411_09688_b200 import sqz
+
+    K, V = sqz.to_device(fc.K), sqz.to_device(fc.V)
+    idx, Kp, Vp, its = sqz.cluster_keys(K, V, c2, torch.from_numpy(init2).cuda(), c1,
+                                        None if init1 is None else torch.from_numpy(init1).cuda(),
+                                        max_iters=iters, assign_mode=mode)
+    torch.cuda.synchronize()
+    sqz.index_validate(idx)
+    return idx, Kp, Vp
+
+
+@pytest.mark.parametrize("levels", [1, 2])
+def test_tensor_core_assignment_separated_identical_to_oracle(levels):
+    """NEXT-3: the tcgen05 split-bf16 assignment reproduces the oracle's partitions
+    and tables bit for bit on the separated mixture (same shared init)."""
+    from paper_2411_09688_b200 import sqz
+
+    H, L, d, G = 2, 3000, 128, 16
+    c1 = 4 if levels == 2 else 0
+    fc = synth.fixed_context(H, L, d, G, dtype=synth.BF16, seed=41, sep=True, G1=c1)
+    init2 = np.stack([[np.nonzero(fc.labels[h] == g)[0][0] for g in range(G)] for h in range(H)])
+    init1 = np.stack([np.arange(c1) for _ in range(H)]).astype(np.int64) if c1 else None
+    g, Kp, _ = _build_mode(fc, G, init2.astype(np.int64), 50, sqz.KMEANS_TENSOR, c1, init1)
+    r = oracle.build_index(fc.K, G, init2, c1, init1)
+    assert np.array_equal(_np(g.perm), r.perm) and np.array_equal(_np(g.key_off), r.key_off)
+    assert np.array_equal(_np(g.C2), oracle.encode(r.C2, synth.BF16))
+    if levels == 2:
+        assert np.array_equal(_np(g.child_off), r.child_off)
+        assert np.array_equal(_np(g.C1), oracle.encode(r.C1, synth.BF16))
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_tensor_core_assignment_matches_exact_on_generic_data(d):
+    """One Lloyd assignment from the same init, tensor-core vs exact fp32 path:
+    every key gets a centroid whose fp64 distance is within 1e-5 (relative) of the
+    minimum over all centroids, and at most a handful of near-tie keys differ."""
+    from paper_2411_09688_b200 import sqz
+
+    H, L, c2 = 2, 9000, 300
+    fc = synth.fixed_context(H, L, d, c2, dtype=synth.BF16, seed=46)
+    init2 = synth.kmeans_init(H, L, c2, seed=47)
+    gt, _, _ = _build_mode(fc, c2, init2, 1, sqz.KMEANS_TENSOR)
+    ge, _, _ = _build_mode(fc, c2, init2, 1, sqz.KMEANS_EXACT)
+    at, ae = _assign_of(gt, H, L), _assign_of(ge, H, L)
+    X = oracle.to_f64(fc.K)
+    X = X / np.linalg.norm(X, axis=2, keepdims=True)
+    diff = 0
+    for h in range(H):
+        mu = X[h][init2[h]]  # the first assignment is against the initial points
+        D2 = ((X[h][:, None, :] - mu[None]) ** 2).sum(-1)
+        dmin = D2.min(1)
+        got = D2[np.arange(L), at[h]]
+        assert np.all(got <= dmin * (1 + 1e-5) + 1e-6)
+        diff += int((at[h] != ae[h]).sum())
+    assert diff <= 0.001 * H * L, diff
+
+
+def test_tensor_core_generic_invariants():
+    """Full runs in tensor-core mode keep every index invariant and are bit-reproducible."""
+    from paper_2411_09688_b200 import sqz
+
+    H, L, d, c2, c1 = 2, 6000, 128, 240, 40
+    fc = synth.fixed_context(H, L, d, c2, dtype=synth.BF16, seed=48, G1=c1)
+    init2 = synth.kmeans_init(H, L, c2, seed=49)
+    init1 = synth.kmeans_init(H, c2, c1, seed=50)
+    g, Kp, _ = _build_mode(fc, c2, init2, 15, sqz.KMEANS_TENSOR, c1, init1)
+    g2, _, _ = _build_mode(fc, c2, init2, 15, sqz.KMEANS_TENSOR, c1, init1)
+    for f in ("C2", "N2", "key_off", "perm", "C1", "N1", "child_off"):
+        assert torch.equal(getattr(g, f), getattr(g2, f)), f
+    perm, N2 = _np(g.perm), _np(g.N2)
+    for h in range(H):
+        assert N2[h].min() >= 1 and N2[h].sum() == L
+    assert np.array_equal(_np(Kp), np.stack([fc.K[h][perm[h]] for h in range(H)]))
