@@ -431,7 +431,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
                  if c1 else None)
         del fc
     t0 = time.time()
-    idx, Kp, Vp, iters = sqz.cluster_keys(K, V, c2, init2, c1, init1, max_iters=kiters)
+    idx, Kp, Vp, iters = sqz.cluster_keys(K, V, c2, init2, c1, init1, max_iters=kiters,
+                                          assign_mode={"auto": sqz.KMEANS_AUTO, "exact": sqz.KMEANS_EXACT,
+                                                       "tensor": sqz.KMEANS_TENSOR}[args.kmeans_mode])
     torch.cuda.synchronize()
     t_index = time.time() - t0
     # host copy of the sampled head (original order) for the oracle parity check
@@ -801,6 +803,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    "mean_union_keys_per_step": allsum(ku_mean),
                    "attention_path": "batch-shared union pass" if shared_attn else "per-(b,h) streams",
                    "retention_realized": k_glob / (B * H * L), "kmeans_iters": list(iters),
+                   "kmeans_mode": args.kmeans_mode,
                    "index_build_s": round(t_index, 2)},
         "phases_ms": {"lookup": round(t_look, 5), "sparse_attention": round(t_attn, 5),
                       "phases_of": "the two-call path (sqz_centroid_lookup, sqz_sparse_attention), "
@@ -843,6 +846,9 @@ def main():
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the rank-0 sampled oracle parity check after the timed region")
     ap.add_argument("--kmeans-iters", type=int, default=30)
+    ap.add_argument("--kmeans-mode", default="auto", choices=["auto", "exact", "tensor"],
+                    help="K-means assignment step: fp32 FFMA (exact), tcgen05 split-bf16 (tensor), "
+                         "or tensor for large problems (auto)")
     ap.add_argument("--kmeans-iters-set", type=int, default=None,
                     help="override the per-config Lloyd iteration count (cfg5: 3)")
     ap.add_argument("--retention", type=float, default=None,
