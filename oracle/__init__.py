@@ -71,6 +71,10 @@ def lib():
         L.sqzref_attention.argtypes = [c_int, c_int, c_int, c_int, c_i64, c_int, dp, dp, dp, u8p,
                                        dp, dp, c_int, c_int, ip, c_d, dp, dp]
         L.sqzref_merge.argtypes = [c_int, c_i64, c_int, dp, dp, dp, dp]
+        vpp = ctypes.POINTER(ctypes.c_void_p)
+        L.sqzref_lookup_ml.restype = c_int
+        L.sqzref_lookup_ml.argtypes = [c_int, c_int, c_int, c_int, dp, c_int, ip, vpp, vpp, vpp, c_d,
+                                       dp, vpp, vpp, vpp, dp]
         L.sqzref_diagnostics.restype = c_int
         L.sqzref_diagnostics.argtypes = [c_int, c_int, c_int, c_i64, dp, dp, u8p, c_d, c_i64, c_d,
                                          dp, dp, dp, dp, i64p, i64p, dp]
@@ -180,9 +184,13 @@ class Index:
     child_off: np.ndarray = None  # [H,c1+1]
     assign2: np.ndarray = None    # [H,L] new level-2 id of every original key
     iters: list = field(default_factory=list)
+    c0: int = 0                   # three levels: Level 0 above Level 1
+    C0: np.ndarray = None         # [H,c0,d]
+    N0: np.ndarray = None         # [H,c0] descendant keys (R4)
+    child_off0: np.ndarray = None  # [H,c0+1] Level-1 children of each Level-0 cluster
 
 
-def build_index(K_stored, c2, init2, c1=0, init1=None, max_iters=50, tol=1e-4):
+def build_index(K_stored, c2, init2, c1=0, init1=None, max_iters=50, tol=1e-4, c0=0, init0=None):
     """Offline clustering of the fixed-context keys of every head.
 
     Level 2 = K-means(keys, c2); Level 1 = K-means(Level-2 centroids, c1)
@@ -190,32 +198,59 @@ def build_index(K_stored, c2, init2, c1=0, init1=None, max_iters=50, tol=1e-4):
     procedure").  C^(1) = unweighted mean of the child
     C^(2) rows (R5); N^(1) = descendant keys (R4).  Centroids are rounded once
     to the storage dtype (R18).  Keys are then ordered cluster-major (Level-2
-    grouped by parent, keys by Level-2 cluster, both stable)."""
+    grouped by parent, keys by Level-2 cluster, both stable).
+    c0 > 0: a third level ("extended to multiple levels"): Level 0 =
+    K-means(Level-1 centroids, c0) by the same procedure, C^(0) = unweighted mean
+    of the child C^(1) rows, N^(0) = descendant keys; Level-1 ids are then grouped
+    by their Level-0 parent (stable in K-means id) before the Level-2 ids are
+    grouped by their (renumbered) Level-1 parent."""
     dt = dtype_of(K_stored)
     K = to_f64(K_stored)
     H, L, d = K.shape
-    levels = 2 if c1 > 0 else 1
+    levels = 3 if c0 > 0 else (2 if c1 > 0 else 1)
+    if c0 > 0 and c1 <= 0:
+        raise ValueError("three levels need c1 > 0")
+    C0 = np.zeros((H, c0, d)) if levels == 3 else None
+    N0 = np.zeros((H, c0), np.int32) if levels == 3 else None
+    child_off0 = np.zeros((H, c0 + 1), np.int32) if levels == 3 else None
     C2o = np.zeros((H, c2, d))
     N2o = np.zeros((H, c2), np.int32)
     key_off = np.zeros((H, c2 + 1), np.int32)
     perm = np.zeros((H, L), np.int32)
     assign_new = np.zeros((H, L), np.int32)
-    C1 = np.zeros((H, c1, d)) if levels == 2 else None
-    N1 = np.zeros((H, c1), np.int32) if levels == 2 else None
-    child_off = np.zeros((H, c1 + 1), np.int32) if levels == 2 else None
+    C1 = np.zeros((H, c1, d)) if levels >= 2 else None
+    N1 = np.zeros((H, c1), np.int32) if levels >= 2 else None
+    child_off = np.zeros((H, c1 + 1), np.int32) if levels >= 2 else None
     iters = []
     for h in range(H):
         a2, _, it2, _ = kmeans(K[h], c2, init2[h], max_iters, tol)
         C2, N2 = cluster_means(K[h], a2, c2)
         C2 = round_to(C2, dt)
         parent = None
-        it1 = 0
-        if levels == 2:
+        it1 = it0 = 0
+        if levels >= 2:
             parent, _, it1, _ = kmeans(C2, c1, init1[h], max_iters, tol)
             C1h, _ = cluster_means(C2, parent, c1)
-            C1[h] = round_to(C1h, dt)
+            C1h = round_to(C1h, dt)
+            N1h = np.zeros(c1, np.int32)
             for o in range(c2):
-                N1[h, parent[o]] += N2[o]
+                N1h[parent[o]] += N2[o]
+            if levels == 3:
+                # Level 0 on the stored Level-1 rows; Level-1 ids grouped by parent
+                parent0, _, it0, _ = kmeans(C1h, c0, init0[h], max_iters, tol)
+                C0h, _ = cluster_means(C1h, parent0, c0)
+                C0[h] = round_to(C0h, dt)
+                l1_order = [p for g in range(c0) for p in range(c1) if parent0[p] == g]
+                new1 = np.empty(c1, np.int32)
+                new1[l1_order] = np.arange(c1, dtype=np.int32)
+                for g in range(c0):
+                    child_off0[h, g + 1] = child_off0[h, g] + int((parent0 == g).sum())
+                    N0[h, g] = int(N1h[parent0 == g].sum())
+                C1h = C1h[l1_order]
+                N1h = N1h[l1_order]
+                parent = new1[parent]
+            C1[h] = C1h
+            N1[h] = N1h
         l2_order = np.zeros(c2, np.int32)
         coff = np.zeros(c1 + 1, np.int32)
         rc = lib().sqzref_build_order(
@@ -225,17 +260,17 @@ def build_index(K_stored, c2, init2, c1=0, init1=None, max_iters=50, tol=1e-4):
             _p(key_off[h], ctypes.c_int32), _p(coff, ctypes.c_int32))
         if rc != 0:
             raise ValueError(f"sqzref_build_order: error {rc}")
-        if levels == 2:
+        if levels >= 2:
             child_off[h] = coff
         C2o[h] = C2[l2_order]
         N2o[h] = N2[l2_order]
         new_of_old = np.empty(c2, np.int32)
         new_of_old[l2_order] = np.arange(c2, dtype=np.int32)
         assign_new[h] = new_of_old[a2]
-        iters.append((it2, it1))
+        iters.append((it2, it1, it0) if levels == 3 else (it2, it1))
     return Index(levels=levels, dtype=dt, H=H, L=L, d=d, c2=c2, C2=C2o, N2=N2o, key_off=key_off,
                  perm=perm, c1=c1, C1=C1, N1=N1, child_off=child_off, assign2=assign_new,
-                 iters=iters)
+                 iters=iters, c0=c0, C0=C0, N0=N0, child_off0=child_off0)
 
 
 def permute_kv(X_stored, idx: Index):
@@ -274,8 +309,52 @@ def select_singlepass(s, N, T):
     return sel.astype(bool)
 
 
-def lookup(Q, idx: Index, scale, T, T1=0.0, forced_l1=None):
+def lookup_ml(Q, idx: Index, scale, T, T1=0.0, T0=0.0, forced_l1=None, forced_l0=None):
+    """Multi-level lookup for a three-level index: Level 0 (all rows,
+    Eq. 2) -> Level 1 over the survivors' children (Eq. 3) -> Level 2 likewise.
+    Returns sel2/Sbar2, surv1/Sbar1, surv0/Sbar0, lse as lookup() does."""
+    Q = _f64(Q)
+    B, H, n_q, d = Q.shape
+    Lv = idx.levels
+    tabs = ([(idx.C0, idx.N0, idx.child_off0, idx.c0)] if Lv == 3 else []) + \
+        ([(idx.C1, idx.N1, idx.child_off, idx.c1)] if Lv >= 2 else []) + [(idx.C2, idx.N2, None, idx.c2)]
+    keep = []
+    c = np.array([t[3] for t in tabs], np.int32)
+    Cs = [_f64(t[0]) for t in tabs]
+    Ns = [_i32(t[1]) for t in tabs]
+    Os = [None if t[2] is None else _i32(t[2]) for t in tabs]
+    Ts = np.array(([T0] if Lv == 3 else []) + ([T1] if Lv >= 2 else []) + [T], np.float64)
+    forced = ([forced_l0] if Lv == 3 else []) + ([forced_l1] if Lv >= 2 else []) + [None]
+    forced = [None if f is None else np.ascontiguousarray(f, dtype=np.uint8) for f in forced]
+    surv = [np.zeros((B, H, ci), np.uint8) for ci in c]
+    Sbar = [np.zeros((B, H, ci)) for ci in c]
+    lse = np.zeros((B, H, n_q))
+    keep += Cs + Ns + Os + forced + surv + Sbar
+
+    def ptrs(arrs):
+        a = (ctypes.c_void_p * len(arrs))(*[None if x is None else x.ctypes.data for x in arrs])
+        keep.append(a)
+        return ctypes.cast(a, ctypes.POINTER(ctypes.c_void_p))
+
+    rc = lib().sqzref_lookup_ml(B, H, n_q, d, _p(Q, ctypes.c_double), Lv, _p(c, ctypes.c_int32),
+                                ptrs(Cs), ptrs(Ns), ptrs(Os), scale, _p(Ts, ctypes.c_double),
+                                ptrs(forced), ptrs(surv), ptrs(Sbar), _p(lse, ctypes.c_double))
+    if rc != 0:
+        raise ValueError(f"sqzref_lookup_ml: error {rc}")
+    out = dict(sel2=surv[-1].astype(bool), Sbar2=Sbar[-1], lse=lse)
+    if Lv >= 2:
+        out["surv1"] = surv[-2].astype(bool)
+        out["Sbar1"] = Sbar[-2]
+    if Lv == 3:
+        out["surv0"] = surv[0].astype(bool)
+        out["Sbar0"] = Sbar[0]
+    return out
+
+
+def lookup(Q, idx: Index, scale, T, T1=0.0, forced_l1=None, T0=0.0, forced_l0=None):
     """Centroid lookup for Q[B,H,n_q,d] (decode: n_q = 1; prefill: averaged)."""
+    if idx.levels == 3:
+        return lookup_ml(Q, idx, scale, T, T1, T0, forced_l1, forced_l0)
     Q = _f64(Q)
     B, H, n_q, d = Q.shape
     c1, c2 = idx.c1, idx.c2

@@ -353,6 +353,79 @@ int sqzref_lookup(int B, int H, int n_q, int d, const double *Q,
     return SQZREF_OK;
 }
 
+/* Multi-level lookup (section 3.3: "this method can be extended to multiple
+ * levels of hierarchy"; complexity O(c' log L + k)).
+ * Lv levels, 0 = coarsest ... Lv-1 = finest (the key clusters).  Level l has
+ * the table C[l] [H, c[l], d] and N[l] [H, c[l]] (descendant keys, R4); for
+ * l < Lv-1, child_off[l] [H, c[l]+1] gives the contiguous level-(l+1) children
+ * of each cluster.  Level 0 scores all its rows with Eq. 2; level l > 0 scores
+ * the children of the level-(l-1) survivors with the denominator restricted to
+ * them (Eq. 3 applied level by level).  Scores are averaged over the n_q queries
+ * of a (b,h) (R7), survivors are S_bar > T[l] (strict; T[l] = 0 keeps all, R6);
+ * forced[l] (optional [B,H,c[l]]) replaces the decision at level l < Lv-1 (the
+ * conditional-parity rule).  Outputs per level: surv[l] [B,H,c[l]], Sbar[l]
+ * [B,H,c[l]] (NaN for rows not scanned); lse [B,H,n_q] of the finest level. */
+int sqzref_lookup_ml(int B, int H, int n_q, int d, const double *Q, int Lv, const int32_t *c,
+                     const double *const *C, const int32_t *const *N,
+                     const int32_t *const *child_off, double scale, const double *T,
+                     const uint8_t *const *forced, uint8_t *const *surv, double *const *Sbar,
+                     double *lse)
+{
+    if (B < 1 || H < 1 || n_q < 1 || d < 1 || Lv < 1) return SQZREF_ERR_INVALID;
+    int cmax = 1;
+    for (int l = 0; l < Lv; ++l) {
+        if (c[l] < 1 || !(T[l] >= 0.0)) return SQZREF_ERR_INVALID;
+        if (c[l] > cmax) cmax = c[l];
+    }
+#pragma omp parallel for schedule(dynamic)
+    for (int bh = 0; bh < B * H; ++bh) {
+        int h = bh % H;
+        const double *Qbh = Q + (size_t)bh * n_q * d;
+        double *s = (double *)malloc(sizeof(double) * (size_t)cmax);
+        double *S = (double *)malloc(sizeof(double) * (size_t)cmax);
+        int32_t *rows = (int32_t *)malloc(sizeof(int32_t) * (size_t)cmax);
+        int32_t *next = (int32_t *)malloc(sizeof(int32_t) * (size_t)cmax);
+        int n_rows = c[0];
+        for (int r = 0; r < n_rows; ++r) rows[r] = r;
+        for (int l = 0; l < Lv; ++l) {
+            const double *Ch = C[l] + (size_t)h * c[l] * d;
+            const int32_t *Nh = N[l] + (size_t)h * c[l];
+            double *Sb = Sbar[l] + (size_t)bh * c[l];
+            uint8_t *sv = surv[l] + (size_t)bh * c[l];
+            for (int i = 0; i < c[l]; ++i) { Sb[i] = NAN; sv[i] = 0; }
+            if (n_rows == 0) {
+                if (l == Lv - 1 && lse) for (int t = 0; t < n_q; ++t) lse[(size_t)bh * n_q + t] = -INFINITY;
+                continue;
+            }
+            for (int r = 0; r < n_rows; ++r) Sb[rows[r]] = 0.0;
+            for (int t = 0; t < n_q; ++t) {
+                double l_t;
+                sqzref_scores(Qbh + (size_t)t * d, Ch, Nh, d, c[l], n_rows, rows, scale, s, S, &l_t);
+                for (int r = 0; r < n_rows; ++r) Sb[rows[r]] += S[rows[r]];
+                if (l == Lv - 1 && lse) lse[(size_t)bh * n_q + t] = l_t;
+            }
+            for (int r = 0; r < n_rows; ++r) {
+                int i = rows[r];
+                Sb[i] /= (double)n_q;
+                if (l < Lv - 1 && forced && forced[l]) sv[i] = forced[l][(size_t)bh * c[l] + i] ? 1 : 0;
+                else sv[i] = (T[l] == 0.0) ? 1 : (Sb[i] > T[l]);
+            }
+            if (l < Lv - 1) {
+                /* expand the survivors, in increasing id, to their children */
+                const int32_t *co = child_off[l] + (size_t)h * (c[l] + 1);
+                int nn = 0;
+                for (int i = 0; i < c[l]; ++i)
+                    if (sv[i])
+                        for (int ch = co[i]; ch < co[i + 1]; ++ch) next[nn++] = ch;
+                for (int r = 0; r < nn; ++r) rows[r] = next[r];
+                n_rows = nn;
+            }
+        }
+        free(s); free(S); free(rows); free(next);
+    }
+    return SQZREF_OK;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Exact attention over the selected fixed keys plus the user KV            */
 /* (section 4.2; separate fixed / user caches P:312; R8).        */

@@ -34,6 +34,12 @@ int sqzref_lookup(int B, int H, int n_q, int d, const double *Q,
                   double scale, double T, double T1, const uint8_t *forced_l1,
                   uint8_t *sel2, double *Sbar2, uint8_t *surv1, double *Sbar1, double *lse);
 
+int sqzref_lookup_ml(int B, int H, int n_q, int d, const double *Q, int Lv, const int32_t *c,
+                     const double *const *C, const int32_t *const *N,
+                     const int32_t *const *child_off, double scale, const double *T,
+                     const uint8_t *const *forced, uint8_t *const *surv, double *const *Sbar,
+                     double *lse);
+
 int sqzref_attention(int B, int H, int n_q, int d, int64_t L, int n_u,
                      const double *Q, const double *K, const double *V, const uint8_t *keymask,
                      const double *Ku, const double *Vu, int causal, int n_q_total,

@@ -112,3 +112,114 @@ def test_brute_force_enumeration_16_keys(ref):
         assert list(out["surv1"][0, 0].astype(int)) == expect
         cand = np.repeat(np.array(expect, bool), 2)
         assert np.array_equal(out["sel2"][0, 0], cand)  # T = 0: every candidate selected
+
+
+# ---- three levels ("extended to multiple levels"; NEXT-2) ----
+
+def _three_level(rng, H, c0, per1, per2, d, nmax=20):
+    idx = _hier_index(rng, H, c0 * per1, per2, d, nmax)
+    c1 = idx.c1
+    idx.levels = 3
+    idx.c0 = c0
+    idx.child_off0 = np.tile(np.arange(0, c1 + 1, per1, dtype=np.int32), (H, 1))
+    idx.C0 = np.stack([idx.C1[:, g * per1:(g + 1) * per1].mean(axis=1) for g in range(c0)], axis=1)
+    idx.N0 = idx.N1.reshape(H, c0, per1).sum(axis=2).astype(np.int32)
+    return idx
+
+
+def _two_level_of(idx):
+    return oracle.Index(levels=2, dtype=idx.dtype, H=idx.H, L=idx.L, d=idx.d, c2=idx.c2,
+                        C2=idx.C2, N2=idx.N2, key_off=idx.key_off, perm=None, c1=idx.c1,
+                        C1=idx.C1, N1=idx.N1, child_off=idx.child_off)
+
+
+def test_three_levels_T0_zero_reduces_to_two_levels(ref):
+    """T0 = 0 keeps every Level-0 cluster, so the Level-1 candidates are all Level-1 rows
+    and the restricted denominator is the full Eq. 2 one: the three-level lookup equals the
+    (pinned) two-level lookup; T0 = T1 = 0 equals single level."""
+    rng = np.random.default_rng(20)
+    for trial in range(60):
+        c0, per1, per2 = int(rng.integers(1, 5)), int(rng.integers(1, 5)), int(rng.integers(1, 5))
+        d = int(rng.choice([4, 16, 64]))
+        idx = _three_level(rng, 2, c0, per1, per2, d)
+        Q = rng.standard_normal((2, 2, int(rng.integers(1, 4)), d)) * 2
+        T, T1 = float(rng.uniform(1e-4, 5e-2)), float(rng.uniform(0, 5e-2))
+        three = ref.lookup(Q, idx, 1.0 / np.sqrt(d), T, T1=T1, T0=0.0)
+        two = ref.lookup(Q, _two_level_of(idx), 1.0 / np.sqrt(d), T, T1=T1)
+        assert np.array_equal(three["sel2"], two["sel2"])
+        assert np.array_equal(three["surv1"], two["surv1"])
+        np.testing.assert_allclose(three["Sbar1"], two["Sbar1"], rtol=1e-12)
+        np.testing.assert_allclose(three["Sbar2"], two["Sbar2"], rtol=1e-12)
+        np.testing.assert_allclose(three["lse"], two["lse"], rtol=1e-13)
+        assert three["surv0"].all()
+        single = oracle.Index(levels=1, dtype=idx.dtype, H=idx.H, L=idx.L, d=d, c2=idx.c2,
+                              C2=idx.C2, N2=idx.N2, key_off=idx.key_off, perm=None)
+        a = ref.lookup(Q, idx, 1.0 / np.sqrt(d), T, T1=0.0, T0=0.0)
+        s = ref.lookup(Q, single, 1.0 / np.sqrt(d), T)
+        assert np.array_equal(a["sel2"], s["sel2"])
+
+
+def test_three_levels_ancestry_and_restricted_sums(ref):
+    """Every selected Level-2 cluster has a surviving parent and grandparent; each level's
+    restricted Eq. 3 scores satisfy sum N S = 1 over its candidates; unscanned rows are NaN."""
+    rng = np.random.default_rng(21)
+    idx = _three_level(rng, 3, 4, 3, 5, 32)
+    Q = rng.standard_normal((2, 3, 1, 32)) * 3
+    out = ref.lookup(Q, idx, 1 / np.sqrt(32), 1e-3, T1=3e-3, T0=2e-3)
+    p2 = np.repeat(np.arange(idx.c1), 5)
+    p1 = np.repeat(np.arange(idx.c0), 3)
+    for b in range(2):
+        for h in range(3):
+            sel = np.nonzero(out["sel2"][b, h])[0]
+            assert np.all(out["surv1"][b, h][p2[sel]]) and np.all(out["surv0"][b, h][p1[p2[sel]]])
+            s1 = np.nonzero(out["surv1"][b, h])[0]
+            assert np.all(out["surv0"][b, h][p1[s1]])
+            for S, N in ((out["Sbar1"][b, h], idx.N1[h]), (out["Sbar2"][b, h], idx.N2[h])):
+                m = ~np.isnan(S)
+                if m.any():
+                    assert np.sum(N[m] * S[m]) == pytest.approx(1.0, rel=1e-12)
+            assert np.all(np.isnan(out["Sbar1"][b, h][~out["surv0"][b, h][p1]]))
+
+
+def test_three_levels_all_pruned_and_forced(ref):
+    """All Level-0 clusters pruned -> empty selection; forcing the natural survivor sets
+    reproduces the natural run."""
+    rng = np.random.default_rng(22)
+    idx = _three_level(rng, 1, 3, 2, 3, 8)
+    Q = rng.standard_normal((1, 1, 1, 8))
+    out = ref.lookup(Q, idx, 1.0, 1e-3, T1=1e-3, T0=1.0)  # S^(0) <= 1/N^(0) < 1
+    assert not out["surv0"].any() and not out["surv1"].any() and not out["sel2"].any()
+    assert np.all(np.isneginf(out["lse"]))
+    idx = _three_level(rng, 2, 4, 3, 3, 16)
+    Q = rng.standard_normal((1, 2, 2, 16)) * 2
+    nat = ref.lookup(Q, idx, 0.25, 1e-3, T1=5e-3, T0=1e-2)
+    f = ref.lookup(Q, idx, 0.25, 1e-3, T1=5e-3, T0=1e-2, forced_l0=nat["surv0"], forced_l1=nat["surv1"])
+    assert np.array_equal(nat["sel2"], f["sel2"])
+
+
+def test_three_level_index_build_invariants():
+    """build_index with c0 > 0: Level-1 ids grouped by their Level-0 parent, N0 = descendant
+    keys, C0 = the (rounded) mean of its Level-1 rows, and the Level-2 / key order still
+    grouped by parent; c0 = 1 puts every Level-1 cluster under one parent."""
+    from paper_2411_09688_b200 import synth
+
+    fc = synth.fixed_context(2, 3000, 32, 90, dtype=synth.F32, seed=23, G1=18)
+    i2 = synth.kmeans_init(2, 3000, 90, seed=24)
+    i1 = synth.kmeans_init(2, 90, 18, seed=25)
+    for c0 in (1, 5):
+        i0 = synth.kmeans_init(2, 18, c0, seed=26)
+        idx = oracle.build_index(fc.K, 90, i2, 18, i1, c0=c0, init0=i0)
+        assert idx.levels == 3
+        for h in range(2):
+            co0, co = idx.child_off0[h], idx.child_off[h]
+            assert co0[0] == 0 and co0[-1] == 18 and np.all(np.diff(co0) >= 1)
+            for g in range(c0):
+                kids = np.arange(co0[g], co0[g + 1])
+                assert idx.N0[h, g] == idx.N1[h, kids].sum()
+                np.testing.assert_allclose(idx.C0[h, g], oracle.round_to(idx.C1[h, kids].mean(0), oracle.F32),
+                                           rtol=1e-6, atol=1e-7)
+            for p in range(18):
+                assert idx.N1[h, p] == idx.N2[h, co[p]:co[p + 1]].sum()
+            assert idx.N0[h].sum() == 3000 and np.array_equal(np.sort(idx.perm[h]), np.arange(3000))
+        if c0 == 1:
+            assert np.array_equal(idx.child_off0, np.tile([0, 18], (2, 1)))
