@@ -75,7 +75,8 @@ typedef enum { SQZ_F32 = 0, SQZ_BF16 = 1 } sqz_dtype;
  *   C1         [H, c1, d]   dtype             Level-1 centroids (levels == 2)
  *   N1         [H, c1]      int32             descendant keys of each Level-1 cluster (R4)
  *   child_off  [H, c1 + 1]  int32             Level-2 children ranges (levels == 2)
- * Single level: levels = 1, c1 = 0, C1/N1/child_off = NULL.
+ * Single level: levels = 1, c1 = 0, C1/N1/child_off = NULL.  Three levels
+ * (levels = 3) add Level 0 above Level 1 (fields c0, C0, N0, child_off0).
  *
  * Fixed-context shards (cluster sharding across GPUs): a shard
  * index (sqz_shard_plan + sqz_index_shard) holds a subset of the clusters of
@@ -88,7 +89,7 @@ typedef struct {
     int32_t H;       /* heads                                  */
     int32_t d;       /* head dimension: 64 or 128              */
     int64_t L;       /* fixed-context keys per head            */
-    int32_t levels;  /* 1 or 2                                 */
+    int32_t levels;  /* 1, 2 or 3                              */
     int32_t c1;      /* Level-1 clusters (0 when levels == 1)  */
     int32_t c2;      /* Level-2 / single-level clusters        */
     int32_t dtype;   /* sqz_dtype of C1, C2 (and of K, V, Q)   */
@@ -100,6 +101,13 @@ typedef struct {
     int32_t *key_off;
     int32_t *perm;
     int64_t L_total; /* 0: unsharded; else global keys per head (see above) */
+    /* levels == 3 ("extended to multiple levels"): Level 0 above Level 1,
+     * its children contiguous Level-1 ids (Level-1 ids are grouped by parent):
+     *   C0 [H, c0, d] dtype, N0 [H, c0] descendant keys, child_off0 [H, c0 + 1] */
+    int32_t c0;
+    void *C0;
+    int32_t *N0;
+    int32_t *child_off0;
 } sqz_index;
 
 /* ---------------------------------------------------------------------- */
@@ -116,6 +124,8 @@ typedef struct {
                          /* FFMA accuracy) with an exact fp32 re-rank of every key     */
                          /* whose two best scores are within 2e-4; SQZ_KMEANS_AUTO (0) */
                          /* = TENSOR when keys x clusters >= 2^26 (d = 64 or 128)      */
+    const int64_t *init0; /* levels == 3: [H, c0] device, the seeded initial subset  */
+                          /* of the Level-1 centroids (K-means id order) for Level 0 */
 } sqz_kmeans_params;
 
 /* Workspace bytes for sqz_cluster_keys with the index geometry in *idx. */
@@ -131,14 +141,17 @@ int sqz_cluster_keys_workspace(const sqz_index *idx, size_t *ws_bytes);
  *          every table pointer must point to caller-allocated device memory of
  *          the shape above; all tables are written.
  *   Kp, Vp [H, L, d] dtype outputs (cluster-major copies)
- *   iters_out optional HOST int32[2]: max Lloyd iterations over heads used by
- *          Level 2 and Level 1.
+ *   iters_out optional HOST int32[2] (int32[3] when levels == 3): max Lloyd
+ *          iterations over heads used by Level 2, Level 1 (and Level 0).
  * Algorithm: Lloyd on unit-normalised keys (assignment argmin ||x^ - mu||^2,
  * ties to the lowest id; farthest-point repair of empty clusters; update =
  * mean of member x^), then C_i = mean of the RAW member keys rounded once to
  * dtype; Level 1 clusters the stored C2 rows, C1 = unweighted mean of child
- * rows, N1 = descendant keys.  This is the only call that synchronises the
- * stream (once per Lloyd iteration, to test convergence). */
+ * rows, N1 = descendant keys; levels == 3: Level 0 clusters the stored C1 rows
+ * (init p->init0) the same way, and the Level-1 ids are renumbered grouped by
+ * their Level-0 parent (stable) before the Level-2 ids are grouped by Level-1
+ * parent.  This is the only call that synchronises the stream (once per Lloyd
+ * iteration, to test convergence). */
 int sqz_cluster_keys(const void *K, const void *V, const int64_t *init2, const int64_t *init1,
                      sqz_index *idx, void *Kp, void *Vp, const sqz_kmeans_params *p, void *ws,
                      size_t ws_bytes, int32_t *iters_out, void *stream);
@@ -166,6 +179,7 @@ typedef struct {
                  /* / Eq. 3 denominator and selects exactly the clusters the        */
                  /* unsharded lookup selects among its own (the workspace must then */
                  /* be sized by sqz_lookup_workspace_comm).                         */
+    float T0;    /* Level-0 threshold (levels == 3), T0 >= 0                        */
 } sqz_lookup_params;
 
 /* Outputs of the lookup, caller-allocated device memory.
@@ -197,6 +211,8 @@ typedef struct {
     float *dbg_S1;
     float *dbg_lse;
     int32_t *key_pref;
+    uint8_t *l0_surv; /* optional [B, H, c0] Level-0 survivors (levels == 3) */
+    float *dbg_S0;    /* optional [B, H, c0] Level-0 S^(0) / S-bar^(0)       */
 } sqz_selection;
 
 int sqz_lookup_workspace(const sqz_index *idx, int32_t B, int32_t n_q, size_t *ws_bytes);
@@ -209,7 +225,11 @@ int sqz_lookup_workspace(const sqz_index *idx, int32_t B, int32_t n_q, size_t *w
  * (1/n_q) sum_t S_{t,i}, selected iff S-bar_i > T, one selection per (b,h)
  * shared by its n_q queries (R7).  levels == 2: Level-1 scores with N1 against
  * T1, survivors expanded to their children, Level-2 scores with the
- * denominator restricted to those children (Eq. 3), against T. */
+ * denominator restricted to those children (Eq. 3), against T.
+ * levels == 3: Level 0 (N0, T0) first, then Level 1 restricted to the
+ * children of the Level-0 survivors (Eq. 3 one level up), then Level 2 as
+ * above (O(c' log L + k)).  Sharded (p->comm) and staged
+ * lookups support levels 1 and 2. */
 int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t n_q,
                         const sqz_lookup_params *p, const sqz_selection *out, void *ws,
                         size_t ws_bytes, void *stream);

@@ -57,15 +57,19 @@ int check_index(const sqz_index *idx, bool need_tables) {
         return fail(SQZ_ERR_UNSUPPORTED, "idx->d = %d: head dimension must be 64 or 128", idx->d);
     if (idx->L < 1 || idx->L > 0x7fffffffLL)
         return fail(SQZ_ERR_INVALID_ARG, "idx->L = %lld out of range [1, 2^31)", (long long)idx->L);
-    if (idx->levels != 1 && idx->levels != 2)
-        return fail(SQZ_ERR_INVALID_ARG, "idx->levels = %d must be 1 or 2", idx->levels);
+    if (idx->levels < 1 || idx->levels > 3)
+        return fail(SQZ_ERR_INVALID_ARG, "idx->levels = %d must be 1, 2 or 3", idx->levels);
     if (idx->dtype != SQZ_F32 && idx->dtype != SQZ_BF16)
         return fail(SQZ_ERR_INVALID_ARG, "idx->dtype = %d is not a sqz_dtype", idx->dtype);
     if (idx->c2 < 1 || (int64_t)idx->c2 > idx->L)
         return fail(SQZ_ERR_INVALID_ARG, "idx->c2 = %d must be in [1, L=%lld]", idx->c2,
                     (long long)idx->L);
-    if (idx->levels == 2 && (idx->c1 < 1 || idx->c1 > idx->c2))
+    if (idx->levels >= 2 && (idx->c1 < 1 || idx->c1 > idx->c2))
         return fail(SQZ_ERR_INVALID_ARG, "idx->c1 = %d must be in [1, c2=%d]", idx->c1, idx->c2);
+    if (idx->levels == 3 && (idx->c0 < 1 || idx->c0 > idx->c1))
+        return fail(SQZ_ERR_INVALID_ARG, "idx->c0 = %d must be in [1, c1=%d]", idx->c0, idx->c1);
+    if (idx->levels == 3 && idx->L_total != 0)
+        return fail(SQZ_ERR_UNSUPPORTED, "three-level indexes cannot be sharded");
     if (idx->L_total < 0 || idx->L_total > 0x7fffffffLL)
         return fail(SQZ_ERR_INVALID_ARG, "idx->L_total = %lld out of range [0, 2^31)",
                     (long long)idx->L_total);
@@ -73,10 +77,15 @@ int check_index(const sqz_index *idx, bool need_tables) {
         if (!idx->C2 || !idx->N2 || !idx->key_off)
             return fail(SQZ_ERR_INVALID_ARG, "idx->C2 / N2 / key_off must be non-NULL");
         if (!aligned16(idx->C2)) return fail(SQZ_ERR_INVALID_ARG, "idx->C2 must be 16-byte aligned");
-        if (idx->levels == 2) {
+        if (idx->levels >= 2) {
             if (!idx->C1 || !idx->N1 || !idx->child_off)
-                return fail(SQZ_ERR_INVALID_ARG, "idx->C1 / N1 / child_off must be non-NULL (levels=2)");
+                return fail(SQZ_ERR_INVALID_ARG, "idx->C1 / N1 / child_off must be non-NULL (levels>=2)");
             if (!aligned16(idx->C1)) return fail(SQZ_ERR_INVALID_ARG, "idx->C1 must be 16-byte aligned");
+        }
+        if (idx->levels == 3) {
+            if (!idx->C0 || !idx->N0 || !idx->child_off0)
+                return fail(SQZ_ERR_INVALID_ARG, "idx->C0 / N0 / child_off0 must be non-NULL (levels=3)");
+            if (!aligned16(idx->C0)) return fail(SQZ_ERR_INVALID_ARG, "idx->C0 must be 16-byte aligned");
         }
     }
     return SQZ_OK;
@@ -84,7 +93,7 @@ int check_index(const sqz_index *idx, bool need_tables) {
 
 // ---------------- lookup workspace ----------------
 struct LookupWs {
-    LevelArgs l1, l2;
+    LevelArgs l0, l1, l2;  // l0: levels == 3 only
     float2 *send, *recv;  // comm mode: this rank's statistics, the gathered [world] ones
     size_t bytes;
 };
@@ -96,6 +105,7 @@ LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base, int worl
     const int nqt = (n_q + lookup_qtile() - 1) / lookup_qtile();
     const bool prefill = n_q > 1;
     LookupWs w;
+    std::memset(&w.l0, 0, sizeof(w.l0));
     std::memset(&w.l1, 0, sizeof(w.l1));
     std::memset(&w.l2, 0, sizeof(w.l2));
     auto level = [&](LevelArgs &lv, int c) {
@@ -112,12 +122,19 @@ LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base, int worl
         }
     };
     level(w.l2, idx->c2);
-    if (idx->levels == 2) {
+    if (idx->levels >= 2) {
         level(w.l1, idx->c1);
         w.l1.list = cv.take<int32_t>(BH * idx->c1);
         w.l1.n_list = cv.take<int32_t>(BH);
         w.l1.exp_list = cv.take<int32_t>(BH * idx->c2);
         w.l1.n_exp = cv.take<int32_t>(BH);
+    }
+    if (idx->levels == 3) {
+        level(w.l0, idx->c0);
+        w.l0.list = cv.take<int32_t>(BH * idx->c0);
+        w.l0.n_list = cv.take<int32_t>(BH);
+        w.l0.exp_list = cv.take<int32_t>(BH * idx->c1);
+        w.l0.n_exp = cv.take<int32_t>(BH);
     }
     w.send = w.recv = nullptr;
     if (world > 0) {
@@ -206,7 +223,9 @@ int sqz_cluster_keys(const void *K, const void *V, const int64_t *init2, const i
     if (idx->L_total != 0)
         return fail(SQZ_ERR_INVALID_ARG, "sqz_cluster_keys builds a full index: L_total must be 0");
     if (!init2) return fail(SQZ_ERR_INVALID_ARG, "init2 is NULL");
-    if (idx->levels == 2 && !init1) return fail(SQZ_ERR_INVALID_ARG, "init1 is NULL (levels=2)");
+    if (idx->levels >= 2 && !init1) return fail(SQZ_ERR_INVALID_ARG, "init1 is NULL (levels>=2)");
+    if (idx->levels == 3 && (!p || !p->init0))
+        return fail(SQZ_ERR_INVALID_ARG, "p->init0 is NULL (levels=3)");
     if (!idx->perm) return fail(SQZ_ERR_INVALID_ARG, "idx->perm is NULL");
     if (!p || p->max_iters < 1 || !(p->tol >= 0.f))
         return fail(SQZ_ERR_INVALID_ARG, "kmeans params: max_iters >= 1 and tol >= 0 required");
@@ -256,8 +275,12 @@ static int lookup_check(const sqz_index *idx, const void *Q, int32_t B, int32_t 
     if (!p) return fail(SQZ_ERR_INVALID_ARG, "params is NULL");
     if (!(p->T >= 0.f) || std::isinf(p->T))
         return fail(SQZ_ERR_INVALID_ARG, "T = %g must be finite and >= 0", (double)p->T);
-    if (idx->levels == 2 && (!(p->T1 >= 0.f) || std::isinf(p->T1)))
+    if (idx->levels >= 2 && (!(p->T1 >= 0.f) || std::isinf(p->T1)))
         return fail(SQZ_ERR_INVALID_ARG, "T1 = %g must be finite and >= 0", (double)p->T1);
+    if (idx->levels == 3 && (!(p->T0 >= 0.f) || std::isinf(p->T0)))
+        return fail(SQZ_ERR_INVALID_ARG, "T0 = %g must be finite and >= 0", (double)p->T0);
+    if (idx->levels == 3 && p->comm)
+        return fail(SQZ_ERR_UNSUPPORTED, "sharded lookup of a three-level index");
     if (!std::isfinite(p->scale)) return fail(SQZ_ERR_INVALID_ARG, "scale must be finite");
     if (!out || !out->clusters || !out->n_clusters || !out->n_keys || !out->key_pref)
         return fail(SQZ_ERR_INVALID_ARG, "selection outputs clusters/n_clusters/n_keys/key_pref required");
@@ -282,7 +305,7 @@ static void lookup_levels(const sqz_index *idx, const sqz_lookup_params *p, cons
     l2.exp_stride = idx->L;
     l2.dbg_S = out->dbg_S;
     l2.dbg_lse = out->dbg_lse;
-    if (idx->levels == 2) {
+    if (idx->levels >= 2) {
         LevelArgs &l1 = w.l1;
         l1.C = idx->C1;
         l1.N = idx->N1;
@@ -295,6 +318,20 @@ static void lookup_levels(const sqz_index *idx, const sqz_lookup_params *p, cons
         l2.rows = l1.exp_list;
         l2.n_rows = l1.n_exp;
         l2.row_stride = idx->c2;
+    }
+    if (idx->levels == 3) {
+        LevelArgs &l0 = w.l0;
+        l0.C = idx->C0;
+        l0.N = idx->N0;
+        l0.off = idx->child_off0;
+        l0.c = idx->c0;
+        l0.T = p->T0;
+        l0.exp_stride = idx->c1;
+        l0.bitmap = out->l0_surv;
+        l0.dbg_S = out->dbg_S0;
+        w.l1.rows = l0.exp_list;
+        w.l1.n_rows = l0.n_exp;
+        w.l1.row_stride = idx->c1;
     }
 }
 
@@ -377,7 +414,11 @@ int sqz_centroid_lookup(const sqz_index *idx, const void *Q, int32_t B, int32_t 
         w.l2.rl_n = w.l1.n_list;
         w.l2.rl_c = idx->c1;
     }
-    if (idx->levels == 2) {
+    if (idx->levels == 3) {
+        cudaError_t e = launch_lookup_level(s, Q, w.l0, st);
+        if (e != cudaSuccess) return cuda_fail(e, "lookup level 0");
+    }
+    if (idx->levels >= 2) {
         cudaError_t e = launch_lookup_level(s, Q, w.l1, st);
         if (e != cudaSuccess) return cuda_fail(e, "lookup level 1");
     }
@@ -392,6 +433,7 @@ int sqz_centroid_lookup_stage(const sqz_index *idx, const void *Q, int32_t B, in
                               void *ws, size_t ws_bytes, void *stream) {
     int rc = lookup_check(idx, Q, B, n_q, p, out, ws);
     if (rc) return rc;
+    if (idx->levels == 3) return fail(SQZ_ERR_UNSUPPORTED, "staged lookup of a three-level index");
     if (stage < 0 || stage > idx->levels)
         return fail(SQZ_ERR_INVALID_ARG, "stage = %d must be in [0, levels=%d]", stage, idx->levels);
     if (stage > 0 && (P < 1 || !stats_in))

@@ -389,6 +389,13 @@ __global__ void k_parent_weights(const int32_t *__restrict__ parent, const int32
         atomicAdd(N1 + (size_t)h * c1 + parent[(size_t)h * c2 + o], N2[(size_t)h * c2 + o]);
 }
 
+// lab[h, j] <- map[h, lab[h, j]] (labels renumbered)
+__global__ void k_remap(int32_t *__restrict__ lab, const int32_t *__restrict__ map, int n, int m) {
+    const int h = blockIdx.y;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        lab[(size_t)h * n + j] = map[(size_t)h * m + lab[(size_t)h * n + j]];
+}
+
 // --------------------------------------------------------------------------
 // host orchestration
 // --------------------------------------------------------------------------
@@ -423,6 +430,9 @@ struct Ws {
     void *cub;
     size_t cub_b;
     void *tc;  // tensor-core assignment region (kmeans_tc.cu)
+    // levels == 3: Level-1 tables in K-means id order, Level-0 labels and order
+    void *C1old;
+    int32_t *N1old, *coff1, *parent0, *order1, *inv1;
 };
 
 Ws carve(const sqz_index &idx, char *base, size_t *total) {
@@ -456,6 +466,13 @@ Ws carve(const sqz_index &idx, char *base, size_t *total) {
     w.cub_b = cub_bytes(H * n);
     w.cub = cv.take<char>(w.cub_b);
     w.tc = cv.take<char>(kmeans_tc_ws_bytes((int)H, n, c, (int)d));
+    const int64_t c1 = idx.levels == 3 ? idx.c1 : 0;
+    w.C1old = cv.take<char>(H * c1 * d * esz);
+    w.N1old = cv.take<int32_t>(H * c1);
+    w.coff1 = cv.take<int32_t>(H * (c1 + 1));
+    w.parent0 = cv.take<int32_t>(H * c1);
+    w.order1 = cv.take<int32_t>(H * c1);
+    w.inv1 = cv.take<int32_t>(H * c1);
     *total = cv.used + 256;
     return w;
 }
@@ -579,7 +596,8 @@ int cluster_keys_t(const T *K, const T *V, const int64_t *init2, const int64_t *
                                                                      C2old, w.N2old);
     CK(cudaGetLastError());
 
-    if (idx->levels == 2) {
+    int32_t it0 = 0;
+    if (idx->levels >= 2) {
         // ---- Level 1: K-means on the stored Level-2 centroids (R5) ----
         k_normalize<T><<<dim3((unsigned)((H * c2 + wpb - 1) / wpb)), 256, 0, st>>>(
             C2old, (int64_t)H * c2, d, w.Xh);
@@ -587,6 +605,51 @@ int cluster_keys_t(const T *K, const T *V, const int64_t *init2, const int64_t *
         if (rc) return rc;
         CK(cudaMemcpyAsync(w.parent, w.assign, sizeof(int32_t) * (size_t)H * c2,
                            cudaMemcpyDeviceToDevice, st));
+    }
+    if (idx->levels == 3) {
+        // ---- Level 0: the Level-1 tables in K-means id order first ----
+        const int c0 = idx->c0;
+        T *C1old = reinterpret_cast<T *>(w.C1old);
+        rc = sort_by_label(w, w.parent, nullptr, H, c2, c1, 0, w.order, st, err, errlen);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(w.done, 0, sizeof(int32_t) * H, st));
+        CK(cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * (size_t)H * c1, st));
+        k_counts<<<dim3((c2 + 255) / 256, H), 256, 0, st>>>(w.parent, c2, c1, w.done, w.counts);
+        k_exscan<<<H, 1024, 0, st>>>(w.counts, c1, w.coff1);
+        k_segment_means<T><<<dim3((c1 + wpb - 1) / wpb, H), 256, 0, st>>>(C2old, c2, w.order, w.coff1, c1,
+                                                                         d, C1old, nullptr);
+        CK(cudaMemsetAsync(w.N1old, 0, sizeof(int32_t) * (size_t)H * c1, st));
+        k_parent_weights<<<dim3((c2 + 255) / 256, H), 256, 0, st>>>(w.parent, w.N2old, c2, c1, w.N1old);
+        CK(cudaGetLastError());
+        // K-means on the stored Level-1 rows -> Level-0 labels
+        k_normalize<T><<<dim3((unsigned)((H * c1 + wpb - 1) / wpb)), 256, 0, st>>>(
+            C1old, (int64_t)H * c1, d, w.Xh);
+        rc = lloyd(w, H, c1, c0, d, p.init0, p, &it0, st, err, errlen);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(w.parent0, w.assign, sizeof(int32_t) * (size_t)H * c1,
+                           cudaMemcpyDeviceToDevice, st));
+        // Level-1 ids grouped by Level-0 parent, stable in K-means id: order1[new] = old
+        rc = sort_by_label(w, w.parent0, nullptr, H, c1, c0, 0, w.order1, st, err, errlen);
+        if (rc) return rc;
+        k_invert<<<dim3((c1 + 255) / 256, H), 256, 0, st>>>(w.order1, c1, w.inv1);
+        CK(cudaMemsetAsync(w.done, 0, sizeof(int32_t) * H, st));
+        CK(cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * (size_t)H * c0, st));
+        k_counts<<<dim3((c1 + 255) / 256, H), 256, 0, st>>>(w.parent0, c1, c0, w.done, w.counts);
+        k_exscan<<<H, 1024, 0, st>>>(w.counts, c0, idx->child_off0);
+        // C0 = unweighted mean of the child Level-1 rows (R5 one level up), N0 = descendant keys
+        k_segment_means<T><<<dim3((c0 + wpb - 1) / wpb, H), 256, 0, st>>>(
+            C1old, c1, w.order1, idx->child_off0, c0, d, (T *)idx->C0, nullptr);
+        CK(cudaMemsetAsync(idx->N0, 0, sizeof(int32_t) * (size_t)H * c0, st));
+        k_parent_weights<<<dim3((c1 + 255) / 256, H), 256, 0, st>>>(w.parent0, w.N1old, c1, c0, idx->N0);
+        // Level-1 tables in the new order; Level-2 parents renumbered
+        k_gather_rows<T><<<dim3(std::max(1, std::min(4096, (c1 * d + 255) / 256)), H), 256, 0, st>>>(
+            C1old, w.order1, c1, d, (T *)idx->C1);
+        k_gather_rows<int32_t><<<dim3(std::max(1, (c1 + 255) / 256), H), 256, 0, st>>>(w.N1old, w.order1,
+                                                                                     c1, 1, idx->N1);
+        k_remap<<<dim3((c2 + 255) / 256, H), 256, 0, st>>>(w.parent, w.inv1, c2, c1);
+        CK(cudaGetLastError());
+    }
+    if (idx->levels >= 2) {
         // Level-2 clusters grouped by parent, stable in old id: order[new] = old
         rc = sort_by_label(w, w.parent, nullptr, H, c2, c1, 0, w.order, st, err, errlen);
         if (rc) return rc;
@@ -595,12 +658,14 @@ int cluster_keys_t(const T *K, const T *V, const int64_t *init2, const int64_t *
         CK(cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * (size_t)H * c1, st));
         k_counts<<<dim3((c2 + 255) / 256, H), 256, 0, st>>>(w.parent, c2, c1, w.done, w.counts);
         k_exscan<<<H, 1024, 0, st>>>(w.counts, c1, idx->child_off);
-        // C1 = unweighted mean of the child rows, summed in increasing old id
-        k_segment_means<T><<<dim3((c1 + wpb - 1) / wpb, H), 256, 0, st>>>(
-            C2old, c2, w.order, idx->child_off, c1, d, (T *)idx->C1, nullptr);
-        CK(cudaMemsetAsync(idx->N1, 0, sizeof(int32_t) * (size_t)H * c1, st));
-        k_parent_weights<<<dim3((c2 + 255) / 256, H), 256, 0, st>>>(w.parent, w.N2old, c2, c1,
-                                                                    idx->N1);
+        if (idx->levels == 2) {
+            // C1 = unweighted mean of the child rows, summed in increasing old id
+            k_segment_means<T><<<dim3((c1 + wpb - 1) / wpb, H), 256, 0, st>>>(
+                C2old, c2, w.order, idx->child_off, c1, d, (T *)idx->C1, nullptr);
+            CK(cudaMemsetAsync(idx->N1, 0, sizeof(int32_t) * (size_t)H * c1, st));
+            k_parent_weights<<<dim3((c2 + 255) / 256, H), 256, 0, st>>>(w.parent, w.N2old, c2, c1,
+                                                                        idx->N1);
+        }
         CK(cudaGetLastError());
     } else {
         k_iota<<<dim3((c2 + 255) / 256, H), 256, 0, st>>>(c2, w.order, w.inv);
@@ -622,7 +687,11 @@ int cluster_keys_t(const T *K, const T *V, const int64_t *init2, const int64_t *
     k_gather_kv<<<gg, 256, 0, st>>>((const uint4 *)V, idx->perm, L, vpr, (uint4 *)Vp);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
-    if (iters_out) { iters_out[0] = it2; iters_out[1] = it1; }
+    if (iters_out) {
+        iters_out[0] = it2;
+        iters_out[1] = it1;
+        if (idx->levels == 3) iters_out[2] = it0;
+    }
     return SQZ_OK;
 }
 }  // namespace
@@ -674,7 +743,21 @@ __global__ void k_validate(sqz_index idx, int32_t *__restrict__ hist, int *__res
         if (v < 0 || v >= Lt) atomicOr(bad, 2);
         else atomicAdd(hist + (size_t)h * Lt + v, 1);
     }
-    if (idx.levels == 2) {
+    if (idx.levels == 3) {  // Level 0 over Level 1: contiguous, non-empty, N0 = descendant keys
+        const int c0 = idx.c0, c1 = idx.c1;
+        const int32_t *co = idx.child_off0 + (size_t)h * (c0 + 1);
+        const int32_t *N0 = idx.N0 + (size_t)h * c0;
+        const int32_t *N1 = idx.N1 + (size_t)h * c1;
+        for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < c0; g += gridDim.x * blockDim.x) {
+            if (co[g + 1] <= co[g] || co[g] < 0 || co[g + 1] > c1) { atomicOr(bad, 16); continue; }
+            if (g == 0 && co[0] != 0) atomicOr(bad, 16);
+            if (g == c0 - 1 && co[c0] != c1) atomicOr(bad, 16);
+            long long t = 0;
+            for (int p = co[g]; p < co[g + 1]; ++p) t += N1[p];
+            if (t != N0[g]) atomicOr(bad, 16);
+        }
+    }
+    if (idx.levels >= 2) {
         const int c1 = idx.c1;
         const int32_t *co = idx.child_off + (size_t)h * (c1 + 1);
         const int32_t *N1 = idx.N1 + (size_t)h * c1;
@@ -721,8 +804,9 @@ int index_validate(const sqz_index &idx, void *ws, size_t ws_bytes, cudaStream_t
     CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (hb) {
-        snprintf(err, errlen, "index invariant violated:%s%s%s%s", (hb & 1) ? " key_off/N2" : "",
-                 (hb & 2) ? " perm" : "", (hb & 4) ? " child_off" : "", (hb & 8) ? " N1" : "");
+        snprintf(err, errlen, "index invariant violated:%s%s%s%s%s", (hb & 1) ? " key_off/N2" : "",
+                 (hb & 2) ? " perm" : "", (hb & 4) ? " child_off" : "", (hb & 8) ? " N1" : "",
+                 (hb & 16) ? " child_off0/N0" : "");
         return SQZ_ERR_INVARIANT;
     }
     return SQZ_OK;

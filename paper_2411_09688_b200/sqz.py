@@ -45,7 +45,8 @@ class sqz_index(ctypes.Structure):
                 ("dtype", ctypes.c_int32), ("C1", ctypes.c_void_p), ("N1", ctypes.c_void_p),
                 ("child_off", ctypes.c_void_p), ("C2", ctypes.c_void_p), ("N2", ctypes.c_void_p),
                 ("key_off", ctypes.c_void_p), ("perm", ctypes.c_void_p),
-                ("L_total", ctypes.c_int64)]
+                ("L_total", ctypes.c_int64), ("c0", ctypes.c_int32), ("C0", ctypes.c_void_p),
+                ("N0", ctypes.c_void_p), ("child_off0", ctypes.c_void_p)]
 
 
 class sqz_shard_plan(ctypes.Structure):
@@ -55,7 +56,8 @@ class sqz_shard_plan(ctypes.Structure):
 
 
 class sqz_kmeans_params(ctypes.Structure):
-    _fields_ = [("max_iters", ctypes.c_int32), ("tol", ctypes.c_float), ("assign_mode", ctypes.c_int32)]
+    _fields_ = [("max_iters", ctypes.c_int32), ("tol", ctypes.c_float), ("assign_mode", ctypes.c_int32),
+                ("init0", ctypes.c_void_p)]
 
 
 KMEANS_AUTO, KMEANS_EXACT, KMEANS_TENSOR = 0, 1, 2
@@ -63,13 +65,13 @@ KMEANS_AUTO, KMEANS_EXACT, KMEANS_TENSOR = 0, 1, 2
 
 class sqz_lookup_params(ctypes.Structure):
     _fields_ = [("scale", ctypes.c_float), ("T", ctypes.c_float), ("T1", ctypes.c_float),
-                ("comm", ctypes.c_void_p)]
+                ("comm", ctypes.c_void_p), ("T0", ctypes.c_float)]
 
 
 class sqz_selection(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in
                 ("clusters", "n_clusters", "n_keys", "key_idx", "l1_surv", "dbg_S", "dbg_S1",
-                 "dbg_lse", "key_pref")]
+                 "dbg_lse", "key_pref", "l0_surv", "dbg_S0")]
 
 
 class sqz_attn_params(ctypes.Structure):
@@ -207,23 +209,28 @@ class Index:
     L_total: int = 0          # > 0: a fixed-context shard (see shard_index)
     c2_src: torch.Tensor = None  # shard: global Level-2 id of each local row (-1 = padding)
     c1_src: torch.Tensor = None  # shard: global Level-1 id of each local row
+    c0: int = 0                  # three levels: Level 0 above Level 1
+    C0: torch.Tensor = None
+    N0: torch.Tensor = None
+    child_off0: torch.Tensor = None
 
     @property
     def levels(self):
-        return 2 if self.c1 > 0 else 1
+        return 3 if self.c0 > 0 else (2 if self.c1 > 0 else 1)
 
     def struct(self) -> sqz_index:
         s = sqz_index()
         s.H, s.d, s.L, s.levels, s.c1, s.c2, s.dtype = (self.H, self.d, self.L, self.levels,
                                                         self.c1, self.c2, self.dtype)
-        for f in ("C1", "N1", "child_off", "C2", "N2", "key_off", "perm"):
+        for f in ("C1", "N1", "child_off", "C2", "N2", "key_off", "perm", "C0", "N0", "child_off0"):
             t = getattr(self, f)
             setattr(s, f, None if t is None else t.data_ptr())
         s.L_total = self.L_total
+        s.c0 = self.c0
         return s
 
     @staticmethod
-    def empty(H, d, L, c2, c1=0, dtype=SQZ_BF16, device="cuda"):
+    def empty(H, d, L, c2, c1=0, dtype=SQZ_BF16, device="cuda", c0=0):
         td = torch_dtype(dtype)
         i32 = dict(dtype=torch.int32, device=device)
         return Index(H=H, d=d, L=L, c2=c2, dtype=dtype,
@@ -232,30 +239,34 @@ class Index:
                      perm=torch.empty(H, L, **i32), c1=c1,
                      C1=torch.empty(H, c1, d, dtype=td, device=device) if c1 else None,
                      N1=torch.empty(H, c1, **i32) if c1 else None,
-                     child_off=torch.empty(H, c1 + 1, **i32) if c1 else None)
+                     child_off=torch.empty(H, c1 + 1, **i32) if c1 else None, c0=c0,
+                     C0=torch.empty(H, c0, d, dtype=td, device=device) if c0 else None,
+                     N0=torch.empty(H, c0, **i32) if c0 else None,
+                     child_off0=torch.empty(H, c0 + 1, **i32) if c0 else None)
 
 
 def cluster_keys(K: torch.Tensor, V: torch.Tensor, c2: int, init2: torch.Tensor, c1: int = 0,
                  init1: torch.Tensor = None, max_iters: int = 50, tol: float = 1e-4,
-                 assign_mode: int = KMEANS_AUTO):
+                 assign_mode: int = KMEANS_AUTO, c0: int = 0, init0: torch.Tensor = None):
     """sqz_cluster_keys: returns (Index, Kp, Vp, (iters_level2, iters_level1)).
     assign_mode: KMEANS_EXACT (fp32 FFMA scores), KMEANS_TENSOR (split-bf16
     tcgen05 GEMM + exact re-rank of near ties) or KMEANS_AUTO."""
     H, L, d = K.shape
-    idx = Index.empty(H, d, L, c2, c1, sqz_dtype(K), K.device)
+    idx = Index.empty(H, d, L, c2, c1, sqz_dtype(K), K.device, c0=c0)
     s = idx.struct()
     nb = ctypes.c_size_t(0)
     _check(lib().sqz_cluster_keys_workspace(ctypes.byref(s), ctypes.byref(nb)))
     ws = torch.empty(nb.value, dtype=torch.uint8, device=K.device)
     Kp = torch.empty_like(K)
     Vp = torch.empty_like(V)
-    it = (ctypes.c_int32 * 2)()
-    p = sqz_kmeans_params(max_iters, tol, assign_mode)
+    it = (ctypes.c_int32 * 3)()
     i2 = init2.to(device=K.device, dtype=torch.int64).contiguous()
     i1 = None if init1 is None else init1.to(device=K.device, dtype=torch.int64).contiguous()
+    i0 = None if init0 is None else init0.to(device=K.device, dtype=torch.int64).contiguous()
+    p = sqz_kmeans_params(max_iters, tol, assign_mode, None if i0 is None else i0.data_ptr())
     _check(lib().sqz_cluster_keys(_p(K), _p(V), _p(i2), _p(i1), ctypes.byref(s), _p(Kp), _p(Vp),
                                   ctypes.byref(p), _p(ws), nb.value, it, _stream()))
-    return idx, Kp, Vp, (it[0], it[1])
+    return idx, Kp, Vp, ((it[0], it[1], it[2]) if c0 else (it[0], it[1]))
 
 
 def index_validate(idx: Index):
@@ -277,6 +288,8 @@ class Selection:
     dbg_S1: torch.Tensor = None
     dbg_lse: torch.Tensor = None
     key_pref: torch.Tensor = None  # run-length key offsets of the selected clusters
+    l0_surv: torch.Tensor = None   # three levels: Level-0 survivors (debug)
+    dbg_S0: torch.Tensor = None
 
     @staticmethod
     def empty(idx: Index, B, n_q, debug=False, device="cuda", key_idx=True):
@@ -295,7 +308,10 @@ class Selection:
             if (debug and idx.c1) else None,
             dbg_S=torch.empty(B, H, idx.c2, **f32) if debug else None,
             dbg_S1=torch.empty(B, H, idx.c1, **f32) if (debug and idx.c1) else None,
-            dbg_lse=torch.empty(B, H, n_q, **f32) if debug else None)
+            dbg_lse=torch.empty(B, H, n_q, **f32) if debug else None,
+            l0_surv=torch.empty(B, H, idx.c0, dtype=torch.uint8, device=device)
+            if (debug and idx.c0) else None,
+            dbg_S0=torch.empty(B, H, idx.c0, **f32) if (debug and idx.c0) else None)
 
     def struct(self) -> sqz_selection:
         s = sqz_selection()
@@ -340,7 +356,7 @@ def attention_workspace_bytes(idx: Index, B, n_q, n_u):
 
 def centroid_lookup(idx: Index, Q: torch.Tensor, scale: float, T: float, T1: float = 0.0,
                     sel: Selection = None, ws: torch.Tensor = None, debug=False,
-                    comm: "Comm" = None) -> Selection:
+                    comm: "Comm" = None, T0: float = 0.0) -> Selection:
     """sqz_centroid_lookup on Q[B,H,n_q,d].  `comm`: idx is this rank's
     fixed-context shard; the lookup exchanges the per-level statistics."""
     B, H, n_q, d = Q.shape
@@ -355,9 +371,9 @@ def centroid_lookup(idx: Index, Q: torch.Tensor, scale: float, T: float, T1: flo
             _check(lib().sqz_lookup_workspace_comm(ctypes.byref(s), B, n_q, comm.world,
                                                    ctypes.byref(nbc)))
             nb = nbc.value
-        ws = _WS.get(("lookup", Q.device, idx.H, idx.L, idx.c1, idx.c2, B, n_q,
+        ws = _WS.get(("lookup", Q.device, idx.H, idx.L, idx.c0, idx.c1, idx.c2, B, n_q,
                       0 if comm is None else comm.world), nb, Q.device)
-    p = sqz_lookup_params(scale, T, T1, None if comm is None else comm.handle)
+    p = sqz_lookup_params(scale, T, T1, None if comm is None else comm.handle, T0)
     ss = sel.struct()
     _check(lib().sqz_centroid_lookup(ctypes.byref(s), _p(Q), B, n_q, ctypes.byref(p),
                                      ctypes.byref(ss), _p(ws), ws.numel(), _stream()))

@@ -222,3 +222,30 @@ def test_tensor_core_generic_invariants():
     for h in range(H):
         assert N2[h].min() >= 1 and N2[h].sum() == L
     assert np.array_equal(_np(Kp), np.stack([fc.K[h][perm[h]] for h in range(H)]))
+
+
+@pytest.mark.parametrize("dtype", [synth.BF16, synth.F32])
+def test_three_level_index_identical_to_oracle(dtype):
+    """Three levels: on the separated mixture from the shared inits the GPU
+    build equals the oracle's build_index bit for bit (Level-0 tables, the Level-1
+    renumbering, and the Level-2 / key order that follows from it)."""
+    from paper_2411_09688_b200 import sqz
+
+    H, L, d, G, c1, c0 = 2, 4000, 128, 32, 8, 3
+    fc = synth.fixed_context(H, L, d, G, dtype=dtype, seed=51, sep=True, G1=c1)
+    init2 = np.stack([[np.nonzero(fc.labels[h] == g)[0][0] for g in range(G)] for h in range(H)])
+    init1 = np.stack([np.arange(c1) for _ in range(H)]).astype(np.int64)
+    init0 = np.stack([np.arange(c0) for _ in range(H)]).astype(np.int64)
+    g, Kp, Vp, its = sqz.cluster_keys(sqz.to_device(fc.K), sqz.to_device(fc.V), G,
+                                      torch.from_numpy(init2.astype(np.int64)).cuda(), c1,
+                                      torch.from_numpy(init1).cuda(), max_iters=50, c0=c0,
+                                      init0=torch.from_numpy(init0).cuda())
+    torch.cuda.synchronize()
+    sqz.index_validate(g)
+    r = oracle.build_index(fc.K, G, init2, c1, init1, c0=c0, init0=init0)
+    for f in ("N2", "key_off", "perm", "N1", "child_off", "N0", "child_off0"):
+        assert np.array_equal(_np(getattr(g, f)), getattr(r, f)), f
+    for f in ("C2", "C1", "C0"):
+        assert np.array_equal(_np(getattr(g, f)), oracle.encode(getattr(r, f), dtype)), f
+    assert np.array_equal(_np(Kp), oracle.permute_kv(fc.K, r))
+    assert np.array_equal(_np(Vp), oracle.permute_kv(fc.V, r))

@@ -54,18 +54,24 @@ def _calibrate(P, scale, retention, prefill=False, n_cal=24, ret1=0.5):
     return T, T1
 
 
-def _check_lookup(P, sel, scale, T, T1, B):
+def _check_lookup(P, sel, scale, T, T1, B, T0=0.0):
     idx = P["idx"]
     Q64 = oracle.to_f64(P["Q"])
     H = idx.H
-    forced = None
-    if idx.levels == 2:
-        ref1 = oracle.lookup(Q64, idx, scale, T, T1)
+    forced = forced0 = None
+    if idx.levels == 3:  # Level 0, then Level 1 conditioned on the GPU's Level-0 set
+        ref0 = oracle.lookup(Q64, idx, scale, T, T1, T0=T0)
+        g0 = sel.l0_surv.cpu().numpy().astype(bool)
+        assert_selection_parity(g0, ref0["surv0"], ref0["Sbar0"], T0, what="level-0")
+        np.testing.assert_allclose(sel.dbg_S0.cpu().numpy(), ref0["Sbar0"], rtol=2e-5, atol=1e-12)
+        forced0 = g0
+    if idx.levels >= 2:
+        ref1 = oracle.lookup(Q64, idx, scale, T, T1, T0=T0, forced_l0=forced0)
         g1 = sel.l1_surv.cpu().numpy().astype(bool)
         assert_selection_parity(g1, ref1["surv1"], ref1["Sbar1"], T1, what="level-1")
         np.testing.assert_allclose(sel.dbg_S1.cpu().numpy(), ref1["Sbar1"], rtol=2e-5, atol=1e-12)
         forced = g1
-    ref = oracle.lookup(Q64, idx, scale, T, T1, forced_l1=forced)
+    ref = oracle.lookup(Q64, idx, scale, T, T1, forced_l1=forced, T0=T0, forced_l0=forced0)
     g = gpu_sets(sel, B, H, idx.c2)
     ndiff = assert_selection_parity(g, ref["sel2"], ref["Sbar2"], T)
     S_gpu = sel.dbg_S.cpu().numpy()
@@ -388,3 +394,69 @@ def test_invalid_arguments_rejected():
     assert e.value.code == sqz.SQZ_ERR_INVALID_ARG and "T" in str(e.value)
     with pytest.raises(sqz.SqzError):
         sqz.centroid_lookup(t["idx"], t["Q"], 0.125, float("nan"))
+
+
+# ---- three levels (NEXT-2) ----
+THREE_CASES = [
+    # name, H, L, d, c2, c1, c0, dtype, B, n_q, n_u, prefill
+    ("decode_bf16_B3", 3, 6000, 128, 240, 48, 8, synth.BF16, 3, 1, 33, False),
+    ("decode_fp32_d64", 2, 5000, 64, 200, 40, 6, synth.F32, 2, 1, 16, False),
+    ("prefill_bf16_causal", 2, 6000, 128, 240, 48, 8, synth.BF16, 1, 150, 150, True),
+]
+
+
+@pytest.mark.parametrize("case", THREE_CASES, ids=lambda c: c[0])
+def test_three_level_lookup_and_attention(case):
+    """Three-level index built on the GPU, then lookup + attention: every level's
+    decision equals the oracle's (band rule) conditioned on the GPU's coarser sets,
+    and attention over the selection equals the oracle's."""
+    sqz = _sqz()
+    name, H, L, d, c2, c1, c0, dt, B, n_q, n_u, prefill = case
+    seed = zlib.crc32(name.encode()) % 1000
+    fc = synth.fixed_context(H, L, d, c2, dtype=dt, seed=seed, G1=c1)
+    i2 = synth.kmeans_init(H, L, c2, seed=seed + 1)
+    i1 = synth.kmeans_init(H, c2, c1, seed=seed + 2)
+    i0 = synth.kmeans_init(H, c1, c0, seed=seed + 5)
+    gidx, Kp, Vp, its = sqz.cluster_keys(sqz.to_device(fc.K), sqz.to_device(fc.V), c2,
+                                         torch.from_numpy(i2).cuda(), c1, torch.from_numpy(i1).cuda(),
+                                         max_iters=20, c0=c0, init0=torch.from_numpy(i0).cuda())
+    torch.cuda.synchronize()
+    sqz.index_validate(gidx)
+    assert len(its) == 3
+    # the oracle evaluates the GPU-built tables
+    def f64(t):
+        a = t.cpu()
+        return oracle.to_f64(a.view(torch.int16).numpy().view(np.uint16) if a.dtype == torch.bfloat16
+                             else a.numpy())
+    idx = oracle.Index(levels=3, dtype=dt, H=H, L=L, d=d, c2=c2, C2=f64(gidx.C2),
+                       N2=gidx.N2.cpu().numpy(), key_off=gidx.key_off.cpu().numpy(),
+                       perm=gidx.perm.cpu().numpy(), c1=c1, C1=f64(gidx.C1), N1=gidx.N1.cpu().numpy(),
+                       child_off=gidx.child_off.cpu().numpy(), c0=c0, C0=f64(gidx.C0),
+                       N0=gidx.N0.cpu().numpy(), child_off0=gidx.child_off0.cpu().numpy())
+    if prefill:
+        Q = synth.prefill_queries(fc.mix, B, n_q, seed=seed + 3, dtype=dt)
+        Qc = synth.prefill_queries(fc.mix, 2, 64, seed=777, dtype=dt)
+    else:
+        Q = synth.decode_queries(fc.mix, B, seed=seed + 3, dtype=dt)
+        Qc = synth.decode_queries(fc.mix, 24, seed=777, dtype=dt)
+    Ku, Vu = synth.user_kv(fc.mix, B, n_u, seed=seed + 4, dtype=dt)
+    scale = 1.0 / np.sqrt(d)
+    Qc64 = oracle.to_f64(Qc)
+    r = oracle.lookup(Qc64, idx, scale, 0.0, 0.0, T0=0.0)
+    T0 = calib.weighted_threshold(r["Sbar0"], idx.N0[None], 0.6)
+    r = oracle.lookup(Qc64, idx, scale, 0.0, 0.0, T0=T0)
+    T1 = calib.weighted_threshold(r["Sbar1"], idx.N1[None], 0.4,
+                                  total_weight=Qc64.shape[0] * H * L)
+    r = oracle.lookup(Qc64, idx, scale, 0.0, T1, T0=T0)
+    T = calib.weighted_threshold(r["Sbar2"], idx.N2[None], 0.1, total_weight=Qc64.shape[0] * H * L)
+    Qd = sqz.to_device(Q)
+    sel = sqz.centroid_lookup(gidx, Qd, scale, T, T1, debug=True, T0=T0)
+    torch.cuda.synchronize()
+    P = dict(fc=fc, idx=idx, Q=Q, Ku=Ku, Vu=Vu, dtype=dt)
+    assert sel.l0_surv.sum() < B * H * c0  # Level 0 prunes
+    _check_lookup(P, sel, scale, T, T1, B, T0=T0)
+    O, LSE = sqz.sparse_attention(Qd, Kp, Vp, gidx, sel, sqz.to_device(Ku), sqz.to_device(Vu), scale,
+                                  causal=prefill, partial=True)
+    torch.cuda.synchronize()
+    fp32 = dt == synth.F32
+    _check_attention(P, sel, O, LSE, scale, prefill, B, 1e-4 if fp32 else 2e-2, None if fp32 else 5e-3)
