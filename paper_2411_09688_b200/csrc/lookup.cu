@@ -124,8 +124,11 @@ __device__ void finalize_colpart(const LevelArgs &lv, int bh, int h, int nrows, 
     const int32_t *rows = ROWLIST ? lv.rows + (size_t)bh * lv.row_stride : nullptr;
     const bool all = !(lv.T > 0.f);
     PL_FIN(bh, 0);
-    if (lv.dbg_S && ROWLIST)
-        for (int r = tid; r < lv.c; r += nt) lv.dbg_S[(size_t)bh * lv.c + r] = NAN;
+    if (ROWLIST && (lv.dbg_S || lv.bitmap))  // rows outside the candidate list: not scanned
+        for (int r = tid; r < lv.c; r += nt) {
+            if (lv.dbg_S) lv.dbg_S[(size_t)bh * lv.c + r] = NAN;
+            if (lv.bitmap) lv.bitmap[(size_t)bh * lv.c + r] = 0;
+        }
     __syncthreads();
     const float *cp = lv.colpart + (size_t)bh * lv.c;
     const size_t stride = (size_t)BH * lv.c;
@@ -297,16 +300,18 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
     const int r0 = rank * per;
     const int nloc = max(0, min(per, nrows - r0));
     const int32_t *rows = ROWLIST ? lv.rows + ((size_t)b0 * H + h) * lv.row_stride : nullptr;
-    if (ROWLIST && lv.dbg_S) {  // rows outside the candidate list are "not scanned"
+    if (ROWLIST && (lv.dbg_S || lv.bitmap)) {  // rows outside the candidate list: not scanned
         const int per = (c + NC - 1) / NC;
-        for (int r = rank * per + tid; r < min(c, (rank + 1) * per); r += NT)
-            lv.dbg_S[((size_t)b0 * H + h) * c + r] = NAN;
+        for (int r = rank * per + tid; r < min(c, (rank + 1) * per); r += NT) {
+            if (lv.dbg_S) lv.dbg_S[((size_t)b0 * H + h) * c + r] = NAN;
+            if (lv.bitmap) lv.bitmap[((size_t)b0 * H + h) * c + r] = 0;
+        }
     }
 
     const int phase = lv.phase;
     // the staged select (phase 2) has no scan barrier: order this CTA's NaN fill
     // before any peer writes a real score to the same rows (uniform branch)
-    if (ROWLIST && lv.dbg_S && phase == 2) cluster.sync();
+    if (ROWLIST && (lv.dbg_S || lv.bitmap) && phase == 2) cluster.sync();
     if (phase == 2) {
         // ---- staged select: the logits and row metadata phase 1 stored, and the
         // (M, log D) folded over every shard ----
