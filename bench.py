@@ -57,12 +57,18 @@ CONFIGS = {
                           "hierarchical, L1 prunes 50%, retention 10%, B=1, n_u=1024, bf16; fixed context "
                           "sharded by cluster over the GPUs (stats all-gather + (O, LSE) all-gather merge)",
                  mode="decode", H=32, d=128, L=1048576, c2=52429, c1=10486, B=1, n_q=1, n_u=1024,
-                 dtype=1, retention=0.1, cfgno=5, shard="clusters", device_gen=True, kmeans_iters=2),
+                 dtype=1, retention=0.1, cfgno=5, shard="clusters", device_gen=True, kmeans_iters=10),
+    "cfg5h3": dict(workload="cfg5 with THREE levels (P:269): LWM-Text-Chat-1M decode, H=32 d128, "
+                            "L=1048576, c0=2097, c1=10486, c2=52429; Level 0 keeps 50% and Level 1 25% of "
+                            "the keys, retention 10%, B=1, n_u=1024, bf16",
+                   mode="decode", H=32, d=128, L=1048576, c2=52429, c1=10486, c0=2097, B=1, n_q=1,
+                   n_u=1024, dtype=1, retention=0.1, cfgno=5, shard="heads", device_gen=True,
+                   kmeans_iters=10),
     "cfg5p": dict(workload="cfg5 prefill: LWM-Text-Chat-1M, H=32 d128, L=1048576, c1=10486, c2=52429 "
                            "hierarchical, retention 10%, n_q=n_u=4096 causal, bf16; fixed context "
                            "sharded by cluster over the GPUs",
                   mode="prefill", H=32, d=128, L=1048576, c2=52429, c1=10486, B=1, n_q=4096, n_u=4096,
-                  dtype=1, retention=0.1, cfgno=5, shard="clusters", device_gen=True, kmeans_iters=2),
+                  dtype=1, retention=0.1, cfgno=5, shard="clusters", device_gen=True, kmeans_iters=10),
 }
 
 
@@ -149,14 +155,18 @@ def cpu_oracle_run(cfg, steps=None, warmup=0, seconds=12.0, h_sample=4):
     L_full = cfg["L"]
     c2s = int(np.ceil(cfg["c2"] / fL))
     c1s = int(np.ceil(cfg["c1"] / fL)) if cfg["c1"] else 0
-    cfg = dict(cfg, L=Ls, c2=c2s, c1=c1s)
+    c0s = int(np.ceil(cfg.get("c0", 0) / fL)) if cfg.get("c0", 0) else 0
+    cfg = dict(cfg, L=Ls, c2=c2s, c1=c1s, c0=c0s)
     fc = synth.fixed_context(hs, cfg["L"], cfg["d"], cfg["c2"], dtype=cfg["dtype"],
                              seed=1000 + cfg["cfgno"], G1=cfg["c1"])
     K, V = fc.K, fc.V
     init2 = synth.kmeans_init(hs, cfg["L"], cfg["c2"], seed=2000 + cfg["cfgno"])
     init1 = (synth.kmeans_init(hs, cfg["c2"], cfg["c1"], seed=2100 + cfg["cfgno"])
              if cfg["c1"] else None)
-    idx = oracle.build_index(K, cfg["c2"], init2, cfg["c1"], init1, max_iters=10)
+    init0 = (synth.kmeans_init(hs, cfg["c1"], cfg["c0"], seed=2200 + cfg["cfgno"])
+             if cfg["c0"] else None)
+    idx = oracle.build_index(K, cfg["c2"], init2, cfg["c1"], init1, max_iters=10, c0=cfg["c0"],
+                             init0=init0)
     scale = 1.0 / np.sqrt(cfg["d"])
     mix = fc.mix
     if cfg["mode"] == "decode":
@@ -171,12 +181,18 @@ def cpu_oracle_run(cfg, steps=None, warmup=0, seconds=12.0, h_sample=4):
         Ku, Vu = synth.user_kv(mix, 1, cfg["n_u"], seed=5000 + cfg["cfgno"], dtype=cfg["dtype"])
     Ku64, Vu64 = oracle.to_f64(Ku[:, :hs]), oracle.to_f64(Vu[:, :hs])
     K64, V64 = oracle.to_f64(K), oracle.to_f64(V)
-    T1 = 0.0
+    T1 = T0 = 0.0
     Qc64 = oracle.to_f64(Qc)
-    if idx.levels == 2:
+    tw = Qc64.shape[0] * hs * cfg["L"]
+    if idx.levels == 3:
+        r = oracle.lookup(Qc64, idx, scale, 0.0, 0.0)
+        T0 = calib.weighted_threshold(r["Sbar0"], idx.N0[None], 0.5)
+        r = oracle.lookup(Qc64, idx, scale, 0.0, 0.0, T0=T0)
+        T1 = calib.weighted_threshold(r["Sbar1"], idx.N1[None], 0.25, total_weight=tw)
+    elif idx.levels == 2:
         r = oracle.lookup(Qc64, idx, scale, 0.0, 0.0)
         T1 = calib.weighted_threshold(r["Sbar1"], idx.N1[None], 0.5)
-    r = oracle.lookup(Qc64, idx, scale, 0.0, T1)
+    r = oracle.lookup(Qc64, idx, scale, 0.0, T1, T0=T0)
     T = calib.weighted_threshold(r["Sbar2"], idx.N2[None], cfg["retention"],
                                  total_weight=r["Sbar2"].shape[0] * hs * cfg["L"])
     Qt64 = oracle.to_f64(Qt)
@@ -184,12 +200,12 @@ def cpu_oracle_run(cfg, steps=None, warmup=0, seconds=12.0, h_sample=4):
     def step(i):
         if cfg["mode"] == "decode":
             q = Qt64[i % Qt64.shape[0]][None]
-            out = oracle.lookup(q, idx, scale, T, T1)
+            out = oracle.lookup(q, idx, scale, T, T1, T0=T0)
             mask = oracle.keymask(idx, out["sel2"])
             oracle.attention(q, K64, V64, mask, Ku64, Vu64, False, scale)
         else:
             # prefill sample: the full lookup (needs all rows), attention on 64 rows
-            out = oracle.lookup(Qt64, idx, scale, T, T1)
+            out = oracle.lookup(Qt64, idx, scale, T, T1, T0=T0)
             mask = oracle.keymask(idx, out["sel2"])
             rows = np.linspace(0, cfg["n_q"] - 1, 64).astype(np.int32)
             oracle.attention(Qt64[:, :, rows], K64, V64, mask, Ku64, Vu64, True, scale, qpos=rows,
@@ -229,7 +245,7 @@ def cpu_oracle_run(cfg, steps=None, warmup=0, seconds=12.0, h_sample=4):
 
 
 def oracle_parity(sqz, gidx, q, sel, O, LSE, T, T1, scale, K0, V0, Ku0, Vu0, loc, causal,
-                  rows_sample=None):
+                  rows_sample=None, T0=0.0):
     """Rank 0, after the timed region (part of the oracle leg): the fp64 oracle
     re-runs the lookup of head 0 on the GPU-built global tables and the
     attention of that head on the selected keys, and compares them with the GPU
@@ -250,18 +266,28 @@ def oracle_parity(sqz, gidx, q, sel, O, LSE, T, T1, scale, K0, V0, Ku0, Vu0, loc
                        C2=oracle.to_f64(bits(gidx.C2[h:h + 1])), N2=gidx.N2[h:h + 1].cpu().numpy(),
                        key_off=gidx.key_off[h:h + 1].cpu().numpy(),
                        perm=gidx.perm[h:h + 1].cpu().numpy())
-    if gidx.levels == 2:
+    if gidx.levels >= 2:
         sub.c1 = gidx.c1
         sub.C1 = oracle.to_f64(bits(gidx.C1[h:h + 1]))
         sub.N1 = gidx.N1[h:h + 1].cpu().numpy()
         sub.child_off = gidx.child_off[h:h + 1].cpu().numpy()
+    if gidx.levels == 3:
+        sub.c0 = gidx.c0
+        sub.C0 = oracle.to_f64(bits(gidx.C0[h:h + 1]))
+        sub.N0 = gidx.N0[h:h + 1].cpu().numpy()
+        sub.child_off0 = gidx.child_off0[h:h + 1].cpu().numpy()
     B, _, n_q, d = q.shape
     Q64 = oracle.to_f64(bits(q[:, h:h + 1]))
     out = {"head": h, "queries": int(B * n_q)}
     sharded = loc.L_total > 0
-    forced = None
-    if gidx.levels == 2:
-        ref1 = oracle.lookup(Q64, sub, scale, T, T1)
+    forced = forced0 = None
+    if gidx.levels == 3:
+        ref0 = oracle.lookup(Q64, sub, scale, T, T1, T0=T0)
+        g0 = sel.l0_surv[:, h:h + 1].cpu().numpy().astype(bool)
+        out["level0_outside_band"] = int(((g0 != ref0["surv0"]) & ~oracle.band(ref0["Sbar0"], T0)).sum())
+        forced0 = g0
+    if gidx.levels >= 2:
+        ref1 = oracle.lookup(Q64, sub, scale, T, T1, T0=T0, forced_l0=forced0)
         g1 = ref1["surv1"].copy()
         mine = np.arange(gidx.c1) if not sharded else loc.c1_src[h].cpu().numpy()
         gl = sel.l1_surv[:, h].cpu().numpy().astype(bool)[:, :len(mine)]
@@ -270,7 +296,7 @@ def oracle_parity(sqz, gidx, q, sel, O, LSE, T, T1, scale, K0, V0, Ku0, Vu0, loc
         band1 = oracle.band(ref1["Sbar1"], T1)
         out["level1_outside_band"] = int((flips & ~band1).sum())
         forced = g1
-    ref = oracle.lookup(Q64, sub, scale, T, T1, forced_l1=forced)
+    ref = oracle.lookup(Q64, sub, scale, T, T1, forced_l1=forced, T0=T0, forced_l0=forced0)
     cl, n = sel.clusters[:, h].cpu().numpy(), sel.n_clusters[:, h].cpu().numpy()
     src = None if not sharded else loc.c2_src[h].cpu().numpy()
     gsel = np.zeros_like(ref["sel2"])
@@ -320,7 +346,7 @@ def oracle_parity(sqz, gidx, q, sel, O, LSE, T, T1, scale, K0, V0, Ku0, Vu0, loc
 # --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
-def selection_quality(sqz, idx, Qt, Kp, scale, T, T1, n_in, B, dev):
+def selection_quality(sqz, idx, Qt, Kp, scale, T, T1, n_in, B, dev, T0=0.0):
     """sqz_selection_diagnostics over the first n_in test inputs: App. A's top-1%
     cumulative attention score per (b,h) and App. D's ideal lookup at
     the same T against the centroid selection at matched budget."""
@@ -329,7 +355,7 @@ def selection_quality(sqz, idx, Qt, Kp, scale, T, T1, n_in, B, dev):
     sel = sqz.Selection.empty(idx, B, 1, False, dev, key_idx=False)
     acc = {k: [] for k in ("skew", "mass_sel", "mass_ideal", "recall", "n_T", "mass_T", "k")}
     for i in range(n_in):
-        sqz.centroid_lookup(idx, Qt[i], scale, T, T1, sel=sel)
+        sqz.centroid_lookup(idx, Qt[i], scale, T, T1, sel=sel, T0=T0)
         out = sqz.selection_diagnostics(idx, Qt[i], Kp, sel, scale, 0.01, T)
         for k, v in out.items():
             acc[k].append(v.float().cpu().numpy().ravel())
@@ -398,6 +424,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     sqz.device_check()
     dt = cfg["dtype"]
     H, d, L, c2, c1, B, n_q, n_u = (cfg[k] for k in ("H", "d", "L", "c2", "c1", "B", "n_q", "n_u"))
+    c0 = cfg.get("c0", 0)
     scale = 1.0 / float(np.sqrt(d))
     # ---- sharding of the work over the ranks ----
     shard = cfg.get("shard", "replicas") if world > 1 else "none"
@@ -422,6 +449,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         init2 = synth.device_kmeans_init(H, L, c2, seed=2000 + cno, device=dev, heads=heads)
         init1 = synth.device_kmeans_init(H, c2, c1, seed=2100 + cno, device=dev, heads=heads) \
             if c1 else None
+        init0 = synth.device_kmeans_init(H, c1, c0, seed=2200 + cno, device=dev, heads=heads) \
+            if c0 else None
     else:
         fc = synth.fixed_context(H, L, d, c2, dtype=dt, seed=1000 + cno, G1=c1)
         mix = fc.mix
@@ -429,11 +458,14 @@ def run_gpu(args, cfg, rank, world, local_rank):
         init2 = torch.from_numpy(synth.kmeans_init(H, L, c2, seed=2000 + cno)[heads]).to(dev)
         init1 = (torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=2100 + cno)[heads]).to(dev)
                  if c1 else None)
+        init0 = (torch.from_numpy(synth.kmeans_init(H, c1, c0, seed=2200 + cno)[heads]).to(dev)
+                 if c0 else None)
         del fc
     t0 = time.time()
     idx, Kp, Vp, iters = sqz.cluster_keys(K, V, c2, init2, c1, init1, max_iters=kiters,
                                           assign_mode={"auto": sqz.KMEANS_AUTO, "exact": sqz.KMEANS_EXACT,
-                                                       "tensor": sqz.KMEANS_TENSOR}[args.kmeans_mode])
+                                                       "tensor": sqz.KMEANS_TENSOR}[args.kmeans_mode],
+                                          c0=c0, init0=init0)
     torch.cuda.synchronize()
     t_index = time.time() - t0
     # host copy of the sampled head (original order) for the oracle parity check
@@ -497,12 +529,19 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # ---- calibration of the global thresholds (R12, R13) ----
     # bisection on the all-reduced retained weight (integer sums, exact in fp64):
     # the same T at every N, so the N-GPU run selects what the 1-GPU run selects
-    T1 = 0.0
-    if c1:
+    T1 = T0 = 0.0
+    if c0:  # three levels: Level 0 keeps 50% of the keys, Level 1 25% (R13 extended)
+        s = sqz.centroid_lookup(idx, Qc, scale, 0.0, 0.0, debug=True, comm=comm)
+        T0 = calib.distributed_threshold(s.dbg_S0, idx.N0[None], 0.5, allsum(float(
+            Bc * idx.N0.sum())), allreduce=allsum)
+        s = sqz.centroid_lookup(idx, Qc, scale, 0.0, 0.0, debug=True, comm=comm, T0=T0)
+        T1 = calib.distributed_threshold(s.dbg_S1, idx.N1[None], 0.25, allsum(float(
+            Bc * idx.N1.sum())), allreduce=allsum)
+    elif c1:
         s = sqz.centroid_lookup(idx, Qc, scale, 0.0, 0.0, debug=True, comm=comm)
         T1 = calib.distributed_threshold(s.dbg_S1, idx.N1[None], 0.5, allsum(float(
             Bc * idx.N1.sum())), allreduce=allsum)
-    s = sqz.centroid_lookup(idx, Qc, scale, 0.0, T1, debug=True, comm=comm)
+    s = sqz.centroid_lookup(idx, Qc, scale, 0.0, T1, debug=True, comm=comm, T0=T0)
     T = calib.distributed_threshold(s.dbg_S, idx.N2[None], cfg["retention"], float(Bc * H * L),
                                     allreduce=allsum)
     del s, Qc
@@ -517,7 +556,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     ks, kus = [], []
     c2l = idx.c2
     for i in range(n_inputs):
-        sqz.centroid_lookup(idx, Qt[i], scale, T, T1, sel=sel, comm=comm)
+        sqz.centroid_lookup(idx, Qt[i], scale, T, T1, sel=sel, comm=comm, T0=T0)
         ks.append(int(sel.n_keys.sum()))
         # keys in the per-head UNION of the B selections (what the batch-shared pass reads)
         ar = torch.arange(c2l, device=dev)
@@ -533,9 +572,17 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # algorithmic bytes / flops of THIS rank
     c1l, c2l = idx.c1, idx.c2
     lookup_rows = c2l + c1l  # rows scanned per head (hier: L2 restricted, approximated below)
-    bytes_lookup = Hl * (c1l if c1l else c2l) * (d * esz + 4)
-    if c1:
-        bytes_lookup += Hl * 0.5 * c2l * (d * esz + 4) * B  # ~50% of L2 rows scanned per query
+    # lookup bytes: the first level's rows once per head (the batch shares the scan),
+    # deeper levels' REALIZED candidate rows per (b, h) (non-NaN debug scores)
+    first = {1: c2l, 2: c1l, 3: idx.c0}[idx.levels]
+    bytes_lookup = Hl * first * (d * esz + 4)
+    if idx.levels >= 2:
+        sd = sqz.centroid_lookup(idx, Qt[0], scale, T, T1, debug=True, comm=comm, T0=T0)
+        deeper = int((~torch.isnan(sd.dbg_S)).sum())
+        if idx.levels == 3:
+            deeper += int((~torch.isnan(sd.dbg_S1)).sum())
+        bytes_lookup += deeper * (d * esz + 4)
+        del sd
     bytes_attn = k_mean * 2 * d * esz + B * Hl * n_u_r * 2 * d * esz + 2 * B * Hl * n_q * d * esz
     bytes_attn_perq = bytes_attn
     if shared_attn:  # NEXT-1: each selected key is read once for all the queries that chose it
@@ -590,9 +637,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     def step_into(q, Oo, Lo):
         if use_step:
-            sqz.decode_step(idx, q, Kp, Vp, Ku, Vu, scale, T, T1, sel=sel, O=Oo, LSE=Lo, ws=step_ws)
+            sqz.decode_step(idx, q, Kp, Vp, Ku, Vu, scale, T, T1, sel=sel, O=Oo, LSE=Lo, ws=step_ws,
+                            T0=T0)
         else:
-            sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel, comm=comm)
+            sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel, comm=comm, T0=T0)
             attend_into(q, Oo, Lo)
 
     def step(i):
@@ -637,7 +685,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         flush.zero_()
         q = Qt[i % n_inputs]
         evp[i][0].record()
-        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel, comm=comm)
+        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel, comm=comm, T0=T0)
         evp[i][1].record()
         attend(q)
         evp[i][2].record()
@@ -706,7 +754,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if not args.no_parity:
         q = Qt[0]
         sel_p = sqz.Selection.empty(idx, B, n_q, debug=True, device=dev, key_idx=False)
-        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel_p, comm=comm)
+        sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel_p, comm=comm, T0=T0)
         attend_into(q, O, LSE, sel_p)
         torch.cuda.synchronize()
         if rank == 0:
@@ -715,13 +763,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 rs = np.unique(np.concatenate([[0, n_q - 1], np.linspace(0, n_q - 1, 62)])).astype(np.int32)
             t_p = time.time()
             parity = oracle_parity(sqz, gidx, q, sel_p, O, LSE, T, T1, scale, K0, V0, Ku0, Vu0, idx,
-                                   causal, rs)
+                                   causal, rs, T0=T0)
             parity["oracle_s"] = round(time.time() - t_p, 1)
         del sel_p
     # ---- selection quality (App. A skewness, App. D ideal lookup; after the timed region) ----
     quality = None
     if cfg["mode"] == "decode" and comm is None and rank == 0 and not args.no_parity:
-        quality = selection_quality(sqz, idx, Qt, Kp, scale, T, T1, min(n_inputs, 8), B, dev)
+        quality = selection_quality(sqz, idx, Qt, Kp, scale, T, T1, min(n_inputs, 8), B, dev, T0=T0)
     # ---- max over ranks ----
     if world > 1:
         tt = torch.tensor([t_step, t_look, t_attn, t_e2e, t_eager], device=dev)
@@ -773,7 +821,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         whole = {"flops_per_step": int(step_flops),
                  "achieved_TFLOPs": round(step_flops / (t_step * 1e-3) / 1e12, 2)}
     # libsqz kernels per step (NCCL's own kernels not counted)
-    levels = 2 if c1 else 1
+    levels = idx.levels
     per_select = 1 if cfg["mode"] == "decode" else (2 if dt == 1 and d in (64, 128) else 3)
     if comm is None:
         n_look = levels * per_select
@@ -799,7 +847,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
                           "write+read": "flushed between timed steps: 512 MB write, then a 512 MB "
                                         "read of another buffer (untimed), so the step starts from "
                                         "a cold L2 of clean lines"}[args.flush],
-                   "T": T, "T1": T1, "mean_selected_keys_per_step": k_glob,
+                   "T": T, "T1": T1, "T0": T0, "levels": idx.levels,
+                   "mean_selected_keys_per_step": k_glob,
                    "mean_union_keys_per_step": allsum(ku_mean),
                    "attention_path": "batch-shared union pass" if shared_attn else "per-(b,h) streams",
                    "retention_realized": k_glob / (B * H * L), "kmeans_iters": list(iters),

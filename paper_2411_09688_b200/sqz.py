@@ -409,7 +409,7 @@ def sparse_attention(Q, Kp, Vp, idx: Index, sel: Selection, Ku=None, Vu=None, sc
 
 
 def decode_step(idx: Index, Q, Kp, Vp, Ku, Vu, scale, T, T1=0.0, sel: Selection = None,
-                partial=False, out_dtype=None, O=None, LSE=None, ws=None, debug=False):
+                partial=False, out_dtype=None, O=None, LSE=None, ws=None, debug=False, T0=0.0):
     """sqz_decode_step: the centroid lookup and the sparse attention of one decode
     step (Q [B,H,1,d]) in one call.  Returns (Selection, O [B,H,1,d], LSE [B,H,1])."""
     B, H, n_q, d = Q.shape
@@ -430,7 +430,7 @@ def decode_step(idx: Index, Q, Kp, Vp, Ku, Vu, scale, T, T1=0.0, sel: Selection 
         _check(lib().sqz_decode_step_workspace(ctypes.byref(s), B, n_u, ctypes.byref(nb)))
         ws = _WS.get(("step", Q.device, idx.H, idx.L, idx.c1, idx.c2, B, n_u), nb.value, Q.device)
         _WS.last_attn = ws
-    lp = sqz_lookup_params(scale, T, T1, None)
+    lp = sqz_lookup_params(scale, T, T1, None, T0)
     ap = sqz_attn_params(scale, 0, int(partial), out_dtype)
     ss = sel.struct()
     _check(lib().sqz_decode_step(ctypes.byref(s), _p(Q), B, _p(Kp), _p(Vp), _p(Ku), _p(Vu), n_u,
