@@ -122,6 +122,9 @@ LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base, int worl
         }
     };
     level(w.l2, idx->c2);
+    // candidate-list levels of a bf16 prefill with 4+ query tiles: gathered rows
+    const bool gat = prefill && idx->dtype == SQZ_BF16 && n_q >= 4 * 128;
+    if (gat && idx->levels >= 2) w.l2.cgather = cv.take<char>((size_t)BH * idx->c2 * idx->d * 2);
     if (idx->levels >= 2) {
         level(w.l1, idx->c1);
         w.l1.list = cv.take<int32_t>(BH * idx->c1);
@@ -129,6 +132,7 @@ LookupWs lookup_carve(const sqz_index *idx, int B, int n_q, char *base, int worl
         w.l1.exp_list = cv.take<int32_t>(BH * idx->c2);
         w.l1.n_exp = cv.take<int32_t>(BH);
     }
+    if (gat && idx->levels == 3) w.l1.cgather = cv.take<char>((size_t)BH * idx->c1 * idx->d * 2);
     if (idx->levels == 3) {
         level(w.l0, idx->c0);
         w.l0.list = cv.take<int32_t>(BH * idx->c0);

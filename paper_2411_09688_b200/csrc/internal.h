@@ -54,6 +54,9 @@ struct LevelArgs {
     const int32_t *rl_list, *rl_pref, *rl_off;  // [B,H,rl_c], [B,H,rl_c], [H,rl_c+1]
     const int32_t *rl_n;                        // [B,H] survivors
     int32_t rl_c;
+    // bf16 prefill with a candidate list and many query tiles: the candidate
+    // rows gathered contiguously per (b,h), [B*H][c][d] (TMA-loaded)
+    void *cgather;
 };
 
 struct LookupShape {

@@ -916,7 +916,11 @@ template <int D> struct PlSmem {
     static constexpr int BYTES = MISC + 64 + 1024;
 };
 
-template <int D, bool ROWLIST>
+// GATHERED (with ROWLIST): the candidate rows were first copied, per (b,h) and in
+// list order, into the contiguous buffer lv.cgather [B*H][c][D] (k_gather_cand),
+// so every query tile loads them with TMA boxes like a full table: the copy is
+// read once, the n_q / 128 query tiles of the (b,h) reuse it from L2.
+template <int D, bool ROWLIST, bool GATHERED>
 __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
                                                                  const __nv_bfloat16 *__restrict__ Q,
                                                                  LevelArgs lv,
@@ -965,7 +969,7 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
     SQZ_TRACE_AT(g_trace_pl, 0);
 
     // Q tile (rows beyond n_q are zero): TMA for contiguous tables, else cp.async
-    if constexpr (!ROWLIST) {
+    if constexpr (!ROWLIST || GATHERED) {
         if (tid == 0) {
             mbar_arrive_expect_tx(qbar, TILE_BYTES);
 #pragma unroll
@@ -1007,12 +1011,13 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
             s_nw[(k & 3) * PL_T + rr] = nw;
         }
         const uint32_t dst = sbase + SM::C0 + (k & 1) * SM::TILE;
-        if constexpr (!ROWLIST) {  // one thread: two 64-column boxes, rows past c zero-filled
+        if constexpr (!ROWLIST || GATHERED) {  // one thread: two 64-column boxes, rows past c zero-filled
             if (tid == 0) {
                 mbar_arrive_expect_tx(&tbar[k & 1], TILE_BYTES);
 #pragma unroll
                 for (int hb = 0; hb < D / 64; ++hb)
-                    tma_load_3d(dst + hb * HB, &maps.c, hb * 64, (j % ntile) * PL_T, h, &tbar[k & 1]);
+                    tma_load_3d(dst + hb * HB, &maps.c, hb * 64, (j % ntile) * PL_T, GATHERED ? bh : h,
+                                &tbar[k & 1]);
             }
         } else {
             for (int cc = (tid / PL_T) * (CPR / 2); cc < (tid / PL_T + 1) * (CPR / 2); ++cc)
@@ -1023,7 +1028,7 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
     };
     // thread 0, before issuing MMA(j): the TMA loads of its operands have landed
     auto wait_tile = [&](int j) {
-        if constexpr (!ROWLIST) {
+        if constexpr (!ROWLIST || GATHERED) {
             const int k = j - first;
             if (k == 0) mbar_wait(qbar, 0);
             mbar_wait(&tbar[k & 1], (k >> 1) & 1);
@@ -1207,10 +1212,27 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
     SQZ_TRACE_AT(g_trace_pl, 5);
 }
 
-template <int D, bool RL>
+// the candidate rows of every (b,h), in list order, into a contiguous copy
+template <int D>
+__global__ void k_gather_cand(const __nv_bfloat16 *__restrict__ C, const int32_t *__restrict__ rows,
+                              const int32_t *__restrict__ n_rows, int row_stride, int c, int H,
+                              __nv_bfloat16 *__restrict__ out) {
+    constexpr int V = D * 2 / 16;  // 16-byte chunks per row
+    const int bh = blockIdx.y, h = bh % H;
+    const int n = ldcg(n_rows + bh);
+    const int32_t *rl = rows + (size_t)bh * row_stride;
+    const uint4 *src = reinterpret_cast<const uint4 *>(C + (size_t)h * c * D);
+    uint4 *dst = reinterpret_cast<uint4 *>(out + (size_t)bh * c * D);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * V; e += gridDim.x * blockDim.x) {
+        const int rr = e / V, ch = e - rr * V;
+        dst[(size_t)rr * V + ch] = __ldg(src + (size_t)ldcg(rl + rr) * V + ch);
+    }
+}
+
+template <int D, bool RL, bool GATHERED = false>
 static cudaError_t launch_prefill_tc(const LookupShape &s, const __nv_bfloat16 *Q, const LevelArgs &lv,
                                      cudaStream_t st) {
-    auto kern = k_prefill_lookup_tc<D, RL>;
+    auto kern = k_prefill_lookup_tc<D, RL, GATHERED>;
     {
         cudaError_t e = ensure_func_attr((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          PlSmem<D>::BYTES);
@@ -1218,7 +1240,17 @@ static cudaError_t launch_prefill_tc(const LookupShape &s, const __nv_bfloat16 *
     }
     PlMaps maps;
     std::memset(&maps, 0, sizeof(maps));
-    if (!RL) {
+    if (GATHERED) {
+        k_gather_cand<D><<<dim3(64, s.B * s.H), 256, 0, st>>>(
+            reinterpret_cast<const __nv_bfloat16 *>(lv.C), lv.rows, lv.n_rows, lv.row_stride, lv.c, s.H,
+            reinterpret_cast<__nv_bfloat16 *>(lv.cgather));
+        const uint64_t dc[3] = {(uint64_t)D, (uint64_t)lv.c, (uint64_t)s.B * s.H};
+        const uint64_t dq[3] = {(uint64_t)D, (uint64_t)s.n_q, (uint64_t)s.B * s.H};
+        const uint32_t box[3] = {64, PL_T, 1};
+        if (encode_tmap_bf16_3d(&maps.c, lv.cgather, dc, box) != 0 ||
+            encode_tmap_bf16_3d(&maps.q, Q, dq, box) != 0)
+            return cudaErrorInvalidValue;
+    } else if (!RL) {
         const uint64_t dc[3] = {(uint64_t)D, (uint64_t)lv.c, (uint64_t)s.H};
         const uint64_t dq[3] = {(uint64_t)D, (uint64_t)s.n_q, (uint64_t)s.B * s.H};
         const uint32_t box[3] = {64, PL_T, 1};
@@ -1239,6 +1271,8 @@ static cudaError_t launch_level_t(const LookupShape &s, const T *Q, const LevelA
     if constexpr (sizeof(T) == 2) {
         // bf16 prefill: tensor-core lookup (fp32 inputs keep the exact FFMA path)
         if (s.n_q > 1) {
+            // many query tiles: gather the candidates once, then TMA tiles (4+ tiles)
+            if (lv.rows && lv.cgather && s.n_q >= 4 * PL_T) return launch_prefill_tc<D, true, true>(s, Q, lv, st);
             if (lv.rows) return launch_prefill_tc<D, true>(s, Q, lv, st);
             return launch_prefill_tc<D, false>(s, Q, lv, st);
         }

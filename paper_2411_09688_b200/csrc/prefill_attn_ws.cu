@@ -4,7 +4,7 @@
 // Work decomposition.  A "segment" is one (b,h) x one pair of 128-row query
 // tiles (256 rows) with its key stream: the selected fixed keys of (b,h), then
 // the user keys visible to the pair's last row (R8).  The segments' 128-key
-// tiles are laid end to end (segment s = bh * npairs + pair) and the grid --
+// tiles are laid end to end (segment s = pair * B*H + bh, see seg_ids) and the grid --
 // one CTA per SM -- cuts that list into equal contiguous ranges, so every CTA
 // does the same number of tiles whatever the per-head selection sizes are (the
 // decode kernel's equal-key-range idea).  A CTA walks the
@@ -181,10 +181,29 @@ constexpr int SEG_W = 6;
 struct Seg {
     int bh, pair, nkf, nkf4, len, tiles, cost;
 };
+// Segment order: PAIR-major (s = pair * B*H + bh) by default.  The equal-cost
+// ranges then put the npairs query pairs of one head on CTAs G/npairs apart that
+// start at (nearly) the same key of that head's stream and advance at the same
+// rate, so the head's selected K/V tiles are read from DRAM once and served from
+// L2 to the other pairs; with head-major order (s = bh * npairs + pair) the
+// pairs of a head run on neighbouring CTAs at different offsets of the stream
+// and every pair re-reads it from DRAM once it exceeds the L2 window.
+#ifndef SQZ_PF_PAIR_MAJOR
+#define SQZ_PF_PAIR_MAJOR 1
+#endif
+__device__ __forceinline__ void seg_ids(const AttnArgs &a, int npairs, int s, int &bh, int &pair) {
+#if SQZ_PF_PAIR_MAJOR
+    const int BH = a.B * a.H;
+    pair = s / BH;
+    bh = s - pair * BH;
+#else
+    bh = s / npairs;
+    pair = s - bh * npairs;
+#endif
+}
 __device__ __forceinline__ Seg seg_of(const AttnArgs &a, int npairs, int s) {
     Seg g;
-    g.bh = s / npairs;
-    g.pair = s - g.bh * npairs;
+    seg_ids(a, npairs, s, g.bh, g.pair);
     g.nkf = ldcg(a.n_keys + g.bh);
     const int last_row = min(g.pair * ws::PR + ws::PR, a.n_q) - 1;
     int nuv = a.causal ? last_row + a.n_u - a.n_q + 1 : a.n_u;
@@ -728,7 +747,8 @@ __global__ void __launch_bounds__(256) k_merge_cut(AttnArgs a, int npairs) {
     if (s >= 0) {
         const int c0 = ldcg(a.cut + 3 * k + 1), c1 = ldcg(a.cut + 3 * k + 2);
         const int np = c1 - c0 + 1;
-        const int bh = s / npairs, pair = s - bh * npairs;
+        int bh, pair;
+        seg_ids(a, npairs, s, bh, pair);
         const int nrow_seg = min(PR, a.n_q - pair * PR);
         const int r_lo = blockIdx.y * MERGE_ROWS, nrow = min(MERGE_ROWS, nrow_seg - r_lo);
         if (nrow > 0) {

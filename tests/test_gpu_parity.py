@@ -305,6 +305,9 @@ PREFILL_CASES = [
     ("bf16_d64_noncausal_B2", 2, 2048, 64, 100, 0, synth.BF16, 2, 300, 150, 0.3, False),
     ("hier_bf16_d64", 2, 3000, 64, 150, 30, synth.BF16, 1, 130, 130, 0.15, True),
     ("hier_bf16_d64_noncausal", 2, 3000, 64, 150, 30, synth.BF16, 1, 170, 60, 0.15, False),
+    # 5 query tiles: the candidate rows are gathered once and TMA-loaded per tile
+    ("hier_bf16_gathered", 2, 4000, 128, 200, 40, synth.BF16, 2, 600, 300, 0.15, True),
+    ("hier_bf16_d64_gathered", 2, 3000, 64, 150, 30, synth.BF16, 1, 520, 100, 0.15, False),
     ("bf16_d64_multiseg", 4, 6000, 64, 150, 0, synth.BF16, 1, 600, 600, 0.4, True),
     # fp32 d = 128 prefill (k_prefill_rowlse / colsum<float,128>, exact FFMA attention)
     ("fp32_d128", 1, 1500, 128, 40, 0, synth.F32, 1, 70, 90, 0.3, True),
