@@ -436,6 +436,22 @@ int sqz_comm_allgather_merge(void *comm, const float *O_part, const float *LSE_p
                              int32_t d, void *O, float *LSE, int32_t out_dtype, void *ws,
                              size_t ws_bytes, void *stream);
 
+/* Output exchange by HEAD SLICE (the prefill form): a 4K-token
+ * prefill partial is [B, H, n_q, d] fp32 per rank, and all-gathering it would
+ * land world x that on every rank.  Here rank r receives from every rank only
+ * the partial rows of its heads [r H/world, (r+1) H/world) (grouped
+ * ncclSend/ncclRecv) and merges them in rank order:
+ *   O_part [B, H, n_q, d] fp32, LSE_part [B, H, n_q] fp32 (this rank's partial;
+ *   -inf = identity) -> O_slice [B, H/world, n_q, d] out_dtype, LSE_slice
+ *   [B, H/world, n_q] fp32: the exact output of this rank's heads (what a
+ *   head-parallel o_proj consumes).  H must be a multiple of world.  ws:
+ *   sqz_comm_alltoall_merge_workspace bytes.  Asynchronous on `stream`. */
+int sqz_comm_alltoall_merge_workspace(int32_t world, int32_t B, int32_t H, int32_t n_q, int32_t d,
+                                      size_t *ws_bytes);
+int sqz_comm_alltoall_merge(void *comm, const float *O_part, const float *LSE_part, int32_t B, int32_t H,
+                            int32_t n_q, int32_t d, void *O_slice, float *LSE_slice, int32_t out_dtype,
+                            void *ws, size_t ws_bytes, void *stream);
+
 /* ---------------------------------------------------------------------- */
 /* Misc                                                                      */
 /* ---------------------------------------------------------------------- */

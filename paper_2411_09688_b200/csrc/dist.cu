@@ -32,6 +32,11 @@ struct NcclApi {
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    // point-to-point (the head-slice exchange); optional
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     bool ok = false;
     char why[256] = "";
 };
@@ -53,6 +58,10 @@ NcclApi &nccl() {
         api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
         api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
         api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+        api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+        api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+        api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+        api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
         api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather &&
                  api.GetErrorString;
         if (!api.ok) snprintf(api.why, sizeof(api.why), "libnccl.so.2 lacks a required symbol");
@@ -256,6 +265,58 @@ int sqz_comm_allgather_merge(void *comm, const float *O_part, const float *LSE_p
     rc = comm_allgather_f32(comm, LSE_part, Lg, (size_t)rows, st);
     if (rc) return rc;
     cudaError_t e = launch_merge(c->world, Og, Lg, rows, d, O, LSE, out_dtype, st);
+    if (e != cudaSuccess) return set_error(SQZ_ERR_CUDA, "merge launch: %s", cudaGetErrorString(e));
+    return SQZ_OK;
+}
+
+int sqz_comm_alltoall_merge_workspace(int32_t world, int32_t B, int32_t H, int32_t n_q, int32_t d,
+                                      size_t *ws_bytes) {
+    if (world < 1 || B < 1 || H < 1 || n_q < 1 || d < 1 || !ws_bytes)
+        return set_error(SQZ_ERR_INVALID_ARG, "world, B, H, n_q, d >= 1 and ws_bytes required");
+    if (H % world) return set_error(SQZ_ERR_INVALID_ARG, "H = %d is not a multiple of world = %d", H, world);
+    const size_t rows = (size_t)B * (H / world) * n_q;
+    *ws_bytes = (size_t)world * rows * (d + 1) * sizeof(float) + 1024;
+    return SQZ_OK;
+}
+
+int sqz_comm_alltoall_merge(void *comm, const float *O_part, const float *LSE_part, int32_t B, int32_t H,
+                            int32_t n_q, int32_t d, void *O_slice, float *LSE_slice, int32_t out_dtype,
+                            void *ws, size_t ws_bytes, void *stream) {
+    if (!comm) return set_error(SQZ_ERR_INVALID_ARG, "comm is NULL");
+    if (!O_part || !LSE_part || !O_slice || !LSE_slice || !ws)
+        return set_error(SQZ_ERR_INVALID_ARG, "O_part, LSE_part, O_slice, LSE_slice, ws required");
+    if (out_dtype != SQZ_F32 && out_dtype != SQZ_BF16)
+        return set_error(SQZ_ERR_INVALID_ARG, "out_dtype = %d is not a sqz_dtype", out_dtype);
+    Comm *c = static_cast<Comm *>(comm);
+    size_t need = 0;
+    int rc = sqz_comm_alltoall_merge_workspace(c->world, B, H, n_q, d, &need);
+    if (rc) return rc;
+    if (ws_bytes < need) return set_error(SQZ_ERR_INVALID_ARG, "ws_bytes = %zu < %zu", ws_bytes, need);
+    NcclApi &api = nccl();
+    if (!api.Send || !api.Recv || !api.GroupStart || !api.GroupEnd)
+        return set_error(SQZ_ERR_NCCL, "libnccl.so.2 lacks ncclSend / ncclRecv / ncclGroupStart / ncclGroupEnd");
+    const int W = c->world, Hs = H / W;
+    const size_t rows = (size_t)B * Hs * n_q, blk = (size_t)Hs * n_q;  // rows of one (b, head slice)
+    char *base = reinterpret_cast<char *>(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    float *Or = reinterpret_cast<float *>(base);  // [W][B][Hs][n_q][d] (merge layout [P][rows][d])
+    float *Lr = Or + (size_t)W * rows * d;        // [W][B][Hs][n_q]
+    cudaStream_t st = (cudaStream_t)stream;
+    ncclResult_t r = api.GroupStart();
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+    for (int p = 0; p < W && r == ncclSuccess; ++p)
+        for (int b = 0; b < B && r == ncclSuccess; ++b) {
+            // my partial rows of peer p's heads, and peer p's partial rows of my heads
+            const size_t src = ((size_t)b * H + (size_t)p * Hs) * n_q;
+            const size_t dst = ((size_t)p * B + b) * blk;
+            r = api.Send(O_part + src * d, blk * d, ncclFloat32, p, c->c, st);
+            if (r == ncclSuccess) r = api.Recv(Or + dst * d, blk * d, ncclFloat32, p, c->c, st);
+            if (r == ncclSuccess) r = api.Send(LSE_part + src, blk, ncclFloat32, p, c->c, st);
+            if (r == ncclSuccess) r = api.Recv(Lr + dst, blk, ncclFloat32, p, c->c, st);
+        }
+    const ncclResult_t r2 = api.GroupEnd();
+    if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
+    if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
+    cudaError_t e = launch_merge(W, Or, Lr, (int64_t)rows, d, O_slice, LSE_slice, out_dtype, st);
     if (e != cudaSuccess) return set_error(SQZ_ERR_CUDA, "merge launch: %s", cudaGetErrorString(e));
     return SQZ_OK;
 }

@@ -36,6 +36,7 @@ EXPORTS = [
     "sqz_comm_unique_id", "sqz_comm_init", "sqz_comm_destroy", "sqz_lookup_workspace_comm",
     "sqz_comm_merge_workspace", "sqz_comm_allgather_merge", "sqz_decode_step_workspace",
     "sqz_decode_step", "sqz_selection_diagnostics_workspace", "sqz_selection_diagnostics",
+    "sqz_comm_alltoall_merge_workspace", "sqz_comm_alltoall_merge",
 ]
 
 
@@ -138,6 +139,8 @@ def lib():
                                       ctypes.POINTER(sqz_lookup_params),
                                       ctypes.POINTER(sqz_attn_params), ctypes.POINTER(sqz_selection),
                                       vp, vp, vp, sz, vp]
+        L.sqz_comm_alltoall_merge_workspace.argtypes = [i32, i32, i32, i32, i32, szp]
+        L.sqz_comm_alltoall_merge.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp, vp, i32, vp, sz, vp]
         L.sqz_selection_diagnostics_workspace.argtypes = [ip, i32, szp]
         L.sqz_selection_diagnostics.argtypes = [ip, vp, i32, vp, ctypes.POINTER(sqz_selection),
                                                 ctypes.c_float, ctypes.c_double, ctypes.c_float,
@@ -606,3 +609,21 @@ def selection_diagnostics(idx: Index, Q: torch.Tensor, Kp: torch.Tensor, sel: Se
                                            float(scale), float(top_frac), float(T), ctypes.byref(d),
                                            _p(ws), nb.value, _stream()))
     return out
+
+
+def alltoall_merge(comm: "Comm", O_part: torch.Tensor, LSE_part: torch.Tensor, out_dtype=SQZ_BF16,
+                   O=None, LSE=None):
+    """sqz_comm_alltoall_merge: partials O_part [B,H,n_q,d] fp32 / LSE_part [B,H,n_q]
+    of this rank -> the merged output of this rank's head slice [B,H/world,n_q,d]."""
+    B, H, n_q, d = O_part.shape
+    Hs = H // comm.world
+    if O is None:
+        O = torch.empty(B, Hs, n_q, d, dtype=torch_dtype(out_dtype), device=O_part.device)
+    if LSE is None:
+        LSE = torch.empty(B, Hs, n_q, dtype=torch.float32, device=O_part.device)
+    nb = ctypes.c_size_t(0)
+    _check(lib().sqz_comm_alltoall_merge_workspace(comm.world, B, H, n_q, d, ctypes.byref(nb)))
+    ws = _WS.get(("a2a", O_part.device, comm.world, B, H, n_q, d), nb.value, O_part.device)
+    _check(lib().sqz_comm_alltoall_merge(comm.handle, _p(O_part), _p(LSE_part), B, H, n_q, d, _p(O),
+                                         _p(LSE), out_dtype, _p(ws), ws.numel(), _stream()))
+    return O, LSE

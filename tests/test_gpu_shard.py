@@ -171,5 +171,10 @@ def test_comm_world1_matches_local_path():
             Oc, Lc = sqz.merge_partials(O.reshape(1, -1, idx.d), LSE.reshape(1, -1))
             torch.cuda.synchronize()
             assert torch.equal(Om.reshape(-1, idx.d), Oc) and torch.equal(Lm.reshape(-1), Lc)
+            # the head-slice exchange of one rank is the merge of its own partial
+            Oa, La = sqz.alltoall_merge(comm, O, LSE, out_dtype=sqz.SQZ_F32)
+            torch.cuda.synchronize()
+            assert Oa.shape == O.shape
+            assert torch.equal(Oa.reshape(-1, idx.d), Oc) and torch.equal(La.reshape(-1), Lc)
     finally:
         comm.close()

@@ -221,6 +221,32 @@ def _worker(rank, world, port, case, errq):
         assert rc == 0
         np.testing.assert_allclose(O_m, O_ref.reshape(-1, d), atol=1e-12)
         np.testing.assert_allclose(L_m, L_ref.reshape(-1), atol=1e-12)
+        # head-slice exchange (the protocol of sqz_comm_alltoall_merge): rank r sends
+        # its partial rows of heads [p Hs, (p+1) Hs) to rank p and merges, in rank
+        # order, the rows of its own heads it receives from every rank
+        Hs = H // world
+        recv_O, recv_L, reqs = [None] * world, [None] * world, []
+        for p in range(world):
+            so = torch.from_numpy(np.ascontiguousarray(O_r[:, p * Hs:(p + 1) * Hs]))
+            sl = torch.from_numpy(np.ascontiguousarray(L_r[:, p * Hs:(p + 1) * Hs]))
+            if p == rank:
+                recv_O[p], recv_L[p] = so, sl
+                continue
+            recv_O[p], recv_L[p] = torch.empty_like(so), torch.empty_like(sl)
+            if rank < p:
+                dist.send(so, p)
+                dist.send(sl, p)
+                dist.recv(recv_O[p], p)
+                dist.recv(recv_L[p], p)
+            else:
+                dist.recv(recv_O[p], p)
+                dist.recv(recv_L[p], p)
+                dist.send(so, p)
+                dist.send(sl, p)
+        O_s, L_s = oracle.merge(np.stack([o.numpy().reshape(-1, d) for o in recv_O]),
+                                np.stack([l.numpy().reshape(-1) for l in recv_L]))
+        np.testing.assert_allclose(O_s, O_ref[:, rank * Hs:(rank + 1) * Hs].reshape(-1, d), atol=1e-12)
+        np.testing.assert_allclose(L_s, L_ref[:, rank * Hs:(rank + 1) * Hs].reshape(-1), atol=1e-12)
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # report to the parent
