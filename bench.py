@@ -590,8 +590,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
     flops_attn = 4.0 * n_q * d * k_mean + (4.0 * d * B * Hl * (n_q * n_u_r - n_q * (n_q - 1) / 2)
                                           if n_u_r else 0.0)
     flops_lookup = 2.0 * B * Hl * n_q * lookup_rows * d
-    O = torch.empty(B, Hl, n_q, d, dtype=sqz.torch_dtype(dt), device=dev)
-    LSE = torch.empty(B, Hl, n_q, dtype=torch.float32, device=dev)
+    # cluster-sharded prefill: each rank ends with its head slice (head-slice all-to-all)
+    a2a = comm is not None and cfg["mode"] == "prefill"
+    Ho = Hl // world if a2a else Hl
+    O = torch.empty(B, Ho, n_q, d, dtype=sqz.torch_dtype(dt), device=dev)
+    LSE = torch.empty(B, Ho, n_q, dtype=torch.float32, device=dev)
     Op = torch.empty(B, Hl, n_q, d, dtype=torch.float32, device=dev) if comm else None
     Lp = torch.empty(B, Hl, n_q, dtype=torch.float32, device=dev) if comm else None
     # L2 flush between timed steps: a 512 MB write (4x the 126 MB L2).  The write
@@ -620,7 +623,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
         else:  # partial over this shard, then the all-gather merge (P:361-363 across GPUs)
             sqz.sparse_attention(q, Kp, Vp, idx, sl, Ku, Vu, scale, causal=causal, partial=True,
                                  out_dtype=sqz.SQZ_F32, O=Op, LSE=Lp, per_row=args.attn_per_row)
-            sqz.allgather_merge(comm, Op, Lp, out_dtype=dt, O=Oo, LSE=Lo)
+            if a2a:  # prefill: each rank merges only its head slice
+                sqz.alltoall_merge(comm, Op, Lp, out_dtype=dt, O=Oo, LSE=Lo)
+            else:
+                sqz.allgather_merge(comm, Op, Lp, out_dtype=dt, O=Oo, LSE=Lo)
 
     def attend(q):
         attend_into(q, O, LSE)
