@@ -1,0 +1,2 @@
+timeout 300 python experiments/trace_decode.py > gpurun_out/trace_decode.log 2>&1
+python -m paper_2411_09688_b200.build --force > /dev/null 2>&1

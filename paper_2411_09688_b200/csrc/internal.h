@@ -183,6 +183,8 @@ int index_validate(const sqz_index &idx, void *ws, size_t ws_bytes, cudaStream_t
 // tmap.cu: TMA tensor map of a contiguous bf16 [dims2][dims1][dims0] tensor
 // (128-byte swizzle, zero out-of-bounds fill); 0 on success
 int encode_tmap_bf16_3d(CUtensorMap *m, const void *ptr, const uint64_t dims[3], const uint32_t box[3]);
+int encode_tmap_bf16_2d(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                        uint32_t box_rows);
 // tmap.cu: per-device launch caches (keyed by device ordinal and kernel, mutex
 // guarded): SM count of the current device; sets a function attribute once per
 // (device, kernel) -- for cudaFuncAttributeMaxDynamicSharedMemorySize only when

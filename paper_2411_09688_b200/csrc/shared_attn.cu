@@ -12,10 +12,10 @@
 //                  streams [union fixed keys | user KV of b = 0 .. B-1] (the
 //                  user keys of b carry the mask {b}); a warp takes 32-key
 //                  tiles (cp.async, 3-stage ring per warp, XOR-swizzled rows)
-//                  and runs S = Q K^T and O += P V on the tensor cores
-//                  (mma.sync m16n8k16 bf16: M = the up-to-16 queries of the
-//                  head, N = keys / head dims) with the per-key query mask
-//                  applied to S before the online softmax (log2 domain);
+//                  and runs S^T = K Q^T and O^T += V^T P^T on the tensor cores
+//                  (mma.sync m16n8k16 bf16: M = 16 keys / 16 head dims, N =
+//                  8 queries per tile) with the per-key query mask applied to
+//                  S before the online softmax (log2 domain);
 //                  each (segment, query) yields a normalised partial, and the
 //                  CTA completing a row's last partial merges it.
 // Every query attends exactly the keys of its own selection plus all n_u of
@@ -28,6 +28,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "tma.cuh"
 
 namespace sqz {
 
@@ -48,18 +49,27 @@ constexpr int NW = SQZ_SHD_NW;     // warps per CTA (one CTA per SM)
 constexpr int NT = NW * 32;
 constexpr int TK = SQZ_SHD_TK;     // keys per warp tile (16 or 32)
 constexpr int NST = SQZ_SHD_NST;   // ring stages per warp
-constexpr int NB8 = TK / 8;        // n8 key tiles of S per warp tile
+// K/V tiles by TMA row gathers (tile::gather4, 4 rows x 128 B per op) instead of
+// cp.async: correct, but measured 321 vs 239 us on cfg4 (32 small TMA ops per tile
+// per warp; the engine's per-op cost dominates at 128-B rows) -- off
+#ifndef SQZ_SHD_TMA
+#define SQZ_SHD_TMA 0
+#endif
 static_assert(TK == 16 || TK == 32, "tile of 16 or 32 keys");
 constexpr int ROWB = D * 2;        // 256 B per bf16 row
 constexpr int TILEB = TK * ROWB;   // 4 KB: one K or V tile
 constexpr int STAGEB = 2 * TILEB;  // K then V
 constexpr int WARPB = NST * STAGEB;
-constexpr int SMEM = NW * WARPB;   // 192 KB by default
+constexpr int SMEM = NW * WARPB + 1024;  // 192 KB by default (+ 1 KB: SW128 tiles need 1024-B alignment)
 static_assert(SMEM <= 200 * 1024 && SMEM >= NW * 16 * 128 * 4, "ring holds the merge buffer");
 constexpr int SEG_KW = 256;        // partition cost of a segment's setup
 constexpr int MIN_KEYS = 1024;     // minimum cost units per CTA
 constexpr int MAXB = 16;
 }  // namespace shd
+
+struct ShdMaps {  // [rows][D] bf16 row tensors, box {64 cols, 1 row}, 128-B swizzle
+    CUtensorMap kp, vp, ku, vu;
+};
 
 struct SharedArgs {
     const __nv_bfloat16 *Q, *Kp, *Vp, *Ku, *Vu;
@@ -105,12 +115,26 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+// 8x8 b16 matrix transpose across the warp (lane l holds row l/4, elements 2(l%4), +1)
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<const uint32_t *>(&v);
 }
-// byte offset of 16-byte chunk c (0..15) of row r in a swizzled 256-byte-row tile
-__device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)(r * shd::ROWB + ((c ^ (r & 7)) << 4)); }
+// byte offset of 16-byte chunk c (0..15) of row r of a K or V tile.  cp.async:
+// 256-B rows, chunk XOR (row & 7).  TMA: two 64-column halves of 128-B rows with
+// the hardware's 128-B swizzle (chunk XOR (row & 7) within each half).
+__device__ __forceinline__ uint32_t swz(int r, int c) {
+#if SQZ_SHD_TMA
+    return (uint32_t)((c >> 3) * (shd::TK * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+#else
+    return (uint32_t)(r * shd::ROWB + ((c ^ (r & 7)) << 4));
+#endif
+}
 
 // warp window of 64 consecutive union runs with their query masks (cf. RunWin)
 struct MWin {
@@ -287,16 +311,31 @@ __device__ void shd_merge_row(const SharedArgs &a, int row, int P) {
 }
 
 // ------------------------------------------------------------- attention
-__global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
+// NQ8 = query tiles of 8 (B <= 8: 1, B <= 16: 2).  The contractions run
+// TRANSPOSED -- S^T = K Q^T (M = 16 keys, N = 8 queries) and O^T += V^T P^T
+// (M = 16 head dims) -- so no MMA row is padding when B <= 8 and the
+// accumulators are 32 registers per query tile; P^T is formed from the S^T
+// fragment with movmatrix (an 8x8 b16 transpose in registers).
+template <int NQ8>
+__global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a, const __grid_constant__ ShdMaps maps) {
     using namespace shd;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ long long s_pref[1025];  // per-head cost prefix
     __shared__ float s_m[NW][MAXB], s_l[NW][MAXB];
     __shared__ int s_last[MAXB];
     __shared__ int s_tm[NW][NST][TK];  // query mask of each key of each stage's tile
+    __shared__ __align__(8) uint64_t s_bar[NW][NST];  // TMA: stage landed (bytes counted)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, t4 = lane & 3;
     const int B = a.B, H = a.H;
+#if SQZ_SHD_TMA
+    if (lane == 0) {
+        for (int st = 0; st < NST; ++st) mbar_init(&s_bar[warp][st], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    int tiles_done = 0;  // this warp's tiles so far (stage / phase of its ring)
+#endif
     griddep_wait();  // the union lists
     const long long ucost = (long long)B * a.n_u;
     if (tid == 0) s_pref[0] = 0;
@@ -351,7 +390,8 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
         else hi = mid - 1;
     }
     const float sl2 = a.scale * LOG2E;
-    unsigned char *wsm = smem + warp * WARPB;
+    unsigned char *wsm = reinterpret_cast<unsigned char *>(((uintptr_t)smem + 1023) & ~(uintptr_t)1023) +
+                         warp * WARPB;
     const uint32_t wbase = smem_addr(wsm);
     for (int h = lo; h < H && s_pref[h] < ke; ++h) {
         const long long cs = s_pref[h], re = s_pref[h + 1], rs = cs + SEG_KW;
@@ -367,24 +407,28 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
         ul.nkf = ldcg(a.u_keys + h);
         const int KU = ul.nkf;
         const __nv_bfloat16 *Kf = a.Kp + (size_t)h * a.L * D, *Vf = a.Vp + (size_t)h * a.L * D;
-        // Q fragments (A operand of S = Q K^T): rows g and g + 8 are queries b = g, g + 8
-        uint32_t qa[8][4];
-        {
-            const bool r0 = g < B, r1 = g + 8 < B;
-            const uint32_t *q0 = reinterpret_cast<const uint32_t *>(a.Q + ((size_t)g * H + h) * D);
-            const uint32_t *q1 = reinterpret_cast<const uint32_t *>(a.Q + ((size_t)(g + 8) * H + h) * D);
+        // Q^T fragments (B operand of S^T = K Q^T): query nq*8 + g, dims kk*16 + 2t4 (+8)
+        uint32_t qb[NQ8][8][2];
+#pragma unroll
+        for (int nq = 0; nq < NQ8; ++nq) {
+            const int q = nq * 8 + g;
+            const bool ok = q < B;
+            const uint32_t *qp = reinterpret_cast<const uint32_t *>(a.Q + ((size_t)q * H + h) * D);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-                qa[kk][0] = r0 ? __ldg(q0 + kk * 8 + t4) : 0u;
-                qa[kk][1] = r1 ? __ldg(q1 + kk * 8 + t4) : 0u;
-                qa[kk][2] = r0 ? __ldg(q0 + kk * 8 + 4 + t4) : 0u;
-                qa[kk][3] = r1 ? __ldg(q1 + kk * 8 + 4 + t4) : 0u;
+                qb[nq][kk][0] = ok ? __ldg(qp + kk * 8 + t4) : 0u;
+                qb[nq][kk][1] = ok ? __ldg(qp + kk * 8 + 4 + t4) : 0u;
             }
         }
-        float o[16][4];
+        // O^T accumulators: dim tile n (dims 16n + g, 16n + g + 8) x queries nq*8 + 2t4 + {0,1}
+        float o[NQ8][8][4];
 #pragma unroll
-        for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-        float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+        for (int nq = 0; nq < NQ8; ++nq)
+#pragma unroll
+            for (int n = 0; n < 8; ++n) o[nq][n][0] = o[nq][n][1] = o[nq][n][2] = o[nq][n][3] = 0.f;
+        float m_r[NQ8][2], l_r[NQ8][2];
+#pragma unroll
+        for (int nq = 0; nq < NQ8; ++nq) m_r[nq][0] = m_r[nq][1] = -INFINITY, l_r[nq][0] = l_r[nq][1] = 0.f;
         MWin win;
         win.J = 0;
         win.end = -1;
@@ -399,6 +443,55 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
             if (k0 < KU) mwin_cover(win, ul, k0, min(kl, KU - 1), lane);
             int pos = 0, msk = 0;
             if (k0 < KU) mwin_get(win, min(myk, KU - 1), pos, msk);
+#if SQZ_SHD_TMA
+            // row of the key in the fixed [H*L] or the user [B*H*n_u] row tensor
+            int row, usr;
+            if (myk < KU) {
+                row = h * (int)a.L + pos;
+                usr = 0;
+            } else {
+                const int u = myk - KU, b = u / a.n_u, uu = u - b * a.n_u;
+                msk = 1 << b;
+                row = (b * H + h) * a.n_u + uu;
+                usr = 1;
+            }
+            if (k0 + (lane & (TK - 1)) > kl) msk = 0;  // past the segment end: masked for every query
+            if (lane < TK) s_tm[warp][st][lane] = msk;
+            const uint32_t sK = wbase + st * STAGEB, sV = sK + TILEB;
+            uint64_t *bar = &s_bar[warp][st];
+            if (lane == 0) mbar_arrive_expect_tx(bar, STAGEB);
+            // lane l < TK/4 gathers keys 4l .. 4l+3 (both halves of K and V rows)
+            int rr[4], us[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                rr[j] = __shfl_sync(FULL, row, (4 * lane + j) & (TK - 1));
+                us[j] = __shfl_sync(FULL, usr, (4 * lane + j) & (TK - 1));
+            }
+            if (lane < TK / 4) {
+                const int u0 = us[0] + us[1] + us[2] + us[3];
+                const uint32_t ro = (uint32_t)(4 * lane) * 128;
+                if (u0 == 0 || u0 == 4) {
+                    const void *mk = u0 ? (const void *)&maps.ku : (const void *)&maps.kp;
+                    const void *mv = u0 ? (const void *)&maps.vu : (const void *)&maps.vp;
+#pragma unroll
+                    for (int hb = 0; hb < 2; ++hb) {
+                        tma_gather4(sK + hb * (TK * 128) + ro, mk, hb * 64, rr[0], rr[1], rr[2], rr[3], bar);
+                        tma_gather4(sV + hb * (TK * 128) + ro, mv, hb * 64, rr[0], rr[1], rr[2], rr[3], bar);
+                    }
+                } else {  // fixed and user rows in one group: one row per load
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const void *mk = us[j] ? (const void *)&maps.ku : (const void *)&maps.kp;
+                        const void *mv = us[j] ? (const void *)&maps.vu : (const void *)&maps.vp;
+#pragma unroll
+                        for (int hb = 0; hb < 2; ++hb) {
+                            tma_load_2d(sK + hb * (TK * 128) + ro + j * 128, mk, hb * 64, rr[j], bar);
+                            tma_load_2d(sV + hb * (TK * 128) + ro + j * 128, mv, hb * 64, rr[j], bar);
+                        }
+                    }
+                }
+            }
+#else
             const __nv_bfloat16 *kr, *vr;
             if (myk < KU) {
                 kr = Kf + (size_t)pos * D;
@@ -421,8 +514,21 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
                 cp16(sK + swz(r, c), reinterpret_cast<const char *>(kp) + c * 16);
                 cp16(sV + swz(r, c), reinterpret_cast<const char *>(vp) + c * 16);
             }
+#endif
         };
         const int my_tiles = ntile > warp ? (ntile - warp + NW - 1) / NW : 0;
+#if SQZ_SHD_TMA
+        // stage of this warp's tile i: its ring continues across segments
+        const int tb = tiles_done;
+        tiles_done += my_tiles;
+#pragma unroll
+        for (int i = 0; i < NST - 1; ++i)
+            if (i < my_tiles) issue(i, (tb + i) % NST);
+        for (int i = 0; i < my_tiles; ++i) {
+            const int st = (tb + i) % NST;
+            if (i + NST - 1 < my_tiles) issue(i + NST - 1, (tb + i + NST - 1) % NST);
+            mbar_wait(&s_bar[warp][st], ((tb + i) / NST) & 1);
+#else
         // prologue: the first NST - 1 tiles of this warp
 #pragma unroll
         for (int i = 0; i < NST - 1; ++i) {
@@ -435,119 +541,127 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
             cp_commit();
             cp_wait<NST - 1>();
             __syncwarp();
+#endif
             const uint32_t sK = wbase + st * STAGEB, sV = sK + TILEB;
-            // ---- S = Q K^T: NB8 n8 tiles of keys ----
-            // two accumulator sets (even / odd k-steps) halve the dependent HMMA chain
-            float s[NB8][4], s2[NB8][4];
+            // ---- S^T = K Q^T: NMT m-tiles of 16 keys ----
+            constexpr int NMT = TK / 16;
+            float sv[NMT][NQ8][4];
 #pragma unroll
-            for (int nt = 0; nt < NB8; ++nt)
+            for (int mt = 0; mt < NMT; ++mt)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) s[nt][e] = s2[nt][e] = 0.f;
+                for (int nq = 0; nq < NQ8; ++nq) sv[mt][nq][0] = sv[mt][nq][1] = sv[mt][nq][2] = sv[mt][nq][3] = 0.f;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
 #pragma unroll
-                for (int pr = 0; pr < NB8 / 2; ++pr) {
-                    // matrices: (keys 16pr+0-7, dims lo), (same keys, dims hi), (keys 16pr+8-15, lo), (hi)
-                    const int mi = lane >> 3, r = pr * 16 + (mi >> 1) * 8 + (lane & 7), c = kk * 2 + (mi & 1);
-                    uint32_t b0, b1, b2, b3;
-                    ldsm_x4(sK + swz(r, c), b0, b1, b2, b3);
-                    float(&d0)[4] = (kk & 1) ? s2[2 * pr] : s[2 * pr];
-                    float(&d1)[4] = (kk & 1) ? s2[2 * pr + 1] : s[2 * pr + 1];
-                    mma16816(d0, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b0, b1);
-                    mma16816(d1, qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3], b2, b3);
+                for (int mt = 0; mt < NMT; ++mt) {
+                    // A = K rows: (keys 0-7, k lo), (keys 8-15, k lo), (0-7, k hi), (8-15, k hi)
+                    const int mi = lane >> 3, r = mt * 16 + (mi & 1) * 8 + (lane & 7), c = kk * 2 + (mi >> 1);
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4(sK + swz(r, c), a0, a1, a2, a3);
+#pragma unroll
+                    for (int nq = 0; nq < NQ8; ++nq)
+                        mma16816(sv[mt][nq], a0, a1, a2, a3, qb[nq][kk][0], qb[nq][kk][1]);
                 }
             }
+            // ---- query mask, online softmax per query column (keys g, g + 8 of each m-tile) ----
+            int km[NMT][2];
 #pragma unroll
-            for (int nt = 0; nt < NB8; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) s[nt][e] += s2[nt][e];
-            // ---- mask, online softmax (rows g, g + 8; keys 8j + 2t4, 8j + 2t4 + 1) ----
-            int mk[NB8][2];
-#pragma unroll
-            for (int jt = 0; jt < NB8; ++jt) {
-                mk[jt][0] = s_tm[warp][st][jt * 8 + 2 * t4];
-                mk[jt][1] = s_tm[warp][st][jt * 8 + 2 * t4 + 1];
+            for (int mt = 0; mt < NMT; ++mt) {
+                km[mt][0] = s_tm[warp][st][mt * 16 + g];
+                km[mt][1] = s_tm[warp][st][mt * 16 + g + 8];
             }
-            float p[NB8][4];
+            uint32_t pb[NMT][NQ8][2];  // P^T fragments (B operand of O^T += V^T P^T)
 #pragma unroll
-            for (int rr = 0; rr < 2; ++rr) {
-                const int q = g + rr * 8;
-                float v[NB8][2];
-                float mx = -INFINITY;
+            for (int nq = 0; nq < NQ8; ++nq) {
+                float pv[NMT][4];
 #pragma unroll
-                for (int jt = 0; jt < NB8; ++jt) {
-                    v[jt][0] = ((mk[jt][0] >> q) & 1) ? s[jt][rr * 2] * sl2 : -INFINITY;
-                    v[jt][1] = ((mk[jt][1] >> q) & 1) ? s[jt][rr * 2 + 1] * sl2 : -INFINITY;
-                    mx = fmaxf(mx, fmaxf(v[jt][0], v[jt][1]));
-                }
-                mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 1));
-                mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 2));
-                const float mn = fmaxf(m_r[rr], mx);
-                float alpha = 1.f, ps = 0.f;
+                for (int e = 0; e < 2; ++e) {
+                    const int q = nq * 8 + 2 * t4 + e;
+                    float v[NMT][2];
+                    float mx = -INFINITY;
 #pragma unroll
-                for (int jt = 0; jt < NB8; ++jt) {
-                    if (mn == -INFINITY) {
-                        p[jt][rr * 2] = p[jt][rr * 2 + 1] = 0.f;
-                    } else {
-                        p[jt][rr * 2] = fast_exp2(v[jt][0] - mn);
-                        p[jt][rr * 2 + 1] = fast_exp2(v[jt][1] - mn);
+                    for (int mt = 0; mt < NMT; ++mt) {
+                        v[mt][0] = ((km[mt][0] >> q) & 1) ? sv[mt][nq][e] * sl2 : -INFINITY;
+                        v[mt][1] = ((km[mt][1] >> q) & 1) ? sv[mt][nq][2 + e] * sl2 : -INFINITY;
+                        mx = fmaxf(mx, fmaxf(v[mt][0], v[mt][1]));
                     }
-                    ps += p[jt][rr * 2] + p[jt][rr * 2 + 1];
-                }
-                if (mn != -INFINITY) alpha = fast_exp2(m_r[rr] - mn);  // exp2(-inf) = 0 for a first key
-                l_r[rr] = l_r[rr] * alpha + ps;
-                m_r[rr] = mn;
+                    mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 4));
+                    mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 8));
+                    mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, 16));
+                    const float mn = fmaxf(m_r[nq][e], mx);
+                    float alpha = 1.f, ps = 0.f;
 #pragma unroll
-                for (int n = 0; n < 16; ++n) {
-                    o[n][rr * 2] *= alpha;
-                    o[n][rr * 2 + 1] *= alpha;
+                    for (int mt = 0; mt < NMT; ++mt) {
+                        const float p0 = mn == -INFINITY ? 0.f : fast_exp2(v[mt][0] - mn);
+                        const float p1 = mn == -INFINITY ? 0.f : fast_exp2(v[mt][1] - mn);
+                        pv[mt][e] = p0;
+                        pv[mt][2 + e] = p1;
+                        ps += p0 + p1;
+                    }
+                    if (mn != -INFINITY) alpha = fast_exp2(m_r[nq][e] - mn);  // exp2(-inf) = 0
+                    l_r[nq][e] = l_r[nq][e] * alpha + ps;
+                    m_r[nq][e] = mn;
+#pragma unroll
+                    for (int n = 0; n < 8; ++n) {
+                        o[nq][n][e] *= alpha;
+                        o[nq][n][2 + e] *= alpha;
+                    }
+                }
+#pragma unroll
+                for (int mt = 0; mt < NMT; ++mt) {
+                    // (key g, queries 2t4..) -> transpose -> (query g, keys 2t4..)
+                    pb[mt][nq][0] = movmatrix_t(pack_bf16(pv[mt][0], pv[mt][1]));
+                    pb[mt][nq][1] = movmatrix_t(pack_bf16(pv[mt][2], pv[mt][3]));
                 }
             }
-            // ---- O += P V: A = P (rows g, g+8; 16 keys per k-step), B = V via ldmatrix.trans ----
+            // ---- O^T += V^T P^T: A = V^T via ldmatrix.trans, per 16-dim tile and 16-key step ----
 #pragma unroll
-            for (int kc = 0; kc < TK / 16; ++kc) {
-                const uint32_t pa0 = pack_bf16(p[2 * kc][0], p[2 * kc][1]);
-                const uint32_t pa1 = pack_bf16(p[2 * kc][2], p[2 * kc][3]);
-                const uint32_t pa2 = pack_bf16(p[2 * kc + 1][0], p[2 * kc + 1][1]);
-                const uint32_t pa3 = pack_bf16(p[2 * kc + 1][2], p[2 * kc + 1][3]);
+            for (int mt = 0; mt < NMT; ++mt) {
 #pragma unroll
-                for (int n2 = 0; n2 < 8; ++n2) {
-                    // matrices: (keys 16kc+0-7, dims 16n2..+7), (keys +8-15, same), (0-7, +8..), (8-15, +8..)
-                    const int mi = lane >> 3, r = kc * 16 + (mi & 1) * 8 + (lane & 7), c = n2 * 2 + (mi >> 1);
-                    uint32_t b0, b1, b2, b3;
-                    ldsm_x4_t(sV + swz(r, c), b0, b1, b2, b3);
-                    mma16816(o[2 * n2], pa0, pa1, pa2, pa3, b0, b1);
-                    mma16816(o[2 * n2 + 1], pa0, pa1, pa2, pa3, b2, b3);
+                for (int n = 0; n < 8; ++n) {
+                    // matrices: (keys 0-7, dims lo), (keys 0-7, dims hi), (keys 8-15, lo), (8-15, hi)
+                    const int mi = lane >> 3, r = mt * 16 + (mi >> 1) * 8 + (lane & 7), c = n * 2 + (mi & 1);
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4_t(sV + swz(r, c), a0, a1, a2, a3);
+#pragma unroll
+                    for (int nq = 0; nq < NQ8; ++nq)
+                        mma16816(o[nq][n], a0, a1, a2, a3, pb[mt][nq][0], pb[mt][nq][1]);
                 }
             }
             __syncwarp();  // the stage is refilled by the next issue
         }
+#if !SQZ_SHD_TMA
         cp_wait<0>();
+#endif
         // ---- combine the warps' states; one partial per query row ----
-        float lr[2];
+        float lr[NQ8][2];
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            float v = l_r[rr];
-            v += __shfl_xor_sync(FULL, v, 1);
-            v += __shfl_xor_sync(FULL, v, 2);
-            lr[rr] = v;
-        }
+        for (int nq = 0; nq < NQ8; ++nq)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                float v = l_r[nq][e];
+                v += __shfl_xor_sync(FULL, v, 4);
+                v += __shfl_xor_sync(FULL, v, 8);
+                v += __shfl_xor_sync(FULL, v, 16);
+                lr[nq][e] = v;
+            }
         __syncthreads();  // every warp is done with its ring: reuse it for the states
-        float *so = reinterpret_cast<float *>(smem);  // [NW][MAXB][D]
-        if (t4 == 0) {
-            s_m[warp][g] = m_r[0];
-            s_l[warp][g] = lr[0];
-            s_m[warp][g + 8] = m_r[1];
-            s_l[warp][g + 8] = lr[1];
-        }
+        float *so = reinterpret_cast<float *>(((uintptr_t)smem + 1023) & ~(uintptr_t)1023);  // [NW][MAXB][D]
 #pragma unroll
-        for (int n = 0; n < 16; ++n) {
-            const int col = n * 8 + 2 * t4;
-            so[(warp * MAXB + g) * D + col] = o[n][0];
-            so[(warp * MAXB + g) * D + col + 1] = o[n][1];
-            so[(warp * MAXB + g + 8) * D + col] = o[n][2];
-            so[(warp * MAXB + g + 8) * D + col + 1] = o[n][3];
-        }
+        for (int nq = 0; nq < NQ8; ++nq)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int q = nq * 8 + 2 * t4 + e;
+                if (g == 0) {
+                    s_m[warp][q] = m_r[nq][e];
+                    s_l[warp][q] = lr[nq][e];
+                }
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    so[(warp * MAXB + q) * D + n * 16 + g] = o[nq][n][e];
+                    so[(warp * MAXB + q) * D + n * 16 + g + 8] = o[nq][n][2 + e];
+                }
+            }
         __syncthreads();
         for (int e = tid; e < B * D; e += NT) {
             const int b = e / D, col = e - b * D;
@@ -579,6 +693,11 @@ __global__ void __launch_bounds__(shd::NT, 1) k_attend_shared(SharedArgs a) {
         for (int b = 0; b < B; ++b)
             if (s_last[b]) shd_merge_row(a, b * H + h, total);
         __syncthreads();
+#if SQZ_SHD_TMA
+        // the ring held the merge buffer (generic stores): order them before the
+        // next segment's TMA writes (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     }
 }
 
@@ -642,8 +761,22 @@ cudaError_t launch_attention_shared(const AttnArgs &x, cudaStream_t st) {
     a.out_dtype = x.out_dtype; a.L = x.L; a.scale = x.scale;
     a.part_o = part_o; a.part_lse = part_lse; a.row_cnt = row_cnt; a.status = x.status;
     a.O = x.O; a.LSE = x.LSE;
-    cudaError_t e = ensure_func_attr((const void *)k_attend_shared, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     shd::SMEM);
+    ShdMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+#if SQZ_SHD_TMA
+    {
+        const uint64_t rf = (uint64_t)x.H * x.L, ru = (uint64_t)x.B * x.H * (x.n_u > 0 ? x.n_u : 1);
+        if (encode_tmap_bf16_2d(&maps.kp, x.Kp, shd::D, rf, 64, 1) != 0 ||
+            encode_tmap_bf16_2d(&maps.vp, x.Vp, shd::D, rf, 64, 1) != 0)
+            return cudaErrorInvalidValue;
+        const void *ku = x.Ku && x.n_u > 0 ? x.Ku : x.Kp, *vu = x.Vu && x.n_u > 0 ? x.Vu : x.Vp;
+        if (encode_tmap_bf16_2d(&maps.ku, ku, shd::D, x.Ku && x.n_u > 0 ? ru : rf, 64, 1) != 0 ||
+            encode_tmap_bf16_2d(&maps.vu, vu, shd::D, x.Vu && x.n_u > 0 ? ru : rf, 64, 1) != 0)
+            return cudaErrorInvalidValue;
+    }
+#endif
+    auto kern = x.B <= 8 ? k_attend_shared<1> : k_attend_shared<2>;
+    cudaError_t e = ensure_func_attr((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, shd::SMEM);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
@@ -652,7 +785,7 @@ cudaError_t launch_attention_shared(const AttnArgs &x, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_attend_shared, a);
+    return cudaLaunchKernelEx(&cfg, kern, a, maps);
 }
 
 }  // namespace sqz

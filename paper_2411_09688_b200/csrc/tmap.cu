@@ -43,6 +43,22 @@ int encode_tmap_bf16_3d(CUtensorMap *m, const void *ptr, const uint64_t dims[3],
     return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
+// Contiguous bf16 matrix [rows][cols], boxes of box_rows x box_cols, 128-byte
+// swizzle (box_cols * 2 = 128 for the swizzle span), out-of-bounds reads = 0.
+int encode_tmap_bf16_2d(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint32_t box_cols,
+                        uint32_t box_rows) {
+    encode_fn fn = resolve();
+    if (!fn) return -1;
+    const cuuint64_t d[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t b[2] = {box_cols, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), d, strides, b, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : (int)r;
+}
+
 }  // namespace sqz
 
 // ---------------------------------------------------------------------------
