@@ -891,6 +891,8 @@ def main():
                          "prefill measured in the same run as its `prefill` object")
     ap.add_argument("--no-prefill", action="store_true",
                     help="default run: skip the cfg3 prefill object")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="default run: skip the cfg4 object (extra_configs)")
     ap.add_argument("--decode-path", default="calls", choices=["step", "calls"],
                     help="decode: the two calls (lookup, then sparse attention, chained by "
                          "programmatic dependent launch; default: measured fastest) or one "
@@ -979,6 +981,20 @@ def main():
                 "phases_ms", "whole_step", "roofline", "e2e", "gpu_launches", "clocks", "parity",
                 "cpu_baseline", "scaling")
         line["prefill"] = {k: pl[k] for k in keep if k in pl}
+    if with_prefill and not args.no_extra:
+        # the 128K hierarchical batch-8 decode (cfg4: batch-shared attention, tensor-core
+        # K-means) in the same run, so the driver's line carries it too
+        import torch
+
+        torch.cuda.empty_cache()
+        xargs = argparse.Namespace(**vars(args))
+        xargs.config = "cfg4"
+        xargs.steps = min(args.steps, 30)
+        xl = run_gpu(xargs, dict(CONFIGS["cfg4"]), rank, world, local_rank)
+        keep = ("metric", "value", "unit", "ms_per_step", "higher_is_better", "dtype", "config",
+                "phases_ms", "whole_step", "roofline", "e2e", "gpu_launches", "clocks", "parity",
+                "selection_quality", "scaling", "steps")
+        line["extra_configs"] = {"cfg4": {k: xl[k] for k in keep if k in xl}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
