@@ -205,8 +205,12 @@ template <bool PERSIST> struct SegIter {
     }
 };
 
-template <typename T, int D, bool PERSIST>
-__global__ void __launch_bounds__(NCT) k_attend(AttnArgs a, int rows) {
+// MINB: CTAs per SM the register allocation must allow.  3 (<= 170 registers)
+// for short per-CTA streams; 4 (128 registers, a few spilled prologue values)
+// for long ones, where the extra warps' bytes in flight pay (cfg5 attention
+// 274 -> 262 us; cfg2 +0.4 us, so it stays at 3 there)
+template <typename T, int D, bool PERSIST, int MINB>
+__global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
     constexpr int G = D / 8;          // lanes per key row (8 elements each)
     constexpr int KPW = 32 / G;       // key rows per warp instruction
     constexpr int KR = keys_per_round<T>();
@@ -461,7 +465,9 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     const long long max_cost = (long long)rows * (a.L + a.n_u + SEG_KW);
     if (a.n_q == 1 && rows <= 8192 && max_cost < 0x7fffffffLL) {
         const size_t dsm = (size_t)(2 * rows + 1) * sizeof(int);
-        auto kern = k_attend<T, D, true>;
+        // long per-CTA streams (upper bound of the selected keys: rows x L) take the
+        // 4-CTAs-per-SM variant
+        auto kern = (long long)rows * a.L >= (1LL << 24) ? k_attend<T, D, true, 4> : k_attend<T, D, true, 3>;
         if (dsm > 48 * 1024) {
             cudaError_t e = ensure_func_attr((const void *)kern,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
@@ -474,7 +480,7 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     }
     cfg.gridDim = dim3(rows, a.max_chunks);
     cfg.dynamicSmemBytes = 0;
-    return cudaLaunchKernelEx(&cfg, k_attend<T, D, false>, a, rows);
+    return cudaLaunchKernelEx(&cfg, k_attend<T, D, false, 3>, a, rows);
 }
 
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st) {
