@@ -83,7 +83,7 @@ int lookup_qtile() { return QT; }
 // --------------------------------------------------------------------------
 __device__ __forceinline__ void tile_scan(bool sel, int n, int &pos, int &kpre, int &tot_c,
                                           int &tot_k) {
-    __shared__ int s_wc[NW], s_wk[NW];
+    __shared__ int s_wc[32], s_wk[32];  // up to 32 warps (blockDim.x / 32)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const unsigned bal = __ballot_sync(FULL, sel);
     const int wpre = __popc(bal & ((1u << lane) - 1u));
@@ -1212,6 +1212,263 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
     SQZ_TRACE_AT(g_trace_pl, 5);
 }
 
+// --------------------------------------------------------------------------
+// Warp-specialised prefill lookup (TMA tables: full tables or gathered candidate
+// lists).  Same arithmetic and outputs as k_prefill_lookup_tc; the roles:
+//   warp 8      TMA producer: the Q tile once, then the C tiles of pass 1 and
+//               pass 2 through a 3-stage ring;
+//   warp 9      MMA issuer: tile t (S = Q C^T in pass 1, S^T = C Q^T in pass 2)
+//               into TMEM buffer t % 4 (4 x 128 columns);
+//   warps 0-3   epilogue group 0 (even tiles), warps 4-7 group 1 (odd tiles):
+//               a thread owns a whole TMEM lane (128 columns) of its tiles, so
+//               the two groups' exponentials overlap each other and the MMAs
+//               without a CTA-wide barrier per tile.
+// Pass 1 leaves each group a partial (m, D) per query row; they are folded
+// (group 0 tiles then group 1 -- a fixed order) before pass 2 needs the LSE.
+// --------------------------------------------------------------------------
+constexpr int PW_NT = 320;
+
+template <int D, bool GATHERED>
+__global__ void __launch_bounds__(PW_NT, 1) k_prefill_lookup_ws(LookupShape s, LevelArgs lv,
+                                                                const __grid_constant__ PlMaps maps) {
+    constexpr int HB = PL_T * 128;                 // one 64-column half of a 128-row tile
+    constexpr uint32_t TILE = PL_T * D * 2;        // 32 KB at d = 128
+    constexpr int NST = 3;                         // C ring stages
+    constexpr uint32_t IDESC = idesc_bf16(128, PL_T, false);
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const uint32_t sQ = smem_u32(sm), sC = sQ + TILE;
+    __shared__ __align__(8) uint64_t c_full[NST], c_empty[NST], acc_full[4], acc_empty[4], q_full;
+    __shared__ uint32_t s_tmem;
+    __shared__ __align__(16) float s_nw[2][2][PL_T];  // per group, double-buffered tile weights
+    __shared__ int s_rid[2][2][PL_T];
+    __shared__ float2 s_md[2][PL_T];
+    __shared__ __align__(16) float s_lse[PL_T];
+    __shared__ int s_last;
+
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int qt = blockIdx.x, bh = blockIdx.y, h = bh % s.H;
+    const int t0 = qt * PL_T, c = lv.c;
+    const int32_t *N = lv.N + (size_t)h * c;
+    const int nrows = GATHERED ? ldcg(lv.n_rows + bh) : c;
+    const int32_t *rows = GATHERED ? lv.rows + (size_t)bh * lv.row_stride : nullptr;
+    const int ntile = (nrows + PL_T - 1) / PL_T;
+    const int total = 2 * ntile;
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&c_full[i], 1);
+            mbar_init(&c_empty[i], 1);
+        }
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], 4);
+        }
+        mbar_init(&q_full, 1);
+        mbar_fence_init();
+    }
+    if (warp == 9) tmem_alloc(&s_tmem, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 8) {
+        // ======================= TMA producer =======================
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&q_full, TILE);
+#pragma unroll
+            for (int hb = 0; hb < D / 64; ++hb) tma_load_3d(sQ + hb * HB, &maps.q, hb * 64, t0, bh, &q_full);
+            for (int t = 0; t < total; ++t) {
+                const int st = t % NST;
+                mbar_wait(&c_empty[st], ((t / NST) & 1) ^ 1);
+                mbar_arrive_expect_tx(&c_full[st], TILE);
+#pragma unroll
+                for (int hb = 0; hb < D / 64; ++hb)
+                    tma_load_3d(sC + st * TILE + hb * HB, &maps.c, hb * 64, (t % ntile) * PL_T,
+                                GATHERED ? bh : h, &c_full[st]);
+            }
+        }
+    } else if (warp == 9) {
+        // ======================= MMA issuer =======================
+        mbar_wait(&q_full, 0);
+        tc_fence_after();
+        for (int t = 0; t < total; ++t) {
+            const int st = t % NST, buf = t & 3;
+            mbar_wait(&c_full[st], (t / NST) & 1);
+            mbar_wait(&acc_empty[buf], ((t >> 2) & 1) ^ 1);
+            tc_fence_after();
+            const bool p0 = t < ntile;  // pass 1: S = Q C^T; pass 2: S^T = C Q^T
+            const uint32_t ca = sC + st * TILE;
+            const uint32_t a_base = p0 ? sQ : ca, b_base = p0 ? ca : sQ;
+            if (lane == 0) {
+#pragma unroll
+                for (int ks = 0; ks < D / 16; ++ks) {
+                    const uint32_t off = (ks >> 2) * HB + (ks & 3) * 32;
+                    umma_bf16(tmem + buf * 128, sdesc_sw128(a_base + off, 16, 1024),
+                              sdesc_sw128(b_base + off, 16, 1024), IDESC, ks > 0);
+                }
+                umma_commit(&c_empty[st]);
+                umma_commit(&acc_full[buf]);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ======================= epilogue groups =======================
+        const int grp = warp >> 2, quarter = warp & 3;
+        const int r = quarter * 32 + lane;              // TMEM lane = M row of this thread
+        const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+        const int gtid = tid & 127, bar_id = 1 + grp;   // named barrier of the group (128 threads)
+        // this group's tiles: t = grp, grp + 2, ...; prefetch the first tile's metadata
+        auto meta = [&](int t, int &rid, float &nw) {
+            rid = -1;
+            nw = 0.f;
+            if (t < total) {
+                const int jj = (t % ntile) * PL_T + gtid;
+                if (jj < nrows) {
+                    rid = GATHERED ? ldcg(rows + jj) : jj;
+                    nw = (float)__ldg(N + rid);
+                }
+            }
+        };
+        int rid_pf;
+        float nw_pf;
+        meta(grp, rid_pf, nw_pf);
+        float m = -INFINITY, Dsum = 0.f;
+        bool lse_ready = false;
+        int k = 0;  // this group's tile count (metadata slot k & 1)
+        for (int t = grp; t < total; t += 2, ++k) {
+            const int buf = t & 3, tl = t % ntile, slot = k & 1;
+            s_nw[grp][slot][gtid] = nw_pf;
+            s_rid[grp][slot][gtid] = rid_pf;
+            named_bar(bar_id, 128);  // this tile's metadata visible; slot k - 2 readers done
+            meta(t + 2, rid_pf, nw_pf);
+            if (t >= ntile && !lse_ready) {
+                // pass 1 complete in both groups: fold the two groups' (m, D), fixed order
+                s_md[grp][r] = make_float2(m, Dsum);
+                named_bar(3, 256);
+                if (grp == 0) {
+                    float mm = s_md[0][r].x, dd = s_md[0][r].y;
+                    md_combine(mm, dd, s_md[1][r].x, s_md[1][r].y);
+                    const bool ok = t0 + r < s.n_q;
+                    float lse = mm + logf(dd);  // -inf when no row
+                    if (ok) {
+                        lv.rowlse[(size_t)bh * s.n_q + t0 + r] = lse;
+                        if (lv.dbg_lse) lv.dbg_lse[(size_t)bh * s.n_q + t0 + r] = lse;
+                    }
+                    if (!ok || !(lse < INFINITY) || lse == -INFINITY) lse = INFINITY;  // p = 0
+                    s_lse[r] = lse;
+                }
+                named_bar(3, 256);
+                lse_ready = true;
+            }
+            mbar_wait(&acc_full[buf], (t >> 2) & 1);
+            tc_fence_after();
+            const float *nwb = s_nw[grp][slot];
+            if (t < ntile) {
+                // pass 1: thread = query row r; the 128 centroid columns of tile tl
+#pragma unroll 1
+                for (int hf = 0; hf < 2; ++hf) {
+                    float v0[32], v1[32];
+                    tmem_ld32(tmem + buf * 128 + lane_off + hf * 64, v0);
+                    tmem_ld32(tmem + buf * 128 + lane_off + hf * 64 + 32, v1);
+                    tmem_wait_ld();
+                    const int lim = nrows - tl * PL_T - hf * 64;
+                    float cmx = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        v0[j] = j < lim ? v0[j] * s.scale : -INFINITY;
+                        v1[j] = j + 32 < lim ? v1[j] * s.scale : -INFINITY;
+                        cmx = fmaxf(cmx, fmaxf(v0[j], v1[j]));
+                    }
+                    const float mn = fmaxf(m, cmx);
+                    if (mn != -INFINITY) {
+                        const float4 *nw4 = reinterpret_cast<const float4 *>(nwb + hf * 64);
+                        float a[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) a[u] = 0.f;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 w0 = nw4[j / 4], w1 = nw4[8 + j / 4];
+                            a[0] = fmaf(w0.x, exp_fast(v0[j] - mn), a[0]);
+                            a[1] = fmaf(w0.y, exp_fast(v0[j + 1] - mn), a[1]);
+                            a[2] = fmaf(w0.z, exp_fast(v0[j + 2] - mn), a[2]);
+                            a[3] = fmaf(w0.w, exp_fast(v0[j + 3] - mn), a[3]);
+                            a[4] = fmaf(w1.x, exp_fast(v1[j] - mn), a[4]);
+                            a[5] = fmaf(w1.y, exp_fast(v1[j + 1] - mn), a[5]);
+                            a[6] = fmaf(w1.z, exp_fast(v1[j + 2] - mn), a[6]);
+                            a[7] = fmaf(w1.w, exp_fast(v1[j + 3] - mn), a[7]);
+                        }
+                        Dsum = Dsum * expf(m - mn) + (((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
+                        m = mn;
+                    }
+                }
+            } else {
+                // pass 2: thread = centroid row r of tile tl; the 128 query columns
+                float tot = 0.f;
+#pragma unroll 1
+                for (int hf = 0; hf < 2; ++hf) {
+                    float v0[32], v1[32];
+                    tmem_ld32(tmem + buf * 128 + lane_off + hf * 64, v0);
+                    tmem_ld32(tmem + buf * 128 + lane_off + hf * 64 + 32, v1);
+                    tmem_wait_ld();
+                    const float4 *l4 = reinterpret_cast<const float4 *>(s_lse + hf * 64);
+                    float a[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a[u] = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 e0 = l4[j / 4], e1 = l4[8 + j / 4];
+                        a[0] += exp_fast(fmaf(v0[j], s.scale, -e0.x));
+                        a[1] += exp_fast(fmaf(v0[j + 1], s.scale, -e0.y));
+                        a[2] += exp_fast(fmaf(v0[j + 2], s.scale, -e0.z));
+                        a[3] += exp_fast(fmaf(v0[j + 3], s.scale, -e0.w));
+                        a[4] += exp_fast(fmaf(v1[j], s.scale, -e1.x));
+                        a[5] += exp_fast(fmaf(v1[j + 1], s.scale, -e1.y));
+                        a[6] += exp_fast(fmaf(v1[j + 2], s.scale, -e1.z));
+                        a[7] += exp_fast(fmaf(v1[j + 3], s.scale, -e1.w));
+                    }
+                    tot += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+                }
+                const int rid = s_rid[grp][slot][r];
+                if (rid >= 0) lv.colpart[((size_t)qt * s.B * s.H + bh) * c + rid] = tot;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        }
+        if (!lse_ready) {  // a group without pass-2 tiles still takes part in the fold
+            s_md[grp][r] = make_float2(m, Dsum);
+            named_bar(3, 256);
+            if (grp == 0) {
+                float mm = s_md[0][r].x, dd = s_md[0][r].y;
+                md_combine(mm, dd, s_md[1][r].x, s_md[1][r].y);
+                const bool ok = t0 + r < s.n_q;
+                float lse = mm + logf(dd);
+                if (ok) {
+                    lv.rowlse[(size_t)bh * s.n_q + t0 + r] = lse;
+                    if (lv.dbg_lse) lv.dbg_lse[(size_t)bh * s.n_q + t0 + r] = lse;
+                }
+                if (!ok || !(lse < INFINITY) || lse == -INFINITY) lse = INFINITY;
+                s_lse[r] = lse;  // the other group's pass-2 tiles read it
+            }
+            named_bar(3, 256);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 9) tmem_dealloc(tmem, 512);
+    // ---- the last CTA of this (b,h) averages the tiles and thresholds ----
+    if (tid == 0) {
+        const int tk = ticket_acq_rel(lv.tick + bh);
+        s_last = (tk == (int)gridDim.x - 1);
+        if (s_last) lv.tick[bh] = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    finalize_colpart<GATHERED>(lv, bh, h, nrows, gridDim.x, s.B * s.H, 1.0f / (float)s.n_q);
+}
+
 // the candidate rows of every (b,h), in list order, into a contiguous copy
 template <int D>
 __global__ void k_gather_cand(const __nv_bfloat16 *__restrict__ C, const int32_t *__restrict__ rows,
@@ -1259,8 +1516,24 @@ static cudaError_t launch_prefill_tc(const LookupShape &s, const __nv_bfloat16 *
             return cudaErrorInvalidValue;
     }
     dim3 grid((s.n_q + PL_T - 1) / PL_T, s.B * s.H);
-    kern<<<grid, PL_NT, PlSmem<D>::BYTES, st>>>(s, Q, lv, maps);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e;
+// warp-specialised kernel for TMA-fed unstaged lookups: correct, but measured
+// slower (cfg3 62.3 vs 58.8 us, cfg5p 6.18 vs 5.90 ms): with one CTA per SM the
+// 8 epilogue warps leave the xu pipe at 43% like the two-CTA kernel, and the
+// second wave of CTAs (256 on 148 SMs) costs more than the overlap gains -- off
+#ifndef SQZ_PL_WS
+#define SQZ_PL_WS 0
+#endif
+    if (SQZ_PL_WS && (!RL || GATHERED) && lv.phase == 0) {
+        auto kw = k_prefill_lookup_ws<D, GATHERED>;
+        constexpr int WBYTES = 4 * PL_T * D * 2 + 1024;  // Q + 3 C stages + alignment
+        e = ensure_func_attr((const void *)kw, cudaFuncAttributeMaxDynamicSharedMemorySize, WBYTES);
+        if (e != cudaSuccess) return e;
+        kw<<<grid, PW_NT, WBYTES, st>>>(s, lv, maps);
+    } else {
+        kern<<<grid, PL_NT, PlSmem<D>::BYTES, st>>>(s, Q, lv, maps);
+    }
+    e = cudaGetLastError();
     if (e == cudaSuccess && lv.phase != 1 && lv.exp_list) e = launch_expand(s, lv, st);
     return e;
 }
