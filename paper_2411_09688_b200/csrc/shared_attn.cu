@@ -35,7 +35,8 @@ namespace sqz {
 namespace shd {
 constexpr int D = 128;
 // measured on cfg4 (same box): 32-key tiles x 4 warps 240 us, 16 x 8 warps 245 us,
-// 16 x 6 warps x 4 stages 254 us, 16 x 4 warps x 6 stages 291 us
+// 16 x 6 warps x 4 stages 254 us, 16 x 4 warps x 6 stages 291 us; 32 x 6 x 2
+// stages 248 us, 32 x 5 x 2 stages 241 us
 #ifndef SQZ_SHD_NW
 #define SQZ_SHD_NW 4
 #endif
@@ -47,6 +48,7 @@ constexpr int D = 128;
 #endif
 constexpr int NW = SQZ_SHD_NW;     // warps per CTA (one CTA per SM)
 constexpr int NT = NW * 32;
+static_assert(NT >= D, "the row merge gives one thread per head-dim column");
 constexpr int TK = SQZ_SHD_TK;     // keys per warp tile (16 or 32)
 constexpr int NST = SQZ_SHD_NST;   // ring stages per warp
 // K/V tiles by TMA row gathers (tile::gather4, 4 rows x 128 B per op) instead of
