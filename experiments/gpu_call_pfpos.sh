@@ -1,0 +1,7 @@
+python -m paper_2411_09688_b200.build > /dev/null 2>&1
+timeout 900 python -m pytest -q -x tests/test_gpu_parity.py tests/test_gpu_fullsize.py -k "prefill or cfg3 or cfg5p" 2>&1 | tail -2 > gpurun_out/pfpos.log
+for r in 1 2; do
+  timeout 300 python bench.py --config cfg3 --no-cpu-baseline --no-parity 2>&1 | grep '^{"metric"' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg3', d['value'], d['phases_ms']['lookup'], d['phases_ms']['sparse_attention'], d['roofline']['frac'])" >> gpurun_out/pfpos.log
+done
+timeout 300 python bench.py --config cfg3 --no-cpu-baseline --no-parity --sel-runs 2>&1 | grep '^{"metric"' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg3 runs', d['value'], d['phases_ms']['lookup'], d['phases_ms']['sparse_attention'], d['roofline']['frac'])" >> gpurun_out/pfpos.log
+timeout 1200 python bench.py --config cfg5p --no-cpu-baseline --no-parity --steps 5 --kmeans-iters-set 3 2>&1 | grep '^{"metric"' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('cfg5p', d['value'], d['phases_ms']['lookup'], d['phases_ms']['sparse_attention'], d['roofline']['frac'])" >> gpurun_out/pfpos.log
