@@ -484,10 +484,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
         torch.cuda.empty_cache()
     comm = sqz.Comm(rank, world) if shard == "clusters" else None
 
+    # reductions travel on the device with NCCL, on the host with gloo (shared-GPU dry run)
+    red_dev = "cpu" if world > 1 and dist.get_backend() == "gloo" else dev
+
     def allsum(x):
         if world == 1 or shard not in ("heads", "clusters"):
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t)
         return float(t.item())
 
@@ -778,7 +781,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         quality = selection_quality(sqz, idx, Qt, Kp, scale, T, T1, min(n_inputs, 8), B, dev, T0=T0)
     # ---- max over ranks ----
     if world > 1:
-        tt = torch.tensor([t_step, t_look, t_attn, t_e2e, t_eager], device=dev)
+        tt = torch.tensor([t_step, t_look, t_attn, t_e2e, t_eager], device=red_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step, t_look, t_attn, t_e2e, t_eager = tt.tolist()
     hbm, bf16, peak_kind = load_peaks()
@@ -804,7 +807,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
             ach = bytes_attn / (t_attn * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                     "frac": round(ach / hbm, 4),
-                    "traffic": traffic_for(args.config, "sparse_attention"),
+                    "traffic": traffic_for(args.config, "sparse_attention_shared" if shared_attn
+                                           else "sparse_attention"),
                     "kernel": ("k_attend_shared (batch-shared union pass, mma.sync tiles, fused merge); "
                                "bytes = union of the B selections per head" if shared_attn else
                                "k_attend (persistent split-KV over equal key ranges + fused merge)"),
@@ -931,6 +935,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # dry run of the N-rank code path on ONE GPU (all ranks on device 0, gloo process
+    # group): checks the sharding, calibration and max-over-ranks logic before a real
+    # multi-GPU run; the numbers of such a run are not measurements
+    shared_gpu = os.environ.get("SQZ_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local_rank = 0
     metric, unit, hib = metric_of(cfg)
 
     if args.impl == "reference":
@@ -956,7 +966,10 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_gpu(args, cfg, rank, world, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         value, sample, cores, _ = cpu_oracle_run(cfg)
