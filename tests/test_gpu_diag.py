@@ -89,3 +89,33 @@ def test_diagnostics_match_oracle(case):
                 (b, h, g["recall"][b, h], ref["recall"][b, h], amb)
     if ret >= 1.0:
         assert np.abs(g["recall"] - 1).max() <= 1e-6 and np.abs(g["mass_sel"] - 1).max() <= 2e-5
+
+
+def test_diagnostics_three_level_index():
+    """The diagnostics read the finest-level selection of any hierarchy: a three-level
+    index gives the oracle's masses and recall on the GPU's selection."""
+    from paper_2411_09688_b200 import sqz
+
+    H, L, d, c2, c1, c0, B = 2, 5000, 128, 200, 40, 6, 2
+    fc = synth.fixed_context(H, L, d, c2, dtype=synth.BF16, seed=621, G1=c1)
+    g, Kp, Vp, _ = sqz.cluster_keys(sqz.to_device(fc.K), sqz.to_device(fc.V), c2,
+                                    torch.from_numpy(synth.kmeans_init(H, L, c2, seed=622)).cuda(), c1,
+                                    torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=623)).cuda(),
+                                    max_iters=15, c0=c0,
+                                    init0=torch.from_numpy(synth.kmeans_init(H, c1, c0, seed=624)).cuda())
+    Q = synth.decode_queries(fc.mix, B, seed=625)
+    Qd = sqz.to_device(Q)
+    scale = 1.0 / np.sqrt(d)
+    sel = sqz.centroid_lookup(g, Qd, scale, 2e-5, 1e-4, T0=1e-4)
+    out = sqz.selection_diagnostics(g, Qd, Kp, sel, scale, 0.01, 1e-3)
+    torch.cuda.synchronize()
+    perm, ko = g.perm.cpu().numpy(), g.key_off.cpu().numpy()
+    mask = np.zeros((B, H, L), bool)
+    cl, n = sel.clusters.cpu().numpy(), sel.n_clusters.cpu().numpy()
+    for b in range(B):
+        for h in range(H):
+            for i in cl[b, h, :n[b, h]]:
+                mask[b, h, perm[h][ko[h, i]:ko[h, i + 1]]] = True
+    ref = oracle.diagnostics(oracle.to_f64(Q), oracle.to_f64(fc.K), mask, scale, 0.01, 1e-3)
+    for key in ("skew", "mass_sel", "mass_ideal", "mass_T"):
+        assert np.abs(out[key].cpu().numpy() - ref[key]).max() <= 2e-5, key

@@ -160,24 +160,35 @@ def _build_mode(fc, c2, init2, iters, mode, c1=0, init1=None):
     return idx, Kp, Vp
 
 
-@pytest.mark.parametrize("levels", [1, 2])
+@pytest.mark.parametrize("levels", [1, 2, 3])
 def test_tensor_core_assignment_separated_identical_to_oracle(levels):
     """NEXT-3: the tcgen05 split-bf16 assignment reproduces the oracle's partitions
     and tables bit for bit on the separated mixture (same shared init)."""
     from paper_2411_09688_b200 import sqz
 
     H, L, d, G = 2, 3000, 128, 16
-    c1 = 4 if levels == 2 else 0
+    c1 = 4 if levels >= 2 else 0
+    c0 = 2 if levels == 3 else 0
     fc = synth.fixed_context(H, L, d, G, dtype=synth.BF16, seed=41, sep=True, G1=c1)
     init2 = np.stack([[np.nonzero(fc.labels[h] == g)[0][0] for g in range(G)] for h in range(H)])
     init1 = np.stack([np.arange(c1) for _ in range(H)]).astype(np.int64) if c1 else None
-    g, Kp, _ = _build_mode(fc, G, init2.astype(np.int64), 50, sqz.KMEANS_TENSOR, c1, init1)
-    r = oracle.build_index(fc.K, G, init2, c1, init1)
+    init0 = np.stack([np.arange(c0) for _ in range(H)]).astype(np.int64) if c0 else None
+    K, V = sqz.to_device(fc.K), sqz.to_device(fc.V)
+    g, Kp, Vp, _ = sqz.cluster_keys(K, V, G, torch.from_numpy(init2.astype(np.int64)).cuda(), c1,
+                                    None if init1 is None else torch.from_numpy(init1).cuda(),
+                                    max_iters=50, assign_mode=sqz.KMEANS_TENSOR, c0=c0,
+                                    init0=None if init0 is None else torch.from_numpy(init0).cuda())
+    torch.cuda.synchronize()
+    sqz.index_validate(g)
+    r = oracle.build_index(fc.K, G, init2, c1, init1, c0=c0, init0=init0)
     assert np.array_equal(_np(g.perm), r.perm) and np.array_equal(_np(g.key_off), r.key_off)
     assert np.array_equal(_np(g.C2), oracle.encode(r.C2, synth.BF16))
-    if levels == 2:
+    if levels >= 2:
         assert np.array_equal(_np(g.child_off), r.child_off)
         assert np.array_equal(_np(g.C1), oracle.encode(r.C1, synth.BF16))
+    if levels == 3:
+        assert np.array_equal(_np(g.child_off0), r.child_off0)
+        assert np.array_equal(_np(g.C0), oracle.encode(r.C0, synth.BF16))
 
 
 @pytest.mark.parametrize("d", [64, 128])

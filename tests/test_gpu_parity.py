@@ -463,3 +463,52 @@ def test_three_level_lookup_and_attention(case):
     torch.cuda.synchronize()
     fp32 = dt == synth.F32
     _check_attention(P, sel, O, LSE, scale, prefill, B, 1e-4 if fp32 else 2e-2, None if fp32 else 5e-3)
+
+
+def test_batch_shared_empty_selections():
+    """Batch-shared decode edges: thresholds that select no fixed key leave each query
+    its own user keys only (exactly the oracle's user-only attention); with no user
+    KV either, partial mode returns the identity (LSE = -inf, O = 0) for every row."""
+    sqz = _sqz()
+    P = oracle_problem(3, 2500, 128, 60, 0, synth.BF16, seed=611, B=4, n_u=9)
+    scale = 1.0 / np.sqrt(128)
+    t = _device(P)
+    sel = sqz.centroid_lookup(t["idx"], t["Q"], scale, 0.9)  # S_i <= 1/N_i < 0.9: nothing selected
+    torch.cuda.synchronize()
+    assert int(sel.n_keys.sum()) == 0
+    O, LSE = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, t["Ku"], t["Vu"], scale)
+    torch.cuda.synchronize()
+    Oref, Lref, _ = oracle.attention(oracle.to_f64(P["Q"]), oracle.to_f64(P["fc"].K),
+                                     oracle.to_f64(P["fc"].V), np.zeros((4, 3, 2500), bool),
+                                     oracle.to_f64(P["Ku"]), oracle.to_f64(P["Vu"]), False, scale)
+    assert np.abs(O.float().cpu().numpy() - Oref).max() <= 2e-2
+    assert np.abs(LSE.cpu().numpy() - Lref).max() <= 1e-3
+    O2, L2 = sqz.sparse_attention(t["Q"], t["Kp"], t["Vp"], t["idx"], sel, None, None, scale, partial=True)
+    torch.cuda.synchronize()
+    assert torch.isneginf(L2).all() and (O2.float() == 0).all()
+
+
+def test_three_level_with_T0_zero_equals_two_levels():
+    """On the GPU: a three-level index with T0 = 0 keeps every Level-0 cluster, so its
+    selection equals the two-level lookup on the same Level-1 / Level-2 tables."""
+    sqz = _sqz()
+    H, L, d, c2, c1, c0, B = 2, 5000, 128, 200, 40, 6, 3
+    fc = synth.fixed_context(H, L, d, c2, dtype=synth.BF16, seed=612, G1=c1)
+    g, Kp, Vp, _ = sqz.cluster_keys(sqz.to_device(fc.K), sqz.to_device(fc.V), c2,
+                                    torch.from_numpy(synth.kmeans_init(H, L, c2, seed=613)).cuda(), c1,
+                                    torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=614)).cuda(),
+                                    max_iters=15, c0=c0,
+                                    init0=torch.from_numpy(synth.kmeans_init(H, c1, c0, seed=615)).cuda())
+    two = sqz.Index(H=H, d=d, L=L, c2=c2, dtype=g.dtype, C2=g.C2, N2=g.N2, key_off=g.key_off, perm=g.perm,
+                    c1=c1, C1=g.C1, N1=g.N1, child_off=g.child_off)
+    Q = sqz.to_device(synth.decode_queries(fc.mix, B, seed=616))
+    scale = 1.0 / np.sqrt(d)
+    for T, T1 in ((1e-4, 2e-4), (3e-5, 0.0)):
+        a = sqz.centroid_lookup(g, Q, scale, T, T1, T0=0.0)
+        b = sqz.centroid_lookup(two, Q, scale, T, T1)
+        torch.cuda.synchronize()
+        assert torch.equal(a.n_clusters, b.n_clusters) and torch.equal(a.n_keys, b.n_keys)
+        for bb in range(B):
+            for h in range(H):
+                n = int(a.n_clusters[bb, h])
+                assert torch.equal(a.clusters[bb, h, :n], b.clusters[bb, h, :n])
