@@ -201,6 +201,9 @@ __device__ void finalize_colpart(const LevelArgs &lv, int bh, int h, int nrows, 
 constexpr int EXP_ROWS = 32;
 __global__ void __launch_bounds__(NT) k_expand_ranges(LevelArgs lv, int H) {
     asm volatile("griddepcontrol.launch_dependents;");
+    // launched programmatically behind the lookup: its CTAs start during the
+    // lookup's tail and wait here for the finished selection
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int bh = blockIdx.y, h = bh % H;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = ldcg(lv.n_list + bh);
@@ -215,9 +218,16 @@ __global__ void __launch_bounds__(NT) k_expand_ranges(LevelArgs lv, int H) {
 }
 
 static cudaError_t launch_expand(const LookupShape &s, const LevelArgs &lv, cudaStream_t st) {
-    dim3 grid((lv.c + EXP_ROWS - 1) / EXP_ROWS, s.B * s.H);
-    k_expand_ranges<<<grid, NT, 0, st>>>(lv, s.H);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((lv.c + EXP_ROWS - 1) / EXP_ROWS, s.B * s.H);
+    cfg.blockDim = dim3(NT);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_expand_ranges, lv, s.H);
 }
 
 // --------------------------------------------------------------------------
