@@ -634,9 +634,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
     def attend(q):
         attend_into(q, O, LSE)
 
-    # decode through sqz_decode_step (one call; the fused single-level kernel)
-    # unless the fixed context is sharded (the exchange needs the two calls)
-    use_step = cfg["mode"] == "decode" and comm is None and args.decode_path == "step"
+    # decode through sqz_decode_step (one call: for one single-level query row the
+    # lookup hands each row's selection to the attention kernel through flags and
+    # attends the user KV itself) unless the fixed context is sharded (the
+    # exchange needs the two calls)
+    step_applies = cfg["mode"] == "decode" and comm is None and idx.levels == 1 and B == 1
+    use_step = step_applies and args.decode_path in ("step", "auto")
     step_ws = None
     if use_step:
         nb = sqz.ctypes.c_size_t(0)
@@ -792,18 +795,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         value = t_step * 1e3 / tokens
         e2e_v = t_e2e * 1e3 / tokens
         step_bytes = bytes_lookup + bytes_attn
-        if use_step and idx.levels == 1:
-            # the fused kernel IS the step: its algorithmic bytes over the
-            # graph-replayed step time (which also holds the ~6 us event/launch floor)
-            ach = step_bytes / (t_step * 1e-3) / 1e9
-            roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                    "frac": round(ach / hbm, 4),
-                    "traffic": traffic_for(args.config, "decode_step"),
-                    "kernel": "k_decode_step (fused lookup + threshold + sparse attention, one "
-                              "persistent cooperative launch)",
-                    "peak_kind": f"{peak_kind} copy bandwidth",
-                    "bytes_per_launch": int(step_bytes)}
-        else:
+        if True:  # the attention kernel of the two-call pass (the same k_attend the step runs)
             ach = bytes_attn / (t_attn * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                     "frac": round(ach / hbm, 4),
@@ -838,8 +830,6 @@ def run_gpu(args, cfg, rank, world, local_rank):
     else:  # stats, then per level: fold + select (+ next level's stats)
         n_look = 1 + levels * (1 + per_select) + (levels - 1)
     launches = K_ * (n_look + 1 + (1 if comm else 0) + (1 if shared_attn else 0))  # + k_union
-    if use_step and idx.levels == 1:
-        launches = K_  # one k_decode_step per step
     metric, unit, hib = metric_of(cfg)
     line = {
         "metric": metric, "value": round(value, 3), "unit": unit, "n_gpus": world,
@@ -897,11 +887,11 @@ def main():
                     help="default run: skip the cfg3 prefill object")
     ap.add_argument("--no-extra", action="store_true",
                     help="default run: skip the cfg4 object (extra_configs)")
-    ap.add_argument("--decode-path", default="calls", choices=["step", "calls"],
-                    help="decode: the two calls (lookup, then sparse attention, chained by "
-                         "programmatic dependent launch; default: measured fastest) or one "
-                         "sqz_decode_step call (the fused single-level kernel: 65-70 us vs 52.7 us "
-                         "on cfg2, DESIGN.md section 7)")
+    ap.add_argument("--decode-path", default="auto", choices=["auto", "step", "calls"],
+                    help="decode: one sqz_decode_step call (flag hand-off from the lookup to the "
+                         "attention kernel, user KV attended by the lookup; B = 1 single level) or "
+                         "the two calls (lookup, then sparse attention, chained by programmatic "
+                         "dependent launch); auto = the step where it applies")
     ap.add_argument("--flush", default="write", choices=["write", "write+read"],
                     help="L2 flush between timed steps (see run_gpu)")
     ap.add_argument("--no-parity", action="store_true",

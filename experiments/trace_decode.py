@@ -38,15 +38,19 @@ for it in range(6):
         rflush.sum()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    sqz.centroid_lookup(idx, Q, 1 / np.sqrt(d), T, sel=sel)
-    sqz.sparse_attention(Q, Kp, Vp, idx, sel, Ku, Vu, O=O, LSE=LSE)
+    if os.environ.get("SQZ_STEP") == "1":  # the decode-step hand-off path
+        sqz.decode_step(idx, Q, Kp, Vp, Ku, Vu, 1 / np.sqrt(d), T, sel=sel, O=O, LSE=LSE)
+    else:
+        sqz.centroid_lookup(idx, Q, 1 / np.sqrt(d), T, sel=sel)
+        sqz.sparse_attention(Q, Kp, Vp, idx, sel, Ku, Vu, O=O, LSE=LSE)
     e1.record()
     torch.cuda.synchronize()
 tl = np.zeros(2048 * 8, np.uint64)
 ta = np.zeros(2048 * 8, np.uint64)
 lib.sqz_trace_look(tl.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(tl.nbytes))
 lib.sqz_trace_attn(ta.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(ta.nbytes))
-tl = tl.reshape(2048, 8)[:256].astype(np.float64)
+tl = tl.reshape(2048, 8).astype(np.float64)
+tl = tl[tl[:, 0] >= tl[:, 0].max() - 200e3]  # the last launch's CTAs only
 ta = ta.reshape(2048, 8).astype(np.float64)
 ta = ta[ta[:, 0] > 0]
 t0 = tl[:, 0].min()
@@ -54,9 +58,11 @@ print(f"retention {ret}: event step time {e0.elapsed_time(e1) * 1e3:.1f} us; k =
 def st(name, v):
     v = (v - t0) / 1e3
     print(f"  {name:38s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us")
-for i, n in enumerate(["lookup start", "lookup scan done", "lookup compaction done (pre-barrier)", "lookup cluster.sync 2",
-                       "lookup writes done", "lookup end"]):
-    st(n, tl[:, i])
+for i, n in [(0, "lookup start"), (1, "lookup scan done"), (6, "lookup local (m,D) done"),
+             (7, "lookup cluster.sync 1 + fold"), (2, "lookup compaction done (pre-barrier)"),
+             (3, "lookup cluster.sync 2"), (4, "lookup writes done"), (5, "lookup end")]:
+    if (tl[:, i] > 0).all():
+        st(n, tl[:, i])
 for i, n in [(0, "attn entry"), (1, "attn after griddep wait"), (2, "attn prologue done"),
              (6, "attn first segment done"), (4, "attn streaming done (last seg)"), (5, "attn end")]:
     col = ta[:, i]

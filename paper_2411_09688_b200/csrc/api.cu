@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/sqz.h"
@@ -519,11 +520,15 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
 }
 
 // ------------------------------------------------------------------ decode step
-// workspace regions: [attention | fused step | lookup].  The attention region
+// workspace regions: [attention | user chunks | lookup].  The attention region
 // comes first so that its status word sits where sqz_attention_status(ws)
-// reads it; the fused kernel reports empty rows through the same word.
-static size_t step_region_bytes(const sqz_index *idx, int B, int n_u) {
-    return (decode_step_ws_bytes(B, idx->H, idx->c2, n_u, idx->d) + 255) & ~(size_t)255;
+// reads it.  The user-chunk region holds the partials of the user KV the
+// attention kernel attends before it waits for the lookup ([B*H, n_chunks, d]
+// + [B*H, n_chunks] fp32).
+static int user_chunks(int n_u) { return (n_u + attention_user_chunk() - 1) / attention_user_chunk(); }
+static size_t hand_region_bytes(const sqz_index *idx, int B, int n_u) {
+    const size_t BH = (size_t)B * idx->H, nch = (size_t)user_chunks(n_u);
+    return (BH * nch * (idx->d + 1) * sizeof(float) + 255) & ~(size_t)255;
 }
 
 int sqz_decode_step_workspace(const sqz_index *idx, int32_t B, int32_t n_u, size_t *ws_bytes) {
@@ -532,7 +537,7 @@ int sqz_decode_step_workspace(const sqz_index *idx, int32_t B, int32_t n_u, size
     if (B < 1 || n_u < 0) return fail(SQZ_ERR_INVALID_ARG, "B = %d must be >= 1 and n_u = %d >= 0", B, n_u);
     if (!ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes is NULL");
     *ws_bytes = 256 + ((attn_carve(idx, B, 1, n_u, nullptr).bytes + 511) & ~(size_t)255) +
-                step_region_bytes(idx, B, n_u) + ((lookup_carve(idx, B, 1, nullptr).bytes + 511) & ~(size_t)255);
+                hand_region_bytes(idx, B, n_u) + ((lookup_carve(idx, B, 1, nullptr).bytes + 511) & ~(size_t)255);
     return SQZ_OK;
 }
 
@@ -551,37 +556,62 @@ int sqz_decode_step(const sqz_index *idx, const void *Q, int32_t B, const void *
     if (ap->out_dtype != SQZ_F32 && ap->out_dtype != SQZ_BF16)
         return fail(SQZ_ERR_INVALID_ARG, "out_dtype = %d is not a sqz_dtype", ap->out_dtype);
     if (!O || !LSE) return fail(SQZ_ERR_INVALID_ARG, "O and LSE must be non-NULL");
+    if (!sel->n_keys || !sel->clusters || !sel->n_clusters || !sel->key_pref)
+        return fail(SQZ_ERR_INVALID_ARG, "sel->clusters, n_clusters, n_keys, key_pref are required");
     size_t need = 0;
     sqz_decode_step_workspace(idx, B, n_u, &need);
     if (ws_bytes < need) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes = %zu < required %zu", ws_bytes, need);
-    // regions: attention (its status word first, as sqz_attention_status reads
-    // it), fused step, lookup
     char *base = align_ws(ws);
     const size_t attn_b = (attn_carve(idx, B, 1, n_u, nullptr).bytes + 511) & ~(size_t)255;
-    char *step_ws = base + attn_b;
-    char *look_ws = step_ws + step_region_bytes(idx, B, n_u);
-    const bool debug = sel->dbg_S || sel->dbg_S1 || sel->dbg_lse || sel->l1_surv;
+    char *hand_ws = base + attn_b;
+    char *look_ws = hand_ws + hand_region_bytes(idx, B, n_u);
+    const size_t look_b = (lookup_carve(idx, B, 1, nullptr).bytes + 511) & ~(size_t)255;
+    const bool debug = sel->dbg_S || sel->dbg_S1 || sel->dbg_lse || sel->l1_surv || sel->dbg_S0 ||
+                       sel->l0_surv;
     cudaStream_t st = (cudaStream_t)stream;
-    if (idx->levels == 1 && !debug && decode_step_rows_ok(B, idx->H, idx->c2, idx->L) &&
-        idx->L_total == 0) {
-        StepLaunch l;
-        std::memset(&l, 0, sizeof(l));
-        l.Q = Q; l.C = idx->C2; l.Kp = Kp; l.Vp = Vp; l.Ku = Ku; l.Vu = Vu;
-        l.N = idx->N2; l.koff = idx->key_off;
-        l.B = B; l.H = idx->H; l.c = idx->c2; l.n_u = n_u; l.d = idx->d; l.dtype = idx->dtype;
-        l.out_dtype = ap->out_dtype; l.partial = ap->partial ? 1 : 0;
-        l.L = idx->L; l.scale = lp->scale; l.T = lp->T;
-        l.ws = step_ws;
-        l.clusters = sel->clusters; l.key_pref = sel->key_pref; l.n_clusters = sel->n_clusters;
-        l.n_keys = sel->n_keys; l.key_idx = sel->key_idx;
-        l.O = O; l.LSE = LSE;
-        l.status = reinterpret_cast<int32_t *>(base);
-        cudaError_t e = launch_decode_step(l, st);
-        if (e != cudaSuccess) return cuda_fail(e, "decode step launch");
+    const long long H = idx->H;
+    // One query row, single level, unsharded: the lookup kernel is limited to
+    // 84 registers (two of its CTAs leave room for an attention CTA on the SM),
+    // and the attention kernel -- launched behind it -- attends the
+    // selection-independent user KV in chunks on those early CTAs before it
+    // waits for the lookup; the chunks' partials join each row's merge.
+    if (idx->levels == 1 && B == 1 && !debug && idx->L_total == 0 && n_u > 0 &&
+        H * (idx->L + n_u + 1024) < 0x7fffffffLL && H <= 8192) {
+        static const bool no_user = std::getenv("SQZ_STEP_NO_USER") != nullptr;  // A/B knob
+        const size_t BH = (size_t)B * H;
+        const int nch = no_user ? 0 : user_chunks(n_u);
+        float *up_o = reinterpret_cast<float *>(hand_ws);
+        float *up_lse = up_o + BH * nch * idx->d;
+        LookupWs w = lookup_carve(idx, B, 1, look_ws);
+        LookupShape s{B, idx->H, 1, idx->d, idx->dtype, lp->scale};
+        lookup_levels(idx, lp, sel, w);
+        w.l2.lean = 1;
+        cudaError_t e = launch_lookup_level(s, Q, w.l2, st);
+        if (e != cudaSuccess) return cuda_fail(e, "decode step lookup");
+        AttnWs aw = attn_carve(idx, B, 1, n_u, base);
+        AttnArgs a;
+        std::memset(&a, 0, sizeof(a));
+        a.Q = Q; a.Kp = Kp; a.Vp = Vp; a.Ku = Ku; a.Vu = Vu;
+        a.n_keys = sel->n_keys; a.key_idx = sel->key_idx;
+        a.sel_cl = sel->clusters; a.sel_pref = sel->key_pref; a.sel_n = sel->n_clusters;
+        a.key_off = idx->key_off; a.c2 = idx->c2;
+        a.B = B; a.H = idx->H; a.n_q = 1; a.n_u = n_u; a.d = idx->d; a.dtype = idx->dtype;
+        a.causal = 0; a.partial = ap->partial ? 1 : 0; a.out_dtype = ap->out_dtype;
+        a.L = idx->L; a.scale = ap->scale;
+        a.kch = aw.kch; a.max_chunks = aw.max_chunks;
+        a.part_o = aw.part_o; a.part_lse = aw.part_lse; a.status = aw.status; a.row_cnt = aw.row_cnt;
+        a.sched = aw.status + 1;
+        a.cut = aw.cut;
+        a.O = O; a.LSE = LSE;
+        if (nch > 0) {
+            a.up_o = up_o; a.up_lse = up_lse;
+            a.up_n = nch;
+        }
+        e = launch_attention(a, st);
+        if (e != cudaSuccess) return cuda_fail(e, "decode step attention");
         return SQZ_OK;
     }
     // the two calls, on sub-workspaces of this one
-    const size_t look_b = (lookup_carve(idx, B, 1, nullptr).bytes + 511) & ~(size_t)255;
     rc = sqz_centroid_lookup(idx, Q, B, 1, lp, sel, look_ws, look_b, stream);
     if (rc) return rc;
     return sqz_sparse_attention(Q, B, 1, Kp, Vp, idx, sel, Ku, Vu, n_u, ap, O, LSE, base, attn_b, stream);

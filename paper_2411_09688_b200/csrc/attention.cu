@@ -48,8 +48,14 @@ constexpr int MIN_KEYS = 256;           // minimum keys per persistent CTA
 #define SQZ_DEC_SEG_KW 128
 #endif
 constexpr int SEG_KW = SQZ_DEC_SEG_KW;
+// decode step: user keys per chunk attended before the wait for the lookup
+#ifndef SQZ_USER_CHUNK
+#define SQZ_USER_CHUNK 256
+#endif
+constexpr int USER_CHUNK = SQZ_USER_CHUNK;
 
 int attention_kch(int n_q) { return n_q == 1 ? 256 : 1024; }
+int attention_user_chunk() { return USER_CHUNK; }
 int attention_max_parts(int64_t L, int n_u, int n_q) {
     const int kch = attention_kch(n_q);
     const int grid_parts = (int)((L + n_u + kch - 1) / kch);
@@ -68,7 +74,7 @@ __device__ __forceinline__ RowInfo row_info(const AttnArgs &a, int row, int nkf 
     const int t = row % a.n_q;
     r.nkf = nkf >= 0 ? nkf : ldcg(a.n_keys + r.bh);
     int vis = a.causal ? t + a.n_u - a.n_q + 1 : a.n_u;
-    r.nu = max(0, min(vis, a.n_u));
+    r.nu = a.up_o ? 0 : max(0, min(vis, a.n_u));  // decode step: the user chunks hold them
     return r;
 }
 
@@ -80,25 +86,30 @@ struct Seg {
 
 // Merge of one row's partials by the CTA: O = sum_p e^(lse_p - M) o_p / L,
 // LSE = M + log L.  Thread k < D owns output column k; the
-// partials are read 16 at a time (their lse values and o columns in the same
+// partials are read 32 at a time (their lse values and o columns in the same
 // memory round trip) with an online rescale, so the merge is one pass without
 // block barriers.  Every thread forms the same weights in the same order (the
 // result does not depend on which CTA merges or when).
 template <int D>
 __device__ void merge_row(const AttnArgs &a, int row, int P) {
-    constexpr int MB = 16;
+    constexpr int MB = 32;
     const int tid = threadIdx.x;
     if (tid >= D) return;
     const float *lse = a.part_lse + (size_t)row * a.max_chunks;
     const float *op = a.part_o + (size_t)row * a.max_chunks * D + tid;
+    // decode step: the user-chunk partials follow the P fixed-key ones
+    const int U = a.up_o ? a.up_n : 0;
+    const float *ulse = U ? a.up_lse + (size_t)row * U : nullptr;
+    const float *uop = U ? a.up_o + (size_t)row * U * D + tid : nullptr;
     float M = -INFINITY, L = 0.f, acc = 0.f;
-    for (int p0 = 0; p0 < P; p0 += MB) {
+    for (int p0 = 0; p0 < P + U; p0 += MB) {
         float lv[MB], ov[MB];
 #pragma unroll
         for (int j = 0; j < MB; ++j) {
-            const bool in = p0 + j < P;
-            lv[j] = in ? ldcg(lse + p0 + j) : -INFINITY;
-            ov[j] = in ? ldcg(op + (size_t)(p0 + j) * D) : 0.f;
+            const int p = p0 + j;
+            const bool in = p < P, inu = !in && p < P + U;
+            lv[j] = in ? ldcg(lse + p) : inu ? ldcg(ulse + (p - P)) : -INFINITY;
+            ov[j] = in ? ldcg(op + (size_t)p * D) : inu ? ldcg(uop + (size_t)(p - P) * D) : 0.f;
         }
         float mt = M;
 #pragma unroll
@@ -205,12 +216,20 @@ template <bool PERSIST> struct SegIter {
     }
 };
 
-// MINB: CTAs per SM the register allocation must allow.  3 (<= 170 registers)
-// for short per-CTA streams; 4 (128 registers, a few spilled prologue values)
-// for long ones, where the extra warps' bytes in flight pay (cfg5 attention
-// 274 -> 262 us; cfg2 +0.4 us, so it stays at 3 there)
-template <typename T, int D, bool PERSIST, int MINB>
-__global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
+// Streams the keys [a0, a1) of row `row`'s stream (stream key k < ri.nkf: the
+// selected fixed key key_idx[k] (or read from the run-length selection), else
+// user key k - nkf) and writes the CTA's normalised partial -- o/l to
+// o_dst[0, D) and the natural-log LSE to *lse_dst (-inf, o = 0 if empty).
+// Every thread of the CTA calls it; no barrier after the partial stores.
+//
+// Data movement: each warp streams KR keys per round; a group of G = D/8 lanes
+// reads one key row with 16-byte non-allocating loads, the K and V rows of all
+// KR keys are in flight before the first FMA, and the next round's key
+// positions are prefetched while they are.
+template <typename T, int D>
+__device__ __forceinline__ void stream_partial(const AttnArgs &a, int row, const RowInfo &ri, int a0,
+                                               int a1, float *o_dst, float *lse_dst, float *s_m,
+                                               float *s_l, float *s_o) {
     constexpr int G = D / 8;          // lanes per key row (8 elements each)
     constexpr int KPW = 32 / G;       // key rows per warp instruction
     constexpr int KR = keys_per_round<T>();
@@ -218,23 +237,186 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
     constexpr int LPS = G / NS;       // lanes holding each reduced key
     constexpr int LG_G = G == 16 ? 4 : 3;
     constexpr int LG_NS = NS == 16 ? 4 : NS == 8 ? 3 : NS == 4 ? 2 : NS == 2 ? 1 : 0;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane / G, sub = lane % G;
+    const int myslot = sub >> (LG_G - LG_NS);
+    const T *Kf = reinterpret_cast<const T *>(a.Kp) + (size_t)ri.h * a.L * D;
+    const T *Vf = reinterpret_cast<const T *>(a.Vp) + (size_t)ri.h * a.L * D;
+    const T *Ku = reinterpret_cast<const T *>(a.Ku) + (size_t)ri.bh * a.n_u * D;
+    const T *Vu = reinterpret_cast<const T *>(a.Vu) + (size_t)ri.bh * a.n_u * D;
+    const int32_t *kidx = a.key_idx ? a.key_idx + (size_t)ri.bh * a.L : nullptr;
+    RunList rl;
+    RunWin rw;
+    if (!kidx && ri.nkf > 0) {
+        rl.cl = a.sel_cl + (size_t)ri.bh * a.c2;
+        rl.pref = a.sel_pref + (size_t)ri.bh * a.c2;
+        rl.koff = a.key_off + (size_t)ri.h * (a.c2 + 1);
+        rl.n = ldcg(a.sel_n + ri.bh);
+        rl.nkf = ri.nkf;
+        rw.J = 0;
+        rw.end = -1;  // empty: the first cover loads
+        rw.p0 = rw.p1 = 0x7fffffff;
+    }
+    // source position of stream key k (this lane's key of a warp round starting
+    // at stream key j): >= 0 fixed key row, < 0 user key -1-u.  Warp-collective.
+    auto pos_of = [&](int j, int k) -> int {
+        if (!kidx) {
+            const int kmax = min(min(j + KR, a1), ri.nkf) - 1;
+            if (j <= kmax) {  // warp-uniform
+                runwin_cover(rw, rl, j, kmax, lane);
+                const int p = runwin_pos(rw, min(k, kmax));
+                if (k <= kmax) return p;
+            }
+            if (k >= a1) return 0;
+            return -1 - (k - ri.nkf);
+        }
+        if (k >= a1) return 0;
+        return k < ri.nkf ? ldcg(kidx + k) : -1 - (k - ri.nkf);
+    };
+    // lane l (< KR) holds the position of key l of this warp's current round;
+    // the first positions are requested before the query row, so the two
+    // loads share one memory round trip
+    int j0 = a0 + warp * KR;
+    int pos_cur = pos_of(j0, j0 + (lane & (KR - 1)));
+    float q[8];
+    load8(reinterpret_cast<const T *>(a.Q) + (size_t)row * D + sub * 8, q);
+    const float sc = a.scale * LOG2E;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q[k] *= sc;
+    float m_run = -INFINITY, l_lane = 0.f, o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = 0.f;
+    for (; j0 < a1; j0 += NCW * KR) {
+        const int nk = min(KR, a1 - j0);
+        Raw<T> kr[NS], vr[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const int kk = s * KPW + g;
+            const int pos = __shfl_sync(FULL, pos_cur, kk);
+            if (kk < nk) {
+                const T *kp = pos >= 0 ? Kf + (size_t)pos * D : Ku + (size_t)(-1 - pos) * D;
+                const T *vp = pos >= 0 ? Vf + (size_t)pos * D : Vu + (size_t)(-1 - pos) * D;
+                ld_raw(kr[s], kp + sub * 8);
+                ld_raw(vr[s], vp + sub * 8);
+            } else {
+#pragma unroll
+                for (int i = 0; i < (int)(sizeof(kr[s].v) / sizeof(uint4)); ++i)
+                    kr[s].v[i] = vr[s].v[i] = make_uint4(0, 0, 0, 0);
+            }
+        }
+        // prefetch the next round's positions while this round's rows are in flight
+        pos_cur = pos_of(j0 + NCW * KR, j0 + NCW * KR + (lane & (KR - 1)));
+        float v[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            float f[8];
+            cvt(kr[s], f);
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc = fmaf(q[k], f[k], acc);
+            v[s] = acc;
+        }
+        float z = group_transpose_reduce<NS, G>(v, lane);
+        if (myslot * KPW + g >= nk) z = -INFINITY;
+        const float mx = warp_max(z);
+        const float m_new = fmaxf(m_run, mx);
+        const float alpha = fast_exp2(m_run - m_new);  // m_run = -inf -> 0
+        const float p = fast_exp2(z - m_new);          // z = -inf -> 0
+        l_lane = l_lane * alpha + p;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] *= alpha;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const float ps = __shfl_sync(FULL, p, g * G + s * LPS);
+            if (s * KPW + g < nk) {
+                float f[8];
+                cvt(vr[s], f);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) o[k] = fmaf(ps, f[k], o[k]);
+            }
+        }
+        m_run = m_new;
+    }
+    // ---- fold the key groups, then the warps ----
+#pragma unroll
+    for (int s2 = G; s2 < 32; s2 <<= 1)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] += __shfl_xor_sync(FULL, o[k], s2);
+    const float l_w = warp_sum(l_lane) * (1.0f / LPS);
+    if (lane == 0) { s_m[warp] = m_run; s_l[warp] = l_w; }
+    if (g == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s_o[warp * D + sub * 8 + k] = o[k];
+    }
+    __syncthreads();
+    if (tid < D) {
+        float M = -INFINITY;
+        for (int w = 0; w < NCW; ++w) M = fmaxf(M, s_m[w]);
+        float L = 0.f, O = 0.f;
+        for (int w = 0; w < NCW; ++w) {
+            const float e = (s_m[w] == -INFINITY) ? 0.f : exp2f(s_m[w] - M);
+            L += s_l[w] * e;
+            O += s_o[w * D + tid] * e;
+        }
+        o_dst[tid] = L > 0.f ? O / L : 0.f;
+        if (tid == 0) *lse_dst = L > 0.f ? (M + log2f(L)) * LN2 : -INFINITY;
+    }
+}
 
+// MINB: CTAs per SM the register allocation must allow.  3 (<= 170 registers)
+// for short per-CTA streams; 4 (128 registers, a few spilled prologue values)
+// for long ones, where the extra warps' bytes in flight pay (cfg5 attention
+// 274 -> 262 us; cfg2 +0.4 us, so it stays at 3 there)
+template <typename T, int D, bool PERSIST, int MINB>
+__global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
     extern __shared__ __align__(16) int dyn_i[];
     int *s_pref = dyn_i;             // [rows + 1] (persistent)
     int *s_nkf = dyn_i + rows + 1;   // [rows]     (persistent)
     __shared__ float s_m[NCW], s_l[NCW], s_o[NCW * D];
     __shared__ int s_last;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
 
     SQZ_TRACE_AT(g_trace_attn, 0);
+    // decode step (a.up_o): the user KV does not depend on the selection, so the
+    // CTAs resident beside the lookup's CTAs attend it now, in USER_CHUNK-key
+    // chunks spread statically over the first up_ctas CTAs, each chunk's
+    // partial counted in the high bits of the row's ticket word
+    if (PERSIST && a.up_o && (int)blockIdx.x < a.up_ctas) {
+        const int nch = rows * a.up_n;
+        for (int c = blockIdx.x; c < nch; c += a.up_ctas) {
+            const int r = c / a.up_n, j = c % a.up_n;
+            RowInfo ri;
+            ri.bh = r;  // n_q == 1
+            ri.h = r % a.H;
+            ri.nkf = 0;
+            ri.nu = a.n_u;
+            const int a0 = j * USER_CHUNK;
+            stream_partial<T, D>(a, r, ri, a0, min(a.n_u, a0 + USER_CHUNK),
+                                 a.up_o + ((size_t)r * a.up_n + j) * D, a.up_lse + (size_t)r * a.up_n + j,
+                                 s_m, s_l, s_o);
+            __syncthreads();
+            // the row's ticket word counts user chunks in its high 16 bits
+            if (tid == 0) red_release_add(a.row_cnt + r, 1 << 16);
+        }
+    }
     // the selection comes from the preceding lookup kernel (programmatic
     // dependent launch: the launch itself overlaps its tail)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     SQZ_TRACE_AT(g_trace_attn, 1);
+    // a row with no fixed-key segment: wait for its user chunks (long done in
+    // practice), then clear its ticket word for the next step
+    auto user_ready = [&](int r) {  // CTA-uniform
+        if (tid == 0) {
+            while ((ld_acquire(a.row_cnt + r) >> 16) < a.up_n) __nanosleep(32);
+            a.row_cnt[r] = 0;
+        }
+        __syncthreads();
+    };
 
     if (PERSIST) {
         // exclusive prefix of the row stream lengths (rows <= a few thousand)
         __shared__ int s_ws[NCW];
+        const int warp = tid >> 5;
         if (tid == 0) s_pref[0] = 0;
         for (int base = 0; base < rows; base += NCT) {
             __syncthreads();
@@ -261,7 +443,15 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
         }
         __syncthreads();
         for (int r = blockIdx.x; r < rows; r += gridDim.x)
-            if (s_pref[r + 1] == s_pref[r]) empty_row<D>(a, r);
+            if (s_pref[r + 1] == s_pref[r]) {
+                if (a.up_o) {  // no selected fixed key: the user-chunk partials alone
+                    user_ready(r);
+                    merge_row<D>(a, r, 0);
+                    __syncthreads();
+                } else {
+                    empty_row<D>(a, r);
+                }
+            }
     } else {
         if (blockIdx.y == 0 && row_info(a, blockIdx.x).total() == 0) empty_row<D>(a, blockIdx.x);
     }
@@ -271,8 +461,6 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
     SegIter<PERSIST> it;
     it.init(a, s_pref, rows);
     Seg sg;
-    const int g = lane / G, sub = lane % G;
-    const int myslot = sub >> (LG_G - LG_NS);
 #ifdef SQZ_TRACE
     int tr_nseg = 0, tr_nmerge = 0, tr_keys = 0;
 #endif
@@ -282,146 +470,35 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
         tr_keys += sg.a1 - sg.a0;
 #endif
         const RowInfo ri = row_info(a, sg.row, PERSIST ? s_nkf[sg.row] : -1);
-        const T *Kf = reinterpret_cast<const T *>(a.Kp) + (size_t)ri.h * a.L * D;
-        const T *Vf = reinterpret_cast<const T *>(a.Vp) + (size_t)ri.h * a.L * D;
-        const T *Ku = reinterpret_cast<const T *>(a.Ku) + (size_t)ri.bh * a.n_u * D;
-        const T *Vu = reinterpret_cast<const T *>(a.Vu) + (size_t)ri.bh * a.n_u * D;
-        const int32_t *kidx = a.key_idx ? a.key_idx + (size_t)ri.bh * a.L : nullptr;
-        RunList rl;
-        RunWin rw;
-        if (!kidx) {
-            rl.cl = a.sel_cl + (size_t)ri.bh * a.c2;
-            rl.pref = a.sel_pref + (size_t)ri.bh * a.c2;
-            rl.koff = a.key_off + (size_t)ri.h * (a.c2 + 1);
-            rl.n = ldcg(a.sel_n + ri.bh);
-            rl.nkf = ri.nkf;
-            rw.J = 0;
-            rw.end = -1;  // empty: the first cover loads
-            rw.p0 = rw.p1 = 0x7fffffff;
-        }
-        // source position of stream key k (this lane's key of a warp round starting
-        // at stream key j): >= 0 fixed key row, < 0 user key -1-u.  Warp-collective.
-        auto pos_of = [&](int j, int k) -> int {
-            if (!kidx) {
-                const int kmax = min(min(j + KR, sg.a1), ri.nkf) - 1;
-                if (j <= kmax) {  // warp-uniform
-                    runwin_cover(rw, rl, j, kmax, lane);
-                    const int p = runwin_pos(rw, min(k, kmax));
-                    if (k <= kmax) return p;
-                }
-                if (k >= sg.a1) return 0;
-                return -1 - (k - ri.nkf);
-            }
-            if (k >= sg.a1) return 0;
-            return k < ri.nkf ? ldcg(kidx + k) : -1 - (k - ri.nkf);
-        };
-        // lane l (< KR) holds the position of key l of this warp's current round;
-        // the first positions are requested before the query row, so the two
-        // loads share one memory round trip
-        int j0 = sg.a0 + warp * KR;
-        int pos_cur = pos_of(j0, j0 + (lane & (KR - 1)));
-        float q[8];
-        load8(reinterpret_cast<const T *>(a.Q) + (size_t)sg.row * D + sub * 8, q);
-        const float sc = a.scale * LOG2E;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) q[k] *= sc;
-        float m_run = -INFINITY, l_lane = 0.f, o[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = 0.f;
-        for (; j0 < sg.a1; j0 += NCW * KR) {
-            const int nk = min(KR, sg.a1 - j0);
-            Raw<T> kr[NS], vr[NS];
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                const int kk = s * KPW + g;
-                const int pos = __shfl_sync(FULL, pos_cur, kk);
-                if (kk < nk) {
-                    const T *kp = pos >= 0 ? Kf + (size_t)pos * D : Ku + (size_t)(-1 - pos) * D;
-                    const T *vp = pos >= 0 ? Vf + (size_t)pos * D : Vu + (size_t)(-1 - pos) * D;
-                    ld_raw(kr[s], kp + sub * 8);
-                    ld_raw(vr[s], vp + sub * 8);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < (int)(sizeof(kr[s].v) / sizeof(uint4)); ++i)
-                        kr[s].v[i] = vr[s].v[i] = make_uint4(0, 0, 0, 0);
-                }
-            }
-            // prefetch the next round's positions while this round's rows are in flight
-            pos_cur = pos_of(j0 + NCW * KR, j0 + NCW * KR + (lane & (KR - 1)));
-            float v[NS];
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                float f[8];
-                cvt(kr[s], f);
-                float acc = 0.f;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) acc = fmaf(q[k], f[k], acc);
-                v[s] = acc;
-            }
-            float z = group_transpose_reduce<NS, G>(v, lane);
-            if (myslot * KPW + g >= nk) z = -INFINITY;
-            const float mx = warp_max(z);
-            const float m_new = fmaxf(m_run, mx);
-            const float alpha = fast_exp2(m_run - m_new);  // m_run = -inf -> 0
-            const float p = fast_exp2(z - m_new);          // z = -inf -> 0
-            l_lane = l_lane * alpha + p;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) o[k] *= alpha;
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                const float ps = __shfl_sync(FULL, p, g * G + s * LPS);
-                if (s * KPW + g < nk) {
-                    float f[8];
-                    cvt(vr[s], f);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) o[k] = fmaf(ps, f[k], o[k]);
-                }
-            }
-            m_run = m_new;
-        }
+        const size_t slot = (size_t)sg.row * a.max_chunks + sg.slot;
+        stream_partial<T, D>(a, sg.row, ri, sg.a0, sg.a1, a.part_o + slot * D, a.part_lse + slot, s_m,
+                             s_l, s_o);
         SQZ_TRACE_AT(g_trace_attn, 4);
 #ifdef SQZ_TRACE
         if (tr_nseg == 1) SQZ_TRACE_AT(g_trace_attn, 6);
 #endif
-        // ---- segment epilogue: fold key groups, then the warps ----
-#pragma unroll
-        for (int s2 = G; s2 < 32; s2 <<= 1)
-#pragma unroll
-            for (int k = 0; k < 8; ++k) o[k] += __shfl_xor_sync(FULL, o[k], s2);
-        const float l_w = warp_sum(l_lane) * (1.0f / LPS);
-        if (lane == 0) { s_m[warp] = m_run; s_l[warp] = l_w; }
-        if (g == 0) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) s_o[warp * D + sub * 8 + k] = o[k];
-        }
-        __syncthreads();
-        if (tid < D) {
-            float M = -INFINITY;
-            for (int w = 0; w < NCW; ++w) M = fmaxf(M, s_m[w]);
-            float L = 0.f, O = 0.f;
-            for (int w = 0; w < NCW; ++w) {
-                const float e = (s_m[w] == -INFINITY) ? 0.f : exp2f(s_m[w] - M);
-                L += s_l[w] * e;
-                O += s_o[w * D + tid] * e;
-            }
-            const size_t slot = (size_t)sg.row * a.max_chunks + sg.slot;
-            a.part_o[slot * D + tid] = L > 0.f ? O / L : 0.f;
-            if (tid == 0) a.part_lse[slot] = L > 0.f ? (M + log2f(L)) * LN2 : -INFINITY;
-        }
         // the CTA that completes a row's last segment merges its partials (the
         // barrier orders the CTA's partial stores before thread 0's release fence)
         __syncthreads();
         if (tid == 0) {
+            // ticket word: fixed-key partials counted in the low 16 bits, the
+            // decode step's user chunks (released before the wait) in the high ones
 #if SQZ_ATT_ACQREL
             // one acquire-release atomic: releases the CTA's partial (ordered before
             // it by the barrier), and acquires the other segments' partials for the merge
-            const int t = ticket_acq_rel(a.row_cnt + sg.row);
+            int t = ticket_acq_rel(a.row_cnt + sg.row);
 #else
             __threadfence();
-            const int t = atomicAdd(a.row_cnt + sg.row, 1);
+            int t = atomicAdd(a.row_cnt + sg.row, 1);
 #endif
-            s_last = (t == sg.nparts - 1);
-            if (s_last) a.row_cnt[sg.row] = 0;
+            s_last = ((t & 0xffff) == sg.nparts - 1);
+            if (s_last) {
+                while ((t >> 16) < a.up_n) {  // a user chunk still out (not seen in practice)
+                    __nanosleep(32);
+                    t = ld_acquire(a.row_cnt + sg.row);
+                }
+                a.row_cnt[sg.row] = 0;
+            }
         }
         __syncthreads();
         if (s_last) {
@@ -463,7 +540,9 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     // memory: shapes whose total cost could reach 2^31 (e.g. dense attention over
     // 1M keys with B*H >= 2048) take the 2-D split-KV grid instead.
     const long long max_cost = (long long)rows * (a.L + a.n_u + SEG_KW);
-    if (a.n_q == 1 && rows <= 8192 && max_cost < 0x7fffffffLL) {
+    const bool persist = a.n_q == 1 && rows <= 8192 && max_cost < 0x7fffffffLL;
+    if (a.up_o && !persist) return cudaErrorInvalidValue;  // user chunks need the persistent grid
+    if (persist) {
         const size_t dsm = (size_t)(2 * rows + 1) * sizeof(int);
         // long per-CTA streams (upper bound of the selected keys: rows x L) take the
         // 4-CTAs-per-SM variant
@@ -476,7 +555,11 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
         const int occ = occupancy_blocks((const void *)kern, NCT, dsm);
         cfg.gridDim = dim3(std::min(device_sm_count() * occ, MAX_PERSIST_CTAS));
         cfg.dynamicSmemBytes = dsm;
-        return cudaLaunchKernelEx(&cfg, kern, a, rows);
+        AttnArgs a2 = a;
+        // user chunks go to the first CTAs, one per SM: those are dispatched
+        // first and fit beside the lean lookup's CTAs (k_lookup_decode MINB = 3)
+        a2.up_ctas = std::min((int)cfg.gridDim.x, device_sm_count());
+        return cudaLaunchKernelEx(&cfg, kern, a2, rows);
     }
     cfg.gridDim = dim3(rows, a.max_chunks);
     cfg.dynamicSmemBytes = 0;

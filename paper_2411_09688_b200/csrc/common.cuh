@@ -154,6 +154,18 @@ __device__ __forceinline__ int runwin_pos(const RunWin &w, int k) {
 // block barrier: the acquire-release atomic publishes the CTA's earlier global
 // writes (ordered before it by the barrier) and, for the last CTA, makes every
 // other CTA's writes visible to the reads that follow the next barrier.
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add(int *p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// spin (one thread) until *p >= v, acquiring what the releasing writers published
+__device__ __forceinline__ void spin_until_geq(const int *p, int v) {
+    while (ld_acquire(p) < v) __nanosleep(32);
+}
 __device__ __forceinline__ int ticket_acq_rel(int *p) {
     int t;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(p) : "memory");

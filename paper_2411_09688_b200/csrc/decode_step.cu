@@ -74,15 +74,6 @@ struct StepArgs {
     float *LSE;
 };
 
-__device__ __forceinline__ int ld_acquire(const int *p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void red_release_add(int *p, int v) {
-    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 // ---- virtual run list of one (b,h): the concatenation of its S parts' local
 // lists (part k's entries sit at loc_cl[bh*c + k*rpp + e], e < cnt_k, with key
 // offsets local to the part); FC/FK are the flat exclusive prefixes of the

@@ -57,6 +57,9 @@ struct LevelArgs {
     // bf16 prefill with a candidate list and many query tiles: the candidate
     // rows gathered contiguously per (b,h), [B*H][c][d] (TMA-loaded)
     void *cgather;
+    // decode step (sqz_decode_step): the kernel variant limited to 84 registers
+    // (3 CTAs' worth per SM), so that an attention CTA fits beside two of them
+    int32_t lean;
 };
 
 struct LookupShape {
@@ -96,6 +99,14 @@ struct AttnArgs {
     // batch-shared decode (shared_attn.cu): its workspace region and the N2 table
     void *shared_ws;
     const int32_t *N2;
+    // decode step (sqz_decode_step): the user KV is attended BEFORE the wait for
+    // the lookup, in USER_CHUNK-key chunks spread statically over the first
+    // up_ctas CTAs (resident beside the lookup's CTAs); chunk j of row r leaves
+    // its partial at up_o [rows, up_n, d] / up_lse [rows, up_n] and adds 1 << 16
+    // to the row's ticket word row_cnt[r] (its merger waits for up_n of them).
+    // Null up_o: the user keys are part of the rows' streams.
+    float *up_o, *up_lse;
+    int32_t up_n, up_ctas;
 };
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st);
 // shared_attn.cu: batch-shared decode attention over the per-head union of the
@@ -110,6 +121,7 @@ bool prefill_ws_applies(int d, int dtype, int n_q);       // routes to the persi
 size_t prefill_ws_part_rows(int B, int H, int n_q);       // its partial-buffer rows
 int prefill_split_keys();
 int attention_kch(int n_q);
+int attention_user_chunk();  // decode step: user keys per pre-wait chunk
 int attention_max_parts(int64_t L, int n_u, int n_q);
 cudaError_t launch_merge(int P, const float *O_parts, const float *LSE_parts, int64_t rows, int d,
                          void *O, float *LSE, int out_dtype, cudaStream_t st);

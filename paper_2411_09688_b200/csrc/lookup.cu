@@ -252,8 +252,10 @@ template <int NB> struct DecodeSmem {
 // fit one 16-row batch per warp takes U = 16 (every warp loads, fewer registers)
 template <typename T, int NB> constexpr int decode_u_max() { return (sizeof(T) == 2 && NB <= 2) ? 32 : 16; }
 
-template <typename T, int D, int NB, bool ROWLIST, int NC, bool SLIM, int U>
-__global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T *__restrict__ Q,
+// MINB = 3 (decode step, at most 84 registers): two lookup CTAs leave room on
+// the SM for one persistent attention CTA, which attends the user KV meanwhile
+template <typename T, int D, int NB, bool ROWLIST, int NC, bool SLIM, int U, int MINB = 2>
+__global__ void __launch_bounds__(NT, MINB) k_lookup_decode(LookupShape s, const T *__restrict__ Q,
                                                       LevelArgs lv, int rpc) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -302,7 +304,26 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
     __shared__ DecodeSmem<NB> sh;
     __shared__ float s_M[NB], s_lD[NB];
     __shared__ float s_wm[NW][NB], s_wd[NW][NB];
-
+    // Point-to-point exchange (phase 0): every CTA pushes its per-query (m, D)
+    // and later its (count, keys) into every peer's shared memory (st.async,
+    // counted in bytes on the receiver's mbarrier) instead of a cluster barrier
+    // followed by remote reads: a CTA waits only for the messages it needs.
+    __shared__ uint64_t s_xbar[2];
+    __shared__ float2 s_xmd[NC][NB];
+    __shared__ int2 s_xck[NC][NB];
+    const bool push = lv.phase == 0;
+    if (push) {
+        if (tid == 0) {
+            mbar_init(&s_xbar[0], 1);
+            mbar_init(&s_xbar[1], 1);
+            mbar_fence_init();
+            mbar_arrive_expect_tx(&s_xbar[0], (NC - 1) * NB * 8);
+            mbar_arrive_expect_tx(&s_xbar[1], (NC - 1) * NB * 8);
+        }
+        // a peer may push only after every CTA's barriers exist: arrive now,
+        // wait just before the first push (long after every CTA arrived)
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    }
     const int nrows = ROWLIST ? ldcg(lv.n_rows + (size_t)b0 * H + h) : c;
     // a candidate list is split evenly over the cluster by its actual length
     // (the smem is sized for the capacity rpc >= that share)
@@ -517,7 +538,27 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
             sh.md[i] = make_float2(M, dd);
         }
     }
-    cluster.sync();
+    if (!ROWLIST && !ONEQ) SQZ_TRACE_AT(g_trace_look, 6);
+    if (push) {
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (warp == 0) {  // lane r sends this CTA's partials to rank r
+            __syncwarp();  // sh.md was written by thread 0
+            if (lane < NC)
+                for (int i = 0; i < NB; ++i) {
+                    const float2 v = i < nb ? sh.md[i] : make_float2(-INFINITY, 0.f);
+                    if (lane == rank)
+                        s_xmd[rank][i] = v;
+                    else
+                        st_async_b64(&s_xmd[rank][i],
+                                     ((uint64_t)__float_as_uint(v.y) << 32) | __float_as_uint(v.x),
+                                     &s_xbar[0], lane);
+                }
+        }
+        __syncthreads();
+        if (warp < nb) mbar_wait_cluster(&s_xbar[0], 0);
+    } else {
+        cluster.sync();
+    }
     SQZ_TRACE_AT(g_trace_look, 2);
     // ---- global (m, D) per query: warp i reads the NC ranks' partials in
     // parallel (one DSMEM load per lane) and folds them with a butterfly, so
@@ -526,8 +567,7 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         const int i = warp;
         float mm = -INFINITY, dd = 0.f;
         if (lane < NC) {
-            const DecodeSmem<NB> *o = cluster.map_shared_rank(&sh, lane);
-            const float2 v = o->md[i];
+            const float2 v = push ? s_xmd[lane][i] : cluster.map_shared_rank(&sh, lane)->md[i];
             mm = v.x;
             dd = v.y;
         }
@@ -552,6 +592,7 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
     }
     }  // phase != 2
     __syncthreads();
+    if (!ROWLIST && !ONEQ) SQZ_TRACE_AT(g_trace_look, 7);
     // ---- threshold + ordered compaction of the CTA's rows ----
     const bool all = !(lv.T > 0.f);
     const float logT = all ? 0.f : logf(lv.T);
@@ -612,7 +653,24 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         if (tid == 0) { sh.cnt[i] = run; sh.keys[i] = runk; }
     }
     SQZ_TRACE_AT(g_trace_look, 2);  // (overwrites the fold time: compaction done, before the barrier)
-    cluster.sync();
+    if (push) {
+        if (warp == 0) {
+            __syncwarp();  // sh.cnt / sh.keys were written by thread 0
+            if (lane < NC)
+                for (int i = 0; i < NB; ++i) {
+                    const int2 v = i < nb ? make_int2(sh.cnt[i], sh.keys[i]) : make_int2(0, 0);
+                    if (lane == rank)
+                        s_xck[rank][i] = v;
+                    else
+                        st_async_b64(&s_xck[rank][i], ((uint64_t)(uint32_t)v.y << 32) | (uint32_t)v.x,
+                                     &s_xbar[1], lane);
+                }
+        }
+        __syncthreads();
+        if (warp < nb) mbar_wait_cluster(&s_xbar[1], 0);
+    } else {
+        cluster.sync();
+    }
     SQZ_TRACE_AT(g_trace_look, 3);
     // ---- cluster-wide offsets, then write the lists and expand the ranges ----
     __shared__ int s_oc[NB], s_ok[NB];
@@ -620,9 +678,15 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         const int i = warp;
         int cr = 0, kr = 0;
         if (lane < NC) {
-            const DecodeSmem<NB> *o = cluster.map_shared_rank(&sh, lane);
-            cr = o->cnt[i];
-            kr = o->keys[i];
+            if (push) {
+                const int2 v = s_xck[lane][i];
+                cr = v.x;
+                kr = v.y;
+            } else {
+                const DecodeSmem<NB> *o = cluster.map_shared_rank(&sh, lane);
+                cr = o->cnt[i];
+                kr = o->keys[i];
+            }
         }
         int ic = cr, ik = kr;
 #pragma unroll
@@ -644,8 +708,10 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
     }
     __syncthreads();
     // this CTA is done reading its peers' shared memory: arrive now, wait (so
-    // that its own stays alive for the peers' reads) only before exiting
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    // that its own stays alive for the peers' reads) only before exiting.  (The
+    // push exchange reads no remote memory, and every message addressed to this
+    // CTA has arrived: no barrier.)
+    if (!push) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     for (int i = 0; i < nb; ++i) {
         const int bh = (b0 + i) * H + h;
         const int oc = s_oc[i], ok = s_ok[i];
@@ -665,7 +731,7 @@ __global__ void __launch_bounds__(NT, 2) k_lookup_decode(LookupShape s, const T 
         }
     }
     SQZ_TRACE_AT(g_trace_look, 4);
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (!push) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     SQZ_TRACE_AT(g_trace_look, 5);
 }
 
@@ -842,6 +908,8 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
     auto kern = k_lookup_decode<T, D, NB, RL, NC, SLIM, UMAX>;
     if constexpr (UMAX == 32 && !RL)
         if (rpc <= NW * 16) kern = k_lookup_decode<T, D, NB, RL, NC, SLIM, 16>;
+    if constexpr (NB == 1 && !RL && !SLIM)
+        if (lv.lean && rpc <= NW * 16) kern = k_lookup_decode<T, D, NB, RL, NC, SLIM, 16, 3>;
     if (smem > 48 * 1024) {
         cudaError_t e = ensure_func_attr((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -870,26 +938,40 @@ static cudaError_t launch_decode_nc(const LookupShape &s, const T *Q, const Leve
 #ifndef SQZ_LOOKUP_MIN_CTAS
 #define SQZ_LOOKUP_MIN_CTAS 256
 #endif
+// the smallest cluster whose CTAs' rows fit 110 KB (2 CTAs per SM, which is
+// also the register limit) while the grid keeps >= 256 CTAs (one wave):
+// fewer, longer CTAs amortise the per-CTA phases (fold, compaction, cluster
+// exchanges), e.g. 2-CTA clusters for batched Level-2 lookups.  Returns NC;
+// slim = the 12 B/row layout (one query, large row space: keeps 8-CTA clusters).
+static int pick_nc(int NB, int rowspace, int units, bool &slim) {
+    slim = false;
+    const int min_ctas = SQZ_LOOKUP_MIN_CTAS;
+    auto ok = [&](int nc) {
+        return decode_smem_bytes(NB, (rowspace + nc - 1) / nc) <= 110 * 1024 && nc * units >= min_ctas;
+    };
+    if (ok(2)) return 2;
+    if (ok(4)) return 4;
+    if (ok(8) || decode_smem_bytes(NB, (rowspace + 7) / 8) <= 110 * 1024) return 8;
+    if (NB == 1 && decode_smem_bytes(1, (rowspace + 7) / 8, true) <= 110 * 1024) {
+        slim = true;
+        return 8;
+    }
+    return 16;
+}
+
 template <typename T, int D, int NB, bool RL>
 static cudaError_t launch_decode(const LookupShape &s, const T *Q, const LevelArgs &lv, int rowspace,
                                  int groups, cudaStream_t st) {
-    // the smallest cluster whose CTAs' rows fit 110 KB (2 CTAs per SM, which is
-    // also the register limit) while the grid keeps >= 256 CTAs (one wave):
-    // fewer, longer CTAs amortise the per-CTA phases (fold, compaction, cluster
-    // barriers), e.g. 2-CTA clusters for batched Level-2 lookups
-    const int units = s.H * groups;
-    auto ok = [&](int nc) {
-        return decode_smem_bytes(NB, (rowspace + nc - 1) / nc) <= 110 * 1024 && nc * units >= SQZ_LOOKUP_MIN_CTAS;
-    };
-    if (ok(2)) return launch_decode_nc<T, D, NB, RL, 2>(s, Q, lv, rowspace, groups, st);
-    if (ok(4)) return launch_decode_nc<T, D, NB, RL, 4>(s, Q, lv, rowspace, groups, st);
-    if (ok(8) || decode_smem_bytes(NB, (rowspace + 7) / 8) <= 110 * 1024)
-        return launch_decode_nc<T, D, NB, RL, 8>(s, Q, lv, rowspace, groups, st);
-    if constexpr (NB == 1) {  // one query, large row space: 12 B/row keeps 8-CTA clusters (one wave)
-        if (decode_smem_bytes(1, (rowspace + 7) / 8, true) <= 110 * 1024)
-            return launch_decode_nc<T, D, NB, RL, 8, true>(s, Q, lv, rowspace, groups, st);
+    bool slim;
+    switch (pick_nc(NB, rowspace, s.H * groups, slim)) {
+        case 2: return launch_decode_nc<T, D, NB, RL, 2>(s, Q, lv, rowspace, groups, st);
+        case 4: return launch_decode_nc<T, D, NB, RL, 4>(s, Q, lv, rowspace, groups, st);
+        case 8:
+            if constexpr (NB == 1)
+                if (slim) return launch_decode_nc<T, D, NB, RL, 8, true>(s, Q, lv, rowspace, groups, st);
+            return launch_decode_nc<T, D, NB, RL, 8>(s, Q, lv, rowspace, groups, st);
+        default: return launch_decode_nc<T, D, NB, RL, 16>(s, Q, lv, rowspace, groups, st);
     }
-    return launch_decode_nc<T, D, NB, RL, 16>(s, Q, lv, rowspace, groups, st);
 }
 
 // --------------------------------------------------------------------------

@@ -72,6 +72,29 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const void *map, int x
         "r"(smem_u32(bar))
         : "memory");
 }
+// ---- point-to-point DSMEM messages: a remote 8-byte store whose arrival is
+// counted (complete_tx bytes) on the receiving CTA's mbarrier ----
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t local_smem, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_b64(void *local_dst, uint64_t v, uint64_t *local_bar, uint32_t rank) {
+    const uint32_t dst = mapa_rank(smem_u32(local_dst), rank), bar = mapa_rank(smem_u32(local_bar), rank);
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(dst),
+                 "l"(v), "r"(bar)
+                 : "memory");
+}
+// wait for a phase completed by remote (cluster-scope) transactions
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 // named barrier over `n` threads (id 1..15; 0 is __syncthreads)
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");

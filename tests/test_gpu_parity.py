@@ -222,11 +222,30 @@ def test_decode_batch_shared(case):
     assert torch.equal(O, O2) and torch.equal(LSE, L2)
 
 
-@pytest.mark.parametrize("case", DECODE_CASES, ids=lambda c: c[0])
+# decode-step path (B = 1, single level, n_u > 0): a lean lookup grid, and the
+# attention kernel attends the user KV in chunks before it waits for the lookup
+STEP_CASES = [
+    # id, H, L, d, c2, c1, dtype, B, n_u, retention
+    ("step_bf16_d128_nu37", 4, 3000, 128, 97, 0, synth.BF16, 1, 37, 0.3),
+    ("step_bf16_d64_nu9", 3, 2500, 64, 61, 0, synth.BF16, 1, 9, 0.2),
+    ("step_fp32_d128", 3, 2000, 128, 64, 0, synth.F32, 1, 20, 0.3),
+    ("step_fp32_d64_nu1", 2, 1500, 64, 40, 0, synth.F32, 1, 1, 0.3),
+    # rows with no selected cluster (user keys only) and rows with nothing at all
+    ("step_bf16_sparse_nu0", 8, 700, 64, 50, 0, synth.BF16, 1, 0, 0.03),
+    ("step_bf16_sparse_nu5", 8, 700, 64, 50, 0, synth.BF16, 1, 5, 0.03),
+    # many user chunks per row (a ragged last chunk)
+    ("step_bf16_big_nu", 2, 2048, 128, 64, 0, synth.BF16, 1, 3000, 0.3),
+    # many heads, cfg2-like clusters
+    ("step_bf16_h32", 32, 4096, 128, 128, 0, synth.BF16, 1, 300, 0.3),
+]
+
+
+@pytest.mark.parametrize("case", DECODE_CASES + STEP_CASES, ids=lambda c: c[0])
 def test_decode_step(case):
-    """sqz_decode_step (one call: the fused single-level kernel, or the two calls for
-    hierarchical indexes) against the oracle: the selection under the band rule,
-    key_pref / key_idx consistent with it, and the attention on its key set."""
+    """sqz_decode_step (one call: the user-chunk path for one single-level query
+    row, else the two calls) against the oracle: the selection
+    under the band rule, key_pref / key_idx consistent with it, and the attention
+    on its key set."""
     sqz = _sqz()
     _, H, L, d, c2, c1, dt, B, n_u, ret = case
     P = oracle_problem(H, L, d, c2, c1, dt, seed=zlib.crc32(case[0].encode()) % 1000, B=B, n_u=n_u)
@@ -287,6 +306,37 @@ def test_decode_step_empty_rows_and_status():
     with pytest.raises(sqz.SqzError) as e:
         sqz.attention_status()
     assert e.value.code == sqz.SQZ_ERR_EMPTY
+
+
+def test_decode_step_user_chunks_empty_rows_and_status():
+    """The user-chunk path (B = 1) with a threshold no cluster passes: rows attend
+    only their user keys (the chunk partials alone); with no user keys they are
+    empty (identity partial, or SQZ_ERR_EMPTY when final); the chunk counts
+    self-clean across calls."""
+    sqz = _sqz()
+    P = oracle_problem(3, 900, 128, 30, 0, synth.BF16, seed=13, B=1, n_u=21)
+    t = _device(P)
+    scale = 1 / np.sqrt(128)
+    for _ in range(2):
+        sel, O, LSE = sqz.decode_step(t["idx"], t["Q"], t["Kp"], t["Vp"], t["Ku"], t["Vu"], scale, 1.0)
+        torch.cuda.synchronize()
+        assert int(sel.n_keys.sum()) == 0
+        _check_attention(P, sel, O, LSE, scale, False, 1, 2e-2, 5e-3)
+        sqz.attention_status()
+    sel, O, LSE = sqz.decode_step(t["idx"], t["Q"], t["Kp"], t["Vp"], None, None, scale, 1.0, partial=True)
+    torch.cuda.synchronize()
+    assert torch.isneginf(LSE).all() and (O == 0).all()
+    sqz.attention_status()
+    sqz.decode_step(t["idx"], t["Q"], t["Kp"], t["Vp"], None, None, scale, 1.0, partial=False)
+    with pytest.raises(sqz.SqzError) as e:
+        sqz.attention_status()
+    assert e.value.code == sqz.SQZ_ERR_EMPTY
+    # and a normal step right after still selects and attends correctly
+    T, _ = _calibrate(P, scale, 0.3)
+    sel, O, LSE = sqz.decode_step(t["idx"], t["Q"], t["Kp"], t["Vp"], t["Ku"], t["Vu"], scale, T)
+    torch.cuda.synchronize()
+    assert int(sel.n_keys.sum()) > 0
+    _check_attention(P, sel, O, LSE, scale, False, 1, 2e-2, 5e-3)
 
 
 PREFILL_CASES = [
