@@ -64,11 +64,16 @@ for i, n in [(0, "lookup start"), (1, "lookup scan done"), (6, "lookup local (m,
     if (tl[:, i] > 0).all():
         st(n, tl[:, i])
 for i, n in [(0, "attn entry"), (1, "attn after griddep wait"), (2, "attn prologue done"),
-             (6, "attn first segment done"), (4, "attn streaming done (last seg)"), (5, "attn end")]:
+             (6, "attn merger's ticket taken"), (4, "attn streaming done (last seg)"), (5, "attn end")]:
     col = ta[:, i]
     if (col > 0).any():
         st(n, col[col > 0])
 # per-CTA attribution of the tail: segments, merges, keys, SM
+tm = np.zeros(2048 * 4, np.uint64)
+lib.sqz_trace_mrg(tm.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(tm.nbytes))
+tm = tm.reshape(2048, 4)[:32].astype(np.float64)
+for i, n in [(0, "merge start"), (1, "merge partials loaded"), (2, "merge end")]:
+    st(n, tm[:, i])
 info = ta[:, 3].astype(np.uint64)
 nseg = (info & 0xff).astype(int)
 nmer = ((info >> 8) & 0xff).astype(int)

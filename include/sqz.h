@@ -299,17 +299,19 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
  * rule and the same attended set (selected fixed keys + all n_u
  * user keys) -- and writes the same outputs: `sel` (clusters,
  * n_clusters, n_keys, key_pref required; key_idx optional) and O, LSE.
- * For a single-level index without debug outputs it runs as ONE persistent
- * cooperative kernel (scan, threshold, compaction and attention separated by
- * grid barriers; the selection-independent user KV is streamed while the
- * lookup's reductions are in flight).  Hierarchical indexes, debug outputs
- * (dbg_*, l1_surv) and shapes outside the fused kernel's limits run the two
- * calls internally.  ap->causal is ignored (decode sees all n_u user keys, R8).
- * The selection may differ from the two-call path only for clusters inside
- * the 1e-5 near-threshold band (Eq. 1's denominator is reduced in another
- * order).  ws: sqz_decode_step_workspace bytes, zeroed once
- * (sqz_workspace_init); empty rows with ap->partial == 0 are reported by
- * sqz_attention_status(ws) as for sqz_sparse_attention. */
+ * For B = 1, a single-level unsharded index, n_u > 0 and no debug outputs the
+ * two kernels are arranged for decode latency: the user KV does not depend on
+ * the selection (the user input follows the fixed context), so the
+ * attention kernel -- launched behind the lookup -- attends it in 256-key
+ * chunks on CTAs that run beside the lookup's CTAs (a lookup variant limited to
+ * 84 registers leaves them room) BEFORE it waits for the selection; the chunk
+ * partials join each row's split-KV merge.  Other shapes run the
+ * two calls internally.  The selection is identical to the two-call path's
+ * (same lookup arithmetic); O/LSE differ only in summation order.
+ * ap->causal is ignored (decode sees all n_u user keys, R8).  ws:
+ * sqz_decode_step_workspace bytes, zeroed once (sqz_workspace_init), then
+ * self-cleaning for a fixed (idx, B, n_u); empty rows with ap->partial == 0
+ * are reported by sqz_attention_status(ws) as for sqz_sparse_attention. */
 int sqz_decode_step_workspace(const sqz_index *idx, int32_t B, int32_t n_u, size_t *ws_bytes);
 int sqz_decode_step(const sqz_index *idx, const void *Q, int32_t B, const void *Kp, const void *Vp,
                     const void *Ku, const void *Vu, int32_t n_u, const sqz_lookup_params *lp,

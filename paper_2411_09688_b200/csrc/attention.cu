@@ -23,6 +23,8 @@
 // reduced with a transposed butterfly (8 shuffles) and the online softmax runs
 // in the log2 domain (ex2.approx).  The kernel is launched with programmatic
 // stream serialization; griddepcontrol.wait orders it after the lookup kernel.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 #include "stream.cuh"
@@ -31,6 +33,22 @@
 namespace sqz {
 
 SQZ_TRACE_DECL(g_trace_attn)
+#ifdef SQZ_TRACE
+__device__ unsigned long long g_trace_mrg[2048 * 4];  // per row: merge start, loads in, end
+#define MRG_AT(row, slot)                                                                  \
+    do {                                                                                   \
+        if (threadIdx.x == 0 && (row) < 2048) {                                            \
+            unsigned long long t_;                                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+            g_trace_mrg[(row) * 4 + (slot)] = t_;                                          \
+        }                                                                                  \
+    } while (0)
+extern "C" int sqz_trace_mrg(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, g_trace_mrg, bytes < sizeof(g_trace_mrg) ? bytes : sizeof(g_trace_mrg));
+}
+#else
+#define MRG_AT(row, slot) do { } while (0)
+#endif
 
 constexpr int NCW = 4;                  // warps per CTA
 constexpr int NCT = NCW * 32;           // threads per CTA
@@ -95,6 +113,7 @@ __device__ void merge_row(const AttnArgs &a, int row, int P) {
     constexpr int MB = 32;
     const int tid = threadIdx.x;
     if (tid >= D) return;
+    MRG_AT(row, 0);
     const float *lse = a.part_lse + (size_t)row * a.max_chunks;
     const float *op = a.part_o + (size_t)row * a.max_chunks * D + tid;
     // decode step: the user-chunk partials follow the P fixed-key ones
@@ -114,6 +133,7 @@ __device__ void merge_row(const AttnArgs &a, int row, int P) {
         float mt = M;
 #pragma unroll
         for (int j = 0; j < MB; ++j) mt = fmaxf(mt, lv[j]);
+        MRG_AT(row, 1);
         if (mt == -INFINITY) continue;
         const float corr = expf(M - mt);  // M = -inf -> 0
         L *= corr;
@@ -135,6 +155,7 @@ __device__ void merge_row(const AttnArgs &a, int row, int P) {
         a.LSE[row] = (M == -INFINITY) ? -INFINITY : M + logf(L);
         if (M == -INFINITY && !a.partial) atomicOr(a.status, 1);
     }
+    MRG_AT(row, 2);
 }
 
 // Rows with no key at all (no selected fixed key, no visible user key) get the
@@ -377,6 +398,8 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
     const int tid = threadIdx.x, lane = tid & 31;
 
     SQZ_TRACE_AT(g_trace_attn, 0);
+    // the merge kernel behind this one may take the SM slots this grid frees
+    if (PERSIST && a.merge_kernel) asm volatile("griddepcontrol.launch_dependents;");
     // decode step (a.up_o): the user KV does not depend on the selection, so the
     // CTAs resident beside the lookup's CTAs attend it now, in USER_CHUNK-key
     // chunks spread statically over the first up_ctas CTAs, each chunk's
@@ -395,8 +418,9 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
                                  a.up_o + ((size_t)r * a.up_n + j) * D, a.up_lse + (size_t)r * a.up_n + j,
                                  s_m, s_l, s_o);
             __syncthreads();
-            // the row's ticket word counts user chunks in its high 16 bits
-            if (tid == 0) red_release_add(a.row_cnt + r, 1 << 16);
+            // the row's ticket word counts user chunks in its high 16 bits (the
+            // merge kernel, when used, runs after the whole grid instead)
+            if (tid == 0 && !a.merge_kernel) red_release_add(a.row_cnt + r, 1 << 16);
         }
     }
     // the selection comes from the preceding lookup kernel (programmatic
@@ -442,7 +466,7 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
             if (r < rows) s_pref[r + 1] = basev + wb + inc;
         }
         __syncthreads();
-        for (int r = blockIdx.x; r < rows; r += gridDim.x)
+        for (int r = blockIdx.x; r < rows && !a.merge_kernel; r += gridDim.x)
             if (s_pref[r + 1] == s_pref[r]) {
                 if (a.up_o) {  // no selected fixed key: the user-chunk partials alone
                     user_ready(r);
@@ -474,12 +498,13 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
         stream_partial<T, D>(a, sg.row, ri, sg.a0, sg.a1, a.part_o + slot * D, a.part_lse + slot, s_m,
                              s_l, s_o);
         SQZ_TRACE_AT(g_trace_attn, 4);
-#ifdef SQZ_TRACE
-        if (tr_nseg == 1) SQZ_TRACE_AT(g_trace_attn, 6);
-#endif
+        __syncthreads();
+        if (PERSIST && a.merge_kernel) {  // the merge kernel takes it from here
+            if (tid == 0 && sg.slot == 0) a.row_cnt[sg.row] = sg.nparts;
+            continue;
+        }
         // the CTA that completes a row's last segment merges its partials (the
         // barrier orders the CTA's partial stores before thread 0's release fence)
-        __syncthreads();
         if (tid == 0) {
             // ticket word: fixed-key partials counted in the low 16 bits, the
             // decode step's user chunks (released before the wait) in the high ones
@@ -502,6 +527,7 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
         }
         __syncthreads();
         if (s_last) {
+            SQZ_TRACE_AT(g_trace_attn, 6);  // ticket taken (merging CTAs)
 #if !SQZ_ATT_ACQREL
             __threadfence();
 #endif
@@ -524,6 +550,19 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
 #endif
 }
 
+// Decode step: the merge of every row's partials (fixed-key segments, then the
+// user chunks) after the whole attention grid is done (griddepcontrol.wait):
+// no ticket atomics and no last-CTA merge on the attention kernel's tail.
+template <int D>
+__global__ void __launch_bounds__(D) k_merge_rows(AttnArgs a) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int row = blockIdx.x;
+    const int P = ldcg(a.row_cnt + row);
+    merge_row<D>(a, row, P);
+    __syncthreads();
+    if (threadIdx.x == 0) a.row_cnt[row] = 0;  // self-cleaning (the ticket array)
+}
+
 template <typename T, int D>
 static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     const int rows = a.B * a.H * a.n_q;
@@ -541,12 +580,14 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     // 1M keys with B*H >= 2048) take the 2-D split-KV grid instead.
     const long long max_cost = (long long)rows * (a.L + a.n_u + SEG_KW);
     const bool persist = a.n_q == 1 && rows <= 8192 && max_cost < 0x7fffffffLL;
-    if (a.up_o && !persist) return cudaErrorInvalidValue;  // user chunks need the persistent grid
+    if ((a.up_o || a.merge_kernel) && !persist) return cudaErrorInvalidValue;  // decode-step modes
     if (persist) {
         const size_t dsm = (size_t)(2 * rows + 1) * sizeof(int);
         // long per-CTA streams (upper bound of the selected keys: rows x L) take the
         // 4-CTAs-per-SM variant
-        auto kern = (long long)rows * a.L >= (1LL << 24) ? k_attend<T, D, true, 4> : k_attend<T, D, true, 3>;
+        static const int minb_env = std::getenv("SQZ_ATT_MINB") ? std::atoi(std::getenv("SQZ_ATT_MINB")) : 0;  // A/B knob
+        const bool four = minb_env ? minb_env == 4 : (long long)rows * a.L >= (1LL << 24);
+        auto kern = four ? k_attend<T, D, true, 4> : k_attend<T, D, true, 3>;
         if (dsm > 48 * 1024) {
             cudaError_t e = ensure_func_attr((const void *)kern,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
@@ -559,7 +600,12 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
         // user chunks go to the first CTAs, one per SM: those are dispatched
         // first and fit beside the lean lookup's CTAs (k_lookup_decode MINB = 3)
         a2.up_ctas = std::min((int)cfg.gridDim.x, device_sm_count());
-        return cudaLaunchKernelEx(&cfg, kern, a2, rows);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a2, rows);
+        if (e != cudaSuccess || !a.merge_kernel) return e;
+        cfg.gridDim = dim3(rows);
+        cfg.blockDim = dim3(D);
+        cfg.dynamicSmemBytes = 0;
+        return cudaLaunchKernelEx(&cfg, k_merge_rows<D>, a2);
     }
     cfg.gridDim = dim3(rows, a.max_chunks);
     cfg.dynamicSmemBytes = 0;

@@ -107,6 +107,10 @@ struct AttnArgs {
     // Null up_o: the user keys are part of the rows' streams.
     float *up_o, *up_lse;
     int32_t up_n, up_ctas;
+    // decode step: no tickets -- the CTA holding a row's first segment stores the
+    // row's partial count in row_cnt[r], and k_merge_rows (launched behind the
+    // attention kernel) merges every row after the whole grid is done
+    int32_t merge_kernel;
 };
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st);
 // shared_attn.cu: batch-shared decode attention over the per-head union of the
@@ -125,24 +129,6 @@ int attention_user_chunk();  // decode step: user keys per pre-wait chunk
 int attention_max_parts(int64_t L, int n_u, int n_q);
 cudaError_t launch_merge(int P, const float *O_parts, const float *LSE_parts, int64_t rows, int d,
                          void *O, float *LSE, int out_dtype, cudaStream_t st);
-
-// decode_step.cu: the fused single-level decode step (lookup + attention in one
-// persistent cooperative launch)
-struct StepLaunch {
-    const void *Q, *C, *Kp, *Vp, *Ku, *Vu;
-    const int32_t *N, *koff;
-    int32_t B, H, c, n_u, d, dtype, out_dtype, partial;
-    int64_t L;
-    float scale, T;
-    void *ws;  // carved by the launcher (decode_step_ws_bytes)
-    int32_t *clusters, *key_pref, *n_clusters, *n_keys, *key_idx;
-    void *O;
-    float *LSE;
-    int32_t *status;  // set to 1 when a final (non-partial) row attended no key
-};
-size_t decode_step_ws_bytes(int B, int H, int c, int n_u, int d);
-int decode_step_rows_ok(int B, int H, int c, long long L);
-cudaError_t launch_decode_step(const StepLaunch &l, cudaStream_t st);
 
 // diag.cu: App. A skewness + App. D ideal-lookup diagnostics (NEXT-4)
 struct DiagLaunch {
