@@ -105,3 +105,5 @@ order = np.argsort(-done)[:12]
 print("  slowest CTAs (cta, sm, nseg, merges, keys, start, done, end):")
 for i in order:
     print(f"    {i:4d} {smid[i]:4d} {nseg[i]} {nmer[i]} {keys[i]:5d} {start[i]:6.2f} {done[i]:6.2f} {end[i]:6.2f}")
+np.savez(os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", "trace_decode_raw.npz"),
+         tl=tl, ta=ta, t0=t0)

@@ -607,8 +607,6 @@ int sqz_decode_step(const sqz_index *idx, const void *Q, int32_t B, const void *
             a.up_o = up_o; a.up_lse = up_lse;
             a.up_n = nch;
         }
-        static const bool ticket_merge = std::getenv("SQZ_STEP_TICKET_MERGE") != nullptr;  // A/B knob
-        a.merge_kernel = ticket_merge ? 0 : 1;
         e = launch_attention(a, st);
         if (e != cudaSuccess) return cuda_fail(e, "decode step attention");
         return SQZ_OK;

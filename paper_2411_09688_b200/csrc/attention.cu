@@ -580,7 +580,7 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
     // 1M keys with B*H >= 2048) take the 2-D split-KV grid instead.
     const long long max_cost = (long long)rows * (a.L + a.n_u + SEG_KW);
     const bool persist = a.n_q == 1 && rows <= 8192 && max_cost < 0x7fffffffLL;
-    if ((a.up_o || a.merge_kernel) && !persist) return cudaErrorInvalidValue;  // decode-step modes
+    if (a.up_o && !persist) return cudaErrorInvalidValue;  // user chunks need the persistent grid
     if (persist) {
         const size_t dsm = (size_t)(2 * rows + 1) * sizeof(int);
         // long per-CTA streams (upper bound of the selected keys: rows x L) take the
@@ -600,8 +600,15 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
         // user chunks go to the first CTAs, one per SM: those are dispatched
         // first and fit beside the lean lookup's CTAs (k_lookup_decode MINB = 3)
         a2.up_ctas = std::min((int)cfg.gridDim.x, device_sm_count());
+        // short per-CTA streams: rows are merged by k_merge_rows behind the grid
+        // (measured on cfg2: the last-CTA ticket merge put ~3 us of atomics and
+        // L2 round trips on the tail; 56.0 -> 54.3 us for the two calls, 52.8 ->
+        // 51.9 for the step); long ones keep the in-kernel ticket merge, which
+        // their tail hides (cfg5 391 vs 393 us).  SQZ_TICKET_MERGE=1: A/B knob
+        static const bool ticket_merge = std::getenv("SQZ_TICKET_MERGE") != nullptr;
+        a2.merge_kernel = (ticket_merge || four) ? 0 : 1;
         cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a2, rows);
-        if (e != cudaSuccess || !a.merge_kernel) return e;
+        if (e != cudaSuccess || !a2.merge_kernel) return e;
         cfg.gridDim = dim3(rows);
         cfg.blockDim = dim3(D);
         cfg.dynamicSmemBytes = 0;

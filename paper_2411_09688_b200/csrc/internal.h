@@ -107,9 +107,10 @@ struct AttnArgs {
     // Null up_o: the user keys are part of the rows' streams.
     float *up_o, *up_lse;
     int32_t up_n, up_ctas;
-    // decode step: no tickets -- the CTA holding a row's first segment stores the
-    // row's partial count in row_cnt[r], and k_merge_rows (launched behind the
-    // attention kernel) merges every row after the whole grid is done
+    // persistent decode grid: no tickets -- the CTA holding a row's first segment
+    // stores the row's partial count in row_cnt[r], and k_merge_rows (launched
+    // behind the attention kernel) merges every row after the whole grid is done
+    // (set by the launcher)
     int32_t merge_kernel;
 };
 cudaError_t launch_attention(const AttnArgs &a, cudaStream_t st);
