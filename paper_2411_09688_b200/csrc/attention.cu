@@ -307,13 +307,13 @@ __device__ __forceinline__ void stream_partial(const AttnArgs &a, int row, const
     float m_run = -INFINITY, l_lane = 0.f, o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = 0.f;
-    for (; j0 < a1; j0 += NCW * KR) {
-        const int nk = min(KR, a1 - j0);
-        Raw<T> kr[NS], vr[NS];
+    // one warp round: the K and V rows of keys [j, j + KR) (positions in `pc`)
+    auto issue = [&](int j, int pc, Raw<T> (&kr)[NS], Raw<T> (&vr)[NS]) {
+        const int nk = min(KR, a1 - j);
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
             const int kk = s * KPW + g;
-            const int pos = __shfl_sync(FULL, pos_cur, kk);
+            const int pos = __shfl_sync(FULL, pc, kk);
             if (kk < nk) {
                 const T *kp = pos >= 0 ? Kf + (size_t)pos * D : Ku + (size_t)(-1 - pos) * D;
                 const T *vp = pos >= 0 ? Vf + (size_t)pos * D : Vu + (size_t)(-1 - pos) * D;
@@ -325,8 +325,9 @@ __device__ __forceinline__ void stream_partial(const AttnArgs &a, int row, const
                     kr[s].v[i] = vr[s].v[i] = make_uint4(0, 0, 0, 0);
             }
         }
-        // prefetch the next round's positions while this round's rows are in flight
-        pos_cur = pos_of(j0 + NCW * KR, j0 + NCW * KR + (lane & (KR - 1)));
+    };
+    auto consume = [&](int j, const Raw<T> (&kr)[NS], const Raw<T> (&vr)[NS]) {
+        const int nk = min(KR, a1 - j);
         float v[NS];
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
@@ -357,6 +358,14 @@ __device__ __forceinline__ void stream_partial(const AttnArgs &a, int row, const
             }
         }
         m_run = m_new;
+    };
+    constexpr int STRIDE = NCW * KR;
+    for (; j0 < a1; j0 += STRIDE) {
+        Raw<T> kr[NS], vr[NS];
+        issue(j0, pos_cur, kr, vr);
+        // prefetch the next round's positions while this round's rows are in flight
+        pos_cur = pos_of(j0 + STRIDE, j0 + STRIDE + (lane & (KR - 1)));
+        consume(j0, kr, vr);
     }
     // ---- fold the key groups, then the warps ----
 #pragma unroll
