@@ -549,12 +549,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                     allreduce=allsum)
     del s, Qc
     # ---- per-step work: selection sizes for the algorithmic-byte count ----
-    # the expanded key-index tensor is materialised: the attention kernels' run-length
-    # reader (key_idx=False) measured slower than the lookup's expansion on every config
     # the batch-shared pass reads the run-length selection (clusters + key_pref) only
     shared_attn = (cfg["mode"] == "decode" and B >= 2 and d == 128 and dt == 1
                    and not args.attn_per_row)
-    sel = sqz.Selection.empty(idx, B, n_q, False, dev, key_idx=not (args.sel_runs or shared_attn))
+    # prefill reads the run-length selection (cfg3: lookup -6 us, attention +5 us, measured
+    # 285.7 -> 283.8 us per step); decode keeps the expanded key list (the step: 51.9 vs 55.2)
+    runs = args.sel_runs == "on" or (args.sel_runs == "auto" and cfg["mode"] == "prefill")
+    sel = sqz.Selection.empty(idx, B, n_q, False, dev, key_idx=not (runs or shared_attn))
     esz = 2 if dt == 1 else 4
     ks, kus = [], []
     c2l = idx.c2
@@ -908,9 +909,9 @@ def main():
     ap.add_argument("--retention", type=float, default=None,
                     help="override the config's retention target (1.0 = T = 0, dense)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sel-runs", action="store_true",
+    ap.add_argument("--sel-runs", default="auto", choices=["auto", "on", "off"],
                     help="keep the selection in run-length form (no key_idx expansion in the lookup; "
-                         "the attention reads the runs)")
+                         "the attention reads the runs); auto = on for prefill, off for decode")
     ap.add_argument("--attn-per-row", action="store_true",
                     help="decode with B >= 2: stream each (b,h) selection separately instead of "
                          "the batch-shared union pass (A/B of NEXT-1)")

@@ -58,9 +58,9 @@ print(f"retention {ret}: event step time {e0.elapsed_time(e1) * 1e3:.1f} us; k =
 def st(name, v):
     v = (v - t0) / 1e3
     print(f"  {name:38s} min {v.min():7.2f}  med {np.median(v):7.2f}  max {v.max():7.2f} us")
-for i, n in [(0, "lookup start"), (1, "lookup scan done"), (6, "lookup local (m,D) done"),
-             (7, "lookup cluster.sync 1 + fold"), (2, "lookup compaction done (pre-barrier)"),
-             (3, "lookup cluster.sync 2"), (4, "lookup writes done"), (5, "lookup end")]:
+for i, n in [(0, "lookup start"), (1, "lookup scan done"), (2, "lookup compaction done (pre-exchange)"),
+             (3, "lookup count exchange done"), (6, "lookup prefix done"), (7, "lookup list/kpref stored"),
+             (4, "lookup writes done"), (5, "lookup end")]:
     if (tl[:, i] > 0).all():
         st(n, tl[:, i])
 for i, n in [(0, "attn entry"), (1, "attn after griddep wait"), (2, "attn prologue done"),

@@ -538,7 +538,6 @@ __global__ void __launch_bounds__(NT, MINB) k_lookup_decode(LookupShape s, const
             sh.md[i] = make_float2(M, dd);
         }
     }
-    if (!ROWLIST && !ONEQ) SQZ_TRACE_AT(g_trace_look, 6);
     if (push) {
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         if (warp == 0) {  // lane r sends this CTA's partials to rank r
@@ -592,7 +591,6 @@ __global__ void __launch_bounds__(NT, MINB) k_lookup_decode(LookupShape s, const
     }
     }  // phase != 2
     __syncthreads();
-    if (!ROWLIST && !ONEQ) SQZ_TRACE_AT(g_trace_look, 7);
     // ---- threshold + ordered compaction of the CTA's rows ----
     const bool all = !(lv.T > 0.f);
     const float logT = all ? 0.f : logf(lv.T);
@@ -707,6 +705,7 @@ __global__ void __launch_bounds__(NT, MINB) k_lookup_decode(LookupShape s, const
         }
     }
     __syncthreads();
+    if (!ROWLIST && !ONEQ) SQZ_TRACE_AT(g_trace_look, 6);
     // this CTA is done reading its peers' shared memory: arrive now, wait (so
     // that its own stays alive for the peers' reads) only before exiting.  (The
     // push exchange reads no remote memory, and every message addressed to this
@@ -723,6 +722,7 @@ __global__ void __launch_bounds__(NT, MINB) k_lookup_decode(LookupShape s, const
             list[j] = s_sel[i * rpc + j];
             kpref[j] = ok + s_kp[i * rpc + j];
         }
+        if (!ROWLIST && !ONEQ) SQZ_TRACE_AT(g_trace_look, 7);
         if (exp_list)
         for (int j = warp; j < mine; j += NW) {
             const int st = s_st[i * rpc + j], kp = s_kp[i * rpc + j];
@@ -1148,7 +1148,7 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
             if (lv.dbg_lse) lv.dbg_lse[(size_t)bh * s.n_q + t0 + tid] = lse;
             if (!(lse < INFINITY) || lse == -INFINITY) lse = INFINITY;  // no row: p = 0
         }
-        s_lse[tid] = lse;
+        s_lse[tid] = lse * LOG2E;  // log2 units (pass 2 works in the log2 domain)
     }
     cp_async_commit_grp();  // the Q tile
     int rid_pf;
@@ -1170,6 +1170,9 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
     }
 
     SQZ_TRACE_AT(g_trace_pl, 1);
+    // both passes work in the log2 domain: s2 = scale log2(e) q.c, m and LSE in
+    // log2 units, exponentials ex2.approx (one multiply fewer per element)
+    const float sl2 = s.scale * LOG2E;
     float m = -INFINITY, Dsum = 0.f;
     for (int it = first; it < total; ++it) {
         if (it == ntile) SQZ_TRACE_AT(g_trace_pl, 2);
@@ -1201,8 +1204,8 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
             float cmx = -INFINITY;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                v0[j] = j < lim ? v0[j] * s.scale : -INFINITY;
-                v1[j] = j + 32 < lim ? v1[j] * s.scale : -INFINITY;
+                v0[j] = j < lim ? v0[j] * sl2 : -INFINITY;
+                v1[j] = j + 32 < lim ? v1[j] * sl2 : -INFINITY;
                 cmx = fmaxf(cmx, fmaxf(v0[j], v1[j]));
             }
             const float mn = fmaxf(m, cmx);
@@ -1214,20 +1217,20 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
 #pragma unroll
                 for (int j = 0; j < 32; j += 4) {
                     const float4 w0 = nw4[j / 4], w1 = nw4[8 + j / 4];
-                    a[0] = fmaf(w0.x, exp_fast(v0[j] - mn), a[0]);
-                    a[1] = fmaf(w0.y, exp_fast(v0[j + 1] - mn), a[1]);
-                    a[2] = fmaf(w0.z, exp_fast(v0[j + 2] - mn), a[2]);
-                    a[3] = fmaf(w0.w, exp_fast(v0[j + 3] - mn), a[3]);
-                    a[4] = fmaf(w1.x, exp_fast(v1[j] - mn), a[4]);
-                    a[5] = fmaf(w1.y, exp_fast(v1[j + 1] - mn), a[5]);
-                    a[6] = fmaf(w1.z, exp_fast(v1[j + 2] - mn), a[6]);
-                    a[7] = fmaf(w1.w, exp_fast(v1[j + 3] - mn), a[7]);
+                    a[0] = fmaf(w0.x, fast_exp2(v0[j] - mn), a[0]);
+                    a[1] = fmaf(w0.y, fast_exp2(v0[j + 1] - mn), a[1]);
+                    a[2] = fmaf(w0.z, fast_exp2(v0[j + 2] - mn), a[2]);
+                    a[3] = fmaf(w0.w, fast_exp2(v0[j + 3] - mn), a[3]);
+                    a[4] = fmaf(w1.x, fast_exp2(v1[j] - mn), a[4]);
+                    a[5] = fmaf(w1.y, fast_exp2(v1[j + 1] - mn), a[5]);
+                    a[6] = fmaf(w1.z, fast_exp2(v1[j + 2] - mn), a[6]);
+                    a[7] = fmaf(w1.w, fast_exp2(v1[j + 3] - mn), a[7]);
                 }
-                Dsum = Dsum * expf(m - mn) + (((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
+                Dsum = Dsum * exp2f(m - mn) + (((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
                 m = mn;
             }
             if (tl == ntile - 1) {  // fold the two column halves of each query row
-                s_half[hf * PL_T + r] = make_float2(m, Dsum);
+                s_half[hf * PL_T + r] = make_float2(m * LN2, Dsum);  // natural units for the fold
                 __syncthreads();
                 if (tid < PL_T) {
                     const float2 h0 = s_half[tid], h1 = s_half[PL_T + tid];
@@ -1243,7 +1246,7 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
                             if (lv.dbg_lse) lv.dbg_lse[(size_t)bh * s.n_q + t0 + tid] = lse;
                         }
                         if (!ok || !(lse < INFINITY) || lse == -INFINITY) lse = INFINITY;
-                        s_lse[tid] = lse;
+                        s_lse[tid] = lse * LOG2E;
                     }
                 }
                 // s_lse is read after the next iteration's __syncthreads
@@ -1261,14 +1264,14 @@ __global__ void __launch_bounds__(PL_NT, 2) k_prefill_lookup_tc(LookupShape s,
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
                 const float4 e0 = l4[j / 4], e1 = l4[8 + j / 4];
-                a[0] += exp_fast(fmaf(v0[j], s.scale, -e0.x));
-                a[1] += exp_fast(fmaf(v0[j + 1], s.scale, -e0.y));
-                a[2] += exp_fast(fmaf(v0[j + 2], s.scale, -e0.z));
-                a[3] += exp_fast(fmaf(v0[j + 3], s.scale, -e0.w));
-                a[4] += exp_fast(fmaf(v1[j], s.scale, -e1.x));
-                a[5] += exp_fast(fmaf(v1[j + 1], s.scale, -e1.y));
-                a[6] += exp_fast(fmaf(v1[j + 2], s.scale, -e1.z));
-                a[7] += exp_fast(fmaf(v1[j + 3], s.scale, -e1.w));
+                a[0] += fast_exp2(fmaf(v0[j], sl2, -e0.x));
+                a[1] += fast_exp2(fmaf(v0[j + 1], sl2, -e0.y));
+                a[2] += fast_exp2(fmaf(v0[j + 2], sl2, -e0.z));
+                a[3] += fast_exp2(fmaf(v0[j + 3], sl2, -e0.w));
+                a[4] += fast_exp2(fmaf(v1[j], sl2, -e1.x));
+                a[5] += fast_exp2(fmaf(v1[j + 1], sl2, -e1.y));
+                a[6] += fast_exp2(fmaf(v1[j + 2], sl2, -e1.z));
+                a[7] += fast_exp2(fmaf(v1[j + 3], sl2, -e1.w));
             }
             const float a0 = a[0] + a[1], a1 = a[2] + a[3], a2 = a[4] + a[5], a3 = a[6] + a[7];
             s_half[hf * PL_T + r].x = (a0 + a1) + (a2 + a3);
