@@ -804,8 +804,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                            else "sparse_attention"),
                     "kernel": ("k_attend_shared (batch-shared union pass, mma.sync tiles, fused merge); "
                                "bytes = union of the B selections per head" if shared_attn else
-                               "k_attend (persistent split-KV over equal key ranges; rows merged by the fused "
-                               "ticket or, for short streams, by k_merge_rows behind it)"),
+                               "sqz_sparse_attention call: k_attend (persistent split-KV over equal key "
+                               "ranges) + the row merge (fused ticket, or for short streams k_merge_rows "
+                               "behind it, inside the timed call)"),
                     "bytes_if_streamed_per_query": int(bytes_attn_perq),
                     "peak_kind": f"{peak_kind} copy bandwidth",
                     "bytes_per_launch": int(bytes_attn)}
