@@ -833,7 +833,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     else:  # stats, then per level: fold + select (+ next level's stats)
         n_look = 1 + levels * (1 + per_select) + (levels - 1)
     # + k_union (batch-shared) or k_merge_rows (per-row persistent decode)
-    merge_k = cfg["mode"] == "decode" and not shared_attn and B * Hl * L < (1 << 24)  # attention.cu launch_t
+    merge_k = (cfg["mode"] == "decode" and not shared_attn
+               and (1 << 17) <= B * Hl * L < (1 << 24))  # attention.cu launch_t
     launches = K_ * (n_look + 1 + (1 if comm else 0) + (1 if shared_attn or merge_k else 0))
     metric, unit, hib = metric_of(cfg)
     line = {

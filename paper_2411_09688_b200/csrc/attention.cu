@@ -613,9 +613,11 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
         // (measured on cfg2: the last-CTA ticket merge put ~3 us of atomics and
         // L2 round trips on the tail; 56.0 -> 54.3 us for the two calls, 52.8 ->
         // 51.9 for the step); long ones keep the in-kernel ticket merge, which
-        // their tail hides (cfg5 391 vs 393 us).  SQZ_TICKET_MERGE=1: A/B knob
+        // their tail hides (cfg5 391 vs 393 us), and so do tiny problems, whose few
+        // CTAs would pay the extra launch (cfg1 21.5 vs 20.0 us).  SQZ_TICKET_MERGE=1: A/B
         static const bool ticket_merge = std::getenv("SQZ_TICKET_MERGE") != nullptr;
-        a2.merge_kernel = (ticket_merge || four) ? 0 : 1;
+        const bool tiny = (long long)rows * a.L < (1LL << 17);
+        a2.merge_kernel = (ticket_merge || four || tiny) ? 0 : 1;
         cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a2, rows);
         if (e != cudaSuccess || !a2.merge_kernel) return e;
         cfg.gridDim = dim3(rows);
