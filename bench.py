@@ -768,7 +768,22 @@ def run_gpu(args, cfg, rank, world, local_rank):
         q = Qt[0]
         sel_p = sqz.Selection.empty(idx, B, n_q, debug=True, device=dev, key_idx=False)
         sqz.centroid_lookup(idx, q, scale, T, T1, sel=sel_p, comm=comm, T0=T0)
-        attend_into(q, O, LSE, sel_p)
+        same_sel = None
+        if use_step:
+            # the timed path's outputs: O / LSE from sqz_decode_step; its selection must
+            # equal the debug lookup's (same arithmetic), whose scores give the band rule
+            sel_s = sqz.Selection.empty(idx, B, n_q, False, dev, key_idx=True)
+            sqz.decode_step(idx, q, Kp, Vp, Ku, Vu, scale, T, T1, sel=sel_s, O=O, LSE=LSE, ws=step_ws,
+                            T0=T0)
+            torch.cuda.synchronize()
+            nc = sel_s.n_clusters
+            same_sel = bool(torch.equal(nc, sel_p.n_clusters) and torch.equal(sel_s.n_keys, sel_p.n_keys)
+                            and all(torch.equal(sel_s.clusters[b_, h_, :int(nc[b_, h_])],
+                                                sel_p.clusters[b_, h_, :int(nc[b_, h_])])
+                                    for b_ in range(B) for h_ in range(Hl)))
+            del sel_s
+        else:
+            attend_into(q, O, LSE, sel_p)
         torch.cuda.synchronize()
         if rank == 0:
             rs = None
@@ -778,6 +793,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
             parity = oracle_parity(sqz, gidx, q, sel_p, O, LSE, T, T1, scale, K0, V0, Ku0, Vu0, idx,
                                    causal, rs, T0=T0)
             parity["oracle_s"] = round(time.time() - t_p, 1)
+            parity["path"] = "sqz_decode_step" if use_step else "two calls"
+            if same_sel is not None:
+                parity["step_selection_equals_lookup"] = same_sel
+                parity["ok"] = bool(parity.get("ok")) and same_sel
         del sel_p
     # ---- selection quality (App. A skewness, App. D ideal lookup; after the timed region) ----
     quality = None

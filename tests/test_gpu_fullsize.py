@@ -75,9 +75,10 @@ def _key_mask(sel, idx_sub, heads):
     return m
 
 
-def _run(K, V, Q, Ku, Vu, c2, c1, init2, init1, prefill, retention, Qc):
-    """GPU index + calibration + lookup + attention as bench.py runs them; returns the
-    pieces the oracle needs."""
+def _run(K, V, Q, Ku, Vu, c2, c1, init2, init1, prefill, retention, Qc, step=False):
+    """GPU index + calibration + lookup + attention as bench.py runs them (step: one
+    sqz_decode_step call, the path bench.py times for cfg2); returns the pieces the
+    oracle needs."""
     sqz = _sqz()
     H, L, d = K.shape
     scale = 1.0 / np.sqrt(d)
@@ -95,8 +96,11 @@ def _run(K, V, Q, Ku, Vu, c2, c1, init2, init1, prefill, retention, Qc):
                                      total_weight=Bc * H * L)
     B, _, n_q, _ = Q.shape
     sel = sqz.Selection.empty(idx, B, n_q, True)
-    sqz.centroid_lookup(idx, Q, scale, T, T1, sel=sel)
-    O, LSE = sqz.sparse_attention(Q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=prefill)
+    if step:
+        sel, O, LSE = sqz.decode_step(idx, Q, Kp, Vp, Ku, Vu, scale, T, T1, sel=sel)
+    else:
+        sqz.centroid_lookup(idx, Q, scale, T, T1, sel=sel)
+        O, LSE = sqz.sparse_attention(Q, Kp, Vp, idx, sel, Ku, Vu, scale, causal=prefill)
     torch.cuda.synchronize()
     nk = sel.n_keys.cpu().numpy()
     heads = [0, int(np.argmax(nk.sum(0)))]
@@ -151,6 +155,21 @@ def test_cfg2_decode_fullsize(ctx32k):
     Ku, Vu = (sqz.to_device(a) for a in synth.user_kv(fc.mix, 1, 1024, seed=5002))
     idx, sel, O, LSE, T, T1, scale, heads = _run(K, V, Q, Ku, Vu, 1024, 0, init2, None, False, 0.3, Qc)
     _check(idx, sel, O, LSE, T, T1, scale, heads, Q, K, V, Ku, Vu, False)
+
+
+def test_cfg2_decode_step_fullsize(ctx32k):
+    """cfg2 at full size through sqz_decode_step (user KV in chunks beside the lookup,
+    rows merged behind the attention grid), on two sampled heads; run twice on the same
+    workspace (self-cleaning counters)."""
+    sqz = _sqz()
+    fc, K, V, init2 = ctx32k
+    Qc = sqz.to_device(synth.decode_queries(fc.mix, 32, seed=3002))
+    Q = sqz.to_device(synth.decode_queries(fc.mix, 1, seed=4012))
+    Ku, Vu = (sqz.to_device(a) for a in synth.user_kv(fc.mix, 1, 1024, seed=5012))
+    for _ in range(2):
+        idx, sel, O, LSE, T, T1, scale, heads = _run(K, V, Q, Ku, Vu, 1024, 0, init2, None, False, 0.3, Qc,
+                                                     step=True)
+        _check(idx, sel, O, LSE, T, T1, scale, heads, Q, K, V, Ku, Vu, False)
 
 
 def test_cfg3_prefill_fullsize(ctx32k):
