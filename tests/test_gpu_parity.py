@@ -339,6 +339,37 @@ def test_decode_step_user_chunks_empty_rows_and_status():
     _check_attention(P, sel, O, LSE, scale, False, 1, 2e-2, 5e-3)
 
 
+@pytest.mark.parametrize("shape", [(32, 4096, 128, 128, 300), (2, 1024, 64, 32, 16)],
+                         ids=["h32_merge_kernel", "tiny_ticket_merge"])
+def test_decode_step_repeat_bit_identical(shape):
+    """The decode step is deterministic and its workspace self-cleaning: 12 calls on the
+    same input, interleaved with debug calls (which run the two-call path on the same
+    attention region), give bit-identical O, LSE and selections."""
+    sqz = _sqz()
+    H, L, d, c2, n_u = shape
+    P = oracle_problem(H, L, d, c2, 0, synth.BF16, seed=77, B=1, n_u=n_u)
+    scale = 1.0 / np.sqrt(d)
+    T, _ = _calibrate(P, scale, 0.3)
+    t = _device(P)
+    ref = None
+    for it in range(12):
+        debug = it % 4 == 3
+        sel = sqz.Selection.empty(t["idx"], 1, 1, debug=debug)
+        sel, O, LSE = sqz.decode_step(t["idx"], t["Q"], t["Kp"], t["Vp"], t["Ku"], t["Vu"], scale, T, sel=sel)
+        torch.cuda.synchronize()
+        got = (O.clone(), LSE.clone(), sel.n_clusters.clone(), sel.n_keys.clone())
+        if ref is None:
+            ref = got
+            _check_attention(P, sel, O, LSE, scale, False, 1, 2e-2, 5e-3)
+            continue
+        assert torch.equal(got[2], ref[2]) and torch.equal(got[3], ref[3])
+        if debug:  # the two-call path: same rows, another summation order
+            assert (got[0].float() - ref[0].float()).abs().max().item() <= 2e-2
+            assert (got[1] - ref[1]).abs().max().item() <= 1e-3
+        else:
+            assert torch.equal(got[0], ref[0]) and torch.equal(got[1], ref[1])
+
+
 PREFILL_CASES = [
     # id, H, L, d, c2, c1, dtype, B, n_q, n_u, retention, causal
     ("bf16_single", 2, 2048, 128, 100, 0, synth.BF16, 1, 200, 200, 0.3, True),
