@@ -552,9 +552,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # the batch-shared pass reads the run-length selection (clusters + key_pref) only
     shared_attn = (cfg["mode"] == "decode" and B >= 2 and d == 128 and dt == 1
                    and not args.attn_per_row)
-    # prefill reads the run-length selection (cfg3: lookup -6 us, attention +5 us, measured
-    # 285.7 -> 283.8 us per step); decode keeps the expanded key list (the step: 51.9 vs 55.2)
-    runs = args.sel_runs == "on" or (args.sel_runs == "auto" and cfg["mode"] == "prefill")
+    # single-level prefill reads the run-length selection (cfg3: lookup -6 us, attention +5 us,
+    # 285.7 -> 283.8 us per step); hierarchical prefill (cfg5p: 14.49 vs 14.3 ms) and decode
+    # (the step: 55.2 vs 51.9 us) keep the expanded key list
+    runs = args.sel_runs == "on" or (args.sel_runs == "auto" and cfg["mode"] == "prefill"
+                                      and not cfg.get("c1"))
     sel = sqz.Selection.empty(idx, B, n_q, False, dev, key_idx=not (runs or shared_attn))
     esz = 2 if dt == 1 else 4
     ks, kus = [], []
@@ -932,7 +934,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sel-runs", default="auto", choices=["auto", "on", "off"],
                     help="keep the selection in run-length form (no key_idx expansion in the lookup; "
-                         "the attention reads the runs); auto = on for prefill, off for decode")
+                         "the attention reads the runs); auto = on for single-level prefill")
     ap.add_argument("--attn-per-row", action="store_true",
                     help="decode with B >= 2: stream each (b,h) selection separately instead of "
                          "the batch-shared union pass (A/B of NEXT-1)")
