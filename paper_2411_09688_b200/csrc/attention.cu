@@ -414,11 +414,6 @@ __global__ void __launch_bounds__(NCT, MINB) k_attend(AttnArgs a, int rows) {
     // chunks spread statically over the first up_ctas CTAs, each chunk's
     // partial counted in the high bits of the row's ticket word
     if (PERSIST && a.up_o && (int)blockIdx.x < a.up_ctas) {
-        if (a.up_delay_ns > 0) {  // let the lookup's scan requests reach DRAM first (A/B knob)
-            const unsigned long long t0 = clock64();
-            const unsigned long long cyc = (unsigned long long)a.up_delay_ns * 2;  // ~2 GHz
-            while (clock64() - t0 < cyc) __nanosleep(100);
-        }
         const int nch = rows * a.up_n;
         for (int c = blockIdx.x; c < nch; c += a.up_ctas) {
             const int r = c / a.up_n, j = c % a.up_n;
@@ -614,8 +609,6 @@ static cudaError_t launch_t(const AttnArgs &a, cudaStream_t st) {
         // user chunks go to the first CTAs, one per SM: those are dispatched
         // first and fit beside the lean lookup's CTAs (k_lookup_decode MINB = 3)
         a2.up_ctas = std::min((int)cfg.gridDim.x, device_sm_count());
-        static const int up_delay = std::getenv("SQZ_UP_DELAY_NS") ? std::atoi(std::getenv("SQZ_UP_DELAY_NS")) : 0;
-        a2.up_delay_ns = up_delay;
         // short per-CTA streams: rows are merged by k_merge_rows behind the grid
         // (measured on cfg2: the last-CTA ticket merge put ~3 us of atomics and
         // L2 round trips on the tail; 56.0 -> 54.3 us for the two calls, 52.8 ->

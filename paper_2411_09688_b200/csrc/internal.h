@@ -106,7 +106,7 @@ struct AttnArgs {
     // to the row's ticket word row_cnt[r] (its merger waits for up_n of them).
     // Null up_o: the user keys are part of the rows' streams.
     float *up_o, *up_lse;
-    int32_t up_n, up_ctas, up_delay_ns;
+    int32_t up_n, up_ctas;
     // persistent decode grid: no tickets -- the CTA holding a row's first segment
     // stores the row's partial count in row_cnt[r], and k_merge_rows (launched
     // behind the attention kernel) merges every row after the whole grid is done
