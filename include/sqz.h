@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define SQZ_ABI_VERSION 5
+#define SQZ_ABI_VERSION 6
 
 enum {
     SQZ_OK = 0,
@@ -164,6 +164,28 @@ int sqz_cluster_keys(const void *K, const void *V, const int64_t *init2, const i
  * failure.  ws: sqz_index_validate_workspace() bytes. */
 int sqz_index_validate_workspace(const sqz_index *idx, size_t *ws_bytes);
 int sqz_index_validate(const sqz_index *idx, void *ws, size_t ws_bytes, void *stream);
+
+/* Index persistence (ABI v6).  The offline clustering output is the artefact
+ * built once per fixed context and reused online (S:100-103, S:115-123
+ * name the magic and the round-trip property).  File: the 8 bytes "SQZIDX1\0",
+ * u32 version = 1, nine little-endian i64 {H, d, L, levels, c0, c1, c2, dtype,
+ * L_total}, then the tables' raw little-endian bytes in the device layout above,
+ * in the order [C0, N0, child_off0] (levels 3), [C1, N1, child_off] (levels >= 2),
+ * C2, N2, key_off, perm.  load(save(x)) == x bit for bit.
+ *   sqz_index_save      copies the tables device -> host and writes `path`
+ *                       (synchronises the stream).  SQZ_ERR_FORMAT: invalid
+ *                       geometry; SQZ_ERR_INVALID_ARG: NULL table, I/O failure.
+ *   sqz_index_file_info host only: reads and checks the header (magic, version,
+ *                       geometry, payload size == the geometry's tables) and
+ *                       fills the geometry fields of *geom (pointers NULL), so the
+ *                       caller can allocate.  SQZ_ERR_FORMAT on any mismatch.
+ *   sqz_index_load      copies the file's tables into the caller-allocated device
+ *                       tables of *dst, whose geometry must equal the file's
+ *                       (synchronises).  Run sqz_index_validate on the result
+ *                       before trusting a file from elsewhere. */
+int sqz_index_save(const sqz_index *idx, const char *path, void *stream);
+int sqz_index_file_info(const char *path, sqz_index *geom);
+int sqz_index_load(const char *path, const sqz_index *dst, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Online step 1: centroid lookup (Eq. 1-3; section 4.1)          */

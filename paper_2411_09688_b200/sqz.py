@@ -25,7 +25,7 @@ SO = os.path.join(HERE, "libsqz.so")
 SQZ_F32, SQZ_BF16 = 0, 1
 SQZ_OK, SQZ_ERR_INVALID_ARG, SQZ_ERR_FORMAT, SQZ_ERR_INVARIANT = 0, 2, 3, 4
 SQZ_ERR_CUDA, SQZ_ERR_NCCL, SQZ_ERR_EMPTY, SQZ_ERR_UNSUPPORTED = 5, 6, 7, 8
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 EXPORTS = [
     "sqz_cluster_keys_workspace", "sqz_cluster_keys", "sqz_index_validate_workspace",
@@ -37,6 +37,7 @@ EXPORTS = [
     "sqz_comm_merge_workspace", "sqz_comm_allgather_merge", "sqz_decode_step_workspace",
     "sqz_decode_step", "sqz_selection_diagnostics_workspace", "sqz_selection_diagnostics",
     "sqz_comm_alltoall_merge_workspace", "sqz_comm_alltoall_merge",
+    "sqz_index_save", "sqz_index_file_info", "sqz_index_load",
 ]
 
 
@@ -112,6 +113,9 @@ def lib():
                                        ctypes.POINTER(ctypes.c_int32), vp]
         L.sqz_index_validate_workspace.argtypes = [ip, szp]
         L.sqz_index_validate.argtypes = [ip, vp, sz, vp]
+        L.sqz_index_save.argtypes = [ip, ctypes.c_char_p, vp]
+        L.sqz_index_file_info.argtypes = [ctypes.c_char_p, ip]
+        L.sqz_index_load.argtypes = [ctypes.c_char_p, ip, vp]
         L.sqz_lookup_workspace.argtypes = [ip, i32, i32, szp]
         L.sqz_centroid_lookup.argtypes = [ip, vp, i32, i32, ctypes.POINTER(sqz_lookup_params),
                                           ctypes.POINTER(sqz_selection), vp, sz, vp]
@@ -278,6 +282,32 @@ def index_validate(idx: Index):
     _check(lib().sqz_index_validate_workspace(ctypes.byref(s), ctypes.byref(nb)))
     ws = torch.empty(nb.value, dtype=torch.uint8, device=idx.C2.device)
     _check(lib().sqz_index_validate(ctypes.byref(s), _p(ws), nb.value, _stream()))
+
+
+def save_index(idx: Index, path: str):
+    """sqz_index_save: write the index tables to `path` (SQZIDX1 file)."""
+    s = idx.struct()
+    _check(lib().sqz_index_save(ctypes.byref(s), os.fsencode(path), _stream()))
+
+
+def index_file_info(path: str) -> sqz_index:
+    """sqz_index_file_info: the geometry recorded in a SQZIDX1 file (host only)."""
+    g = sqz_index()
+    _check(lib().sqz_index_file_info(os.fsencode(path), ctypes.byref(g)))
+    return g
+
+
+def load_index(path: str, device="cuda", validate: bool = True) -> Index:
+    """sqz_index_load into freshly allocated device tables (then sqz_index_validate)."""
+    g = index_file_info(path)
+    idx = Index.empty(g.H, g.d, g.L, g.c2, g.c1 if g.levels >= 2 else 0, g.dtype, device,
+                      c0=g.c0 if g.levels == 3 else 0)
+    idx.L_total = g.L_total
+    s = idx.struct()
+    _check(lib().sqz_index_load(os.fsencode(path), ctypes.byref(s), _stream()))
+    if validate:
+        index_validate(idx)
+    return idx
 
 
 @dataclass

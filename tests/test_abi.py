@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(lib):
     for name in decl:
         assert hasattr(lib, name), name
     assert sorted(sqz.EXPORTS) == decl
-    assert lib.sqz_abi_version() == sqz.ABI_VERSION == 5
+    assert lib.sqz_abi_version() == sqz.ABI_VERSION == 6
 
 
 def test_struct_layout_matches_header(tmp_path):
@@ -107,3 +107,37 @@ def test_calibration_quantile():
     assert calib.weighted_threshold(S, N, 1.0) == 0.0
     N = np.array([2, 1, 1, 4])
     assert calib.weighted_threshold(S, N, 0.25) == pytest.approx(0.4)
+
+
+def _index_file(path, geom, payload_bytes, magic=b"SQZIDX1\0", version=1):
+    import struct
+    with open(path, "wb") as f:
+        f.write(magic)
+        f.write(struct.pack("<I", version))
+        f.write(struct.pack("<9q", *geom))
+        f.write(b"\0" * payload_bytes)
+
+
+def test_index_file_header_checks(lib, tmp_path):
+    """sqz_index_file_info (host only): the geometry of a well-formed SQZIDX1 file; bad
+    magic, bad version, invalid geometry and a payload of the wrong size are
+    SQZ_ERR_FORMAT (S:115-123: 'bad magic ... rejection')."""
+    from paper_2411_09688_b200 import sqz
+
+    H, d, L, c1, c2 = 2, 64, 100, 4, 10
+    # two levels, bf16: C1, N1, child_off, C2, N2, key_off, perm
+    need = H * c1 * d * 2 + H * c1 * 4 + H * (c1 + 1) * 4 + H * c2 * d * 2 + H * c2 * 4 + H * (c2 + 1) * 4 + H * L * 4
+    geom = (H, d, L, 2, 0, c1, c2, sqz.SQZ_BF16, 0)
+    ok = str(tmp_path / "ok.sqzidx")
+    _index_file(ok, geom, need)
+    g = sqz.index_file_info(ok)
+    assert (g.H, g.d, g.L, g.levels, g.c1, g.c2, g.dtype, g.L_total) == (H, d, L, 2, c1, c2, sqz.SQZ_BF16, 0)
+    bad = [("magic", dict(magic=b"XXXXXXX\0"), geom, need), ("version", dict(version=2), geom, need),
+           ("short", {}, geom, need - 4), ("long", {}, geom, need + 4),
+           ("geometry", {}, (H, 96, L, 2, 0, c1, c2, sqz.SQZ_BF16, 0), need)]
+    for name, kw, gm, nb in bad:
+        p = str(tmp_path / f"{name}.sqzidx")
+        _index_file(p, gm, nb, **kw)
+        with pytest.raises(sqz.SqzError) as e:
+            sqz.index_file_info(p)
+        assert e.value.code == sqz.SQZ_ERR_FORMAT, name

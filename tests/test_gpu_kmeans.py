@@ -260,3 +260,47 @@ def test_three_level_index_identical_to_oracle(dtype):
         assert np.array_equal(_np(getattr(g, f)), oracle.encode(getattr(r, f), dtype)), f
     assert np.array_equal(_np(Kp), oracle.permute_kv(fc.K, r))
     assert np.array_equal(_np(Vp), oracle.permute_kv(fc.V, r))
+
+
+@pytest.mark.parametrize("levels,dt", [(1, synth.F32), (2, synth.BF16), (3, synth.BF16)])
+def test_index_save_load_round_trip(levels, dt, tmp_path):
+    """sqz_index_save / sqz_index_load: load(save(x)) == x bit for bit, the
+    loaded index validates, and a lookup on it selects exactly what the original's
+    does (the offline index is the persisted artefact)."""
+    from paper_2411_09688_b200 import sqz
+
+    H, L, d, c2 = 2, 1200, 64, 48
+    c1 = 12 if levels >= 2 else 0
+    c0 = 4 if levels == 3 else 0
+    fc = synth.fixed_context(H, L, d, c2, dtype=dt, seed=61)
+    K, V = sqz.to_device(fc.K), sqz.to_device(fc.V)
+    i2 = torch.from_numpy(synth.kmeans_init(H, L, c2, seed=62)).cuda()
+    i1 = torch.from_numpy(synth.kmeans_init(H, c2, c1, seed=63)).cuda() if c1 else None
+    i0 = torch.from_numpy(synth.kmeans_init(H, c1, c0, seed=64)).cuda() if c0 else None
+    idx, Kp, Vp, _ = sqz.cluster_keys(K, V, c2, i2, c1, i1, max_iters=20, c0=c0, init0=i0)
+    path = str(tmp_path / "ctx.sqzidx")
+    sqz.save_index(idx, path)
+    got = sqz.load_index(path)
+    assert got.levels == idx.levels == levels
+    for f in ("C2", "N2", "key_off", "perm", "C1", "N1", "child_off", "C0", "N0", "child_off0"):
+        a, b = getattr(idx, f), getattr(got, f)
+        assert (a is None) == (b is None), f
+        if a is not None:
+            assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a,
+                               b.view(torch.int16) if b.dtype == torch.bfloat16 else b), f
+    Q = sqz.to_device(synth.decode_queries(fc.mix, 3, seed=65, dtype=dt))
+    T1 = 1e-3 if levels >= 2 else 0.0
+    s1 = sqz.centroid_lookup(idx, Q, 1 / np.sqrt(d), 2e-4, T1, T0=1e-3 if levels == 3 else 0.0)
+    s2 = sqz.centroid_lookup(got, Q, 1 / np.sqrt(d), 2e-4, T1, T0=1e-3 if levels == 3 else 0.0)
+    torch.cuda.synchronize()
+    assert torch.equal(s1.n_clusters, s2.n_clusters) and torch.equal(s1.n_keys, s2.n_keys)
+    nc = s1.n_clusters.cpu()
+    for b in range(nc.shape[0]):
+        for h in range(H):
+            n = int(nc[b, h])
+            assert torch.equal(s1.clusters[b, h, :n], s2.clusters[b, h, :n])
+    # a dst of another geometry is refused
+    other = sqz.Index.empty(H, d, L, c2 + 1, c1, sqz.sqz_dtype(K), "cuda", c0=c0)
+    with pytest.raises(sqz.SqzError) as e:
+        sqz._check(sqz.lib().sqz_index_load(path.encode(), sqz.ctypes.byref(other.struct()), sqz._stream()))
+    assert e.value.code == sqz.SQZ_ERR_FORMAT
