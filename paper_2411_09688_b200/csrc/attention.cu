@@ -104,13 +104,14 @@ struct Seg {
 
 // Merge of one row's partials by the CTA: O = sum_p e^(lse_p - M) o_p / L,
 // LSE = M + log L.  Thread k < D owns output column k; the
-// partials are read 32 at a time (their lse values and o columns in the same
+// partials are read MB at a time (their lse values and o columns in the same
 // memory round trip) with an online rescale, so the merge is one pass without
 // block barriers.  Every thread forms the same weights in the same order (the
 // result does not depend on which CTA merges or when).
-template <int D>
+// MB partials per memory round trip: 16 for the in-kernel (ticket) merge, 32 for
+// k_merge_rows, whose rows also carry the decode step's user-chunk partials
+template <int D, int MB = 16>
 __device__ void merge_row(const AttnArgs &a, int row, int P) {
-    constexpr int MB = 32;
     const int tid = threadIdx.x;
     if (tid >= D) return;
     MRG_AT(row, 0);
@@ -567,7 +568,7 @@ __global__ void __launch_bounds__(D) k_merge_rows(AttnArgs a) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int row = blockIdx.x;
     const int P = ldcg(a.row_cnt + row);
-    merge_row<D>(a, row, P);
+    merge_row<D, 32>(a, row, P);
     __syncthreads();
     if (threadIdx.x == 0) a.row_cnt[row] = 0;  // self-cleaning (the ticket array)
 }
