@@ -1,4 +1,4 @@
-# merge_row batch (16 in-kernel ticket merge, 32 in k_merge_rows) vs 32 everywhere: decode tests, A/B cfg1/cfg2/cfg5
+# merge_row: short chains + ex2.approx vs the previous build: decode tests, A/B cfg1/cfg2/cfg5
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "decode" > gpurun_out/t_mb.txt 2>&1; echo tests rc=$?
 cp paper_2411_09688_b200/libsqz.so /tmp/libsqz_new.so

@@ -131,20 +131,23 @@ __device__ void merge_row(const AttnArgs &a, int row, int P) {
             lv[j] = in ? ldcg(lse + p) : inu ? ldcg(ulse + (p - P)) : -INFINITY;
             ov[j] = in ? ldcg(op + (size_t)p * D) : inu ? ldcg(uop + (size_t)(p - P) * D) : 0.f;
         }
-        float mt = M;
+        // four short dependency chains (fixed order: the result is deterministic)
+        float m4[4] = {M, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int j = 0; j < MB; ++j) mt = fmaxf(mt, lv[j]);
+        for (int j = 0; j < MB; ++j) m4[j & 3] = fmaxf(m4[j & 3], lv[j]);
+        const float mt = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         MRG_AT(row, 1);
         if (mt == -INFINITY) continue;
-        const float corr = expf(M - mt);  // M = -inf -> 0
-        L *= corr;
-        acc *= corr;
+        const float corr = exp_fast(M - mt);  // M = -inf -> 0
+        float L4[4] = {L * corr, 0.f, 0.f, 0.f}, A4[4] = {acc * corr, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int j = 0; j < MB; ++j) {
-            const float w = expf(lv[j] - mt);  // lse = -inf -> 0
-            L += w;
-            acc = fmaf(w, ov[j], acc);
+            const float w = exp_fast(lv[j] - mt);  // lse = -inf -> 0
+            L4[j & 3] += w;
+            A4[j & 3] = fmaf(w, ov[j], A4[j & 3]);
         }
+        L = (L4[0] + L4[1]) + (L4[2] + L4[3]);
+        acc = (A4[0] + A4[1]) + (A4[2] + A4[3]);
         M = mt;
     }
     const float v = (M == -INFINITY) ? 0.f : acc / L;
