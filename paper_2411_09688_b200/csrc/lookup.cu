@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(NT, MINB) k_lookup_decode(LookupShape s, const
                     lg[u] = in ? s_log[i * rpc + rr] : M;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) e += nw[u] * expf(lg[u] - M);
+                for (int u = 0; u < 4; ++u) e += nw[u] * exp_fast(lg[u] - M);  // O(1) arguments
             }
         e = warp_sum(e);
         if (lane == 0) s_wd[warp][i] = e;
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(NT, MINB) k_lookup_decode(LookupShape s, const
 #pragma unroll
         for (int o = 1; o < NC; o <<= 1) {
             const float m2 = __shfl_xor_sync(FULL, mm, o), d2 = __shfl_xor_sync(FULL, dd, o);
-            md_combine(mm, dd, m2, d2);
+            md_combine_fast(mm, dd, m2, d2);
         }
         if (lane == 0) {
             s_M[i] = mm;
