@@ -526,7 +526,7 @@ int sqz_sparse_attention(const void *Q, int32_t B, int32_t n_q, const void *Kp, 
 // attention kernel attends before it waits for the lookup ([B*H, n_chunks, d]
 // + [B*H, n_chunks] fp32).
 static int user_chunks(int n_u) { return (n_u + attention_user_chunk() - 1) / attention_user_chunk(); }
-static size_t hand_region_bytes(const sqz_index *idx, int B, int n_u) {
+static size_t user_region_bytes(const sqz_index *idx, int B, int n_u) {
     const size_t BH = (size_t)B * idx->H, nch = (size_t)user_chunks(n_u);
     return (BH * nch * (idx->d + 1) * sizeof(float) + 255) & ~(size_t)255;
 }
@@ -537,7 +537,7 @@ int sqz_decode_step_workspace(const sqz_index *idx, int32_t B, int32_t n_u, size
     if (B < 1 || n_u < 0) return fail(SQZ_ERR_INVALID_ARG, "B = %d must be >= 1 and n_u = %d >= 0", B, n_u);
     if (!ws_bytes) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes is NULL");
     *ws_bytes = 256 + ((attn_carve(idx, B, 1, n_u, nullptr).bytes + 511) & ~(size_t)255) +
-                hand_region_bytes(idx, B, n_u) + ((lookup_carve(idx, B, 1, nullptr).bytes + 511) & ~(size_t)255);
+                user_region_bytes(idx, B, n_u) + ((lookup_carve(idx, B, 1, nullptr).bytes + 511) & ~(size_t)255);
     return SQZ_OK;
 }
 
@@ -563,8 +563,8 @@ int sqz_decode_step(const sqz_index *idx, const void *Q, int32_t B, const void *
     if (ws_bytes < need) return fail(SQZ_ERR_INVALID_ARG, "ws_bytes = %zu < required %zu", ws_bytes, need);
     char *base = align_ws(ws);
     const size_t attn_b = (attn_carve(idx, B, 1, n_u, nullptr).bytes + 511) & ~(size_t)255;
-    char *hand_ws = base + attn_b;
-    char *look_ws = hand_ws + hand_region_bytes(idx, B, n_u);
+    char *user_ws = base + attn_b;
+    char *look_ws = user_ws + user_region_bytes(idx, B, n_u);
     const size_t look_b = (lookup_carve(idx, B, 1, nullptr).bytes + 511) & ~(size_t)255;
     const bool debug = sel->dbg_S || sel->dbg_S1 || sel->dbg_lse || sel->l1_surv || sel->dbg_S0 ||
                        sel->l0_surv;
@@ -580,7 +580,7 @@ int sqz_decode_step(const sqz_index *idx, const void *Q, int32_t B, const void *
         static const bool no_user = std::getenv("SQZ_STEP_NO_USER") != nullptr;  // A/B knob
         const size_t BH = (size_t)B * H;
         const int nch = no_user ? 0 : user_chunks(n_u);
-        float *up_o = reinterpret_cast<float *>(hand_ws);
+        float *up_o = reinterpret_cast<float *>(user_ws);
         float *up_lse = up_o + BH * nch * idx->d;
         LookupWs w = lookup_carve(idx, B, 1, look_ws);
         LookupShape s{B, idx->H, 1, idx->d, idx->dtype, lp->scale};
