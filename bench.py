@@ -523,10 +523,14 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                                      dtype=dt)[:, heads], dev).view(n_inputs, B, Hl, n_q, d)
         Ku, Vu = (sqz.to_device(a[:, heads], dev)
                   for a in synth.user_kv(mix, B, n_u, seed=5000 + cno, dtype=dt))
+    # one user-KV cache [2 (K, V), B, H, n_u, d]: the end-to-end step appends a token's K
+    # and V rows with ONE device copy
+    KVu = torch.stack([Ku, Vu])
+    Ku, Vu = KVu[0], KVu[1]
     Ku0 = Ku[:, par_head].contiguous().cpu() if rank == 0 else None
     Vu0 = Vu[:, par_head].contiguous().cpu() if rank == 0 else None
     if shard == "clusters" and rank != 0:
-        Ku = Vu = None  # the user KV partial is computed once, on rank 0
+        Ku = Vu = KVu = None  # the user KV partial is computed once, on rank 0
     n_u_r = 0 if Ku is None else n_u
     Bc = Qc.shape[0]
     # ---- calibration of the global thresholds (R12, R13) ----
@@ -738,11 +742,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
     hout = torch.empty(out_b, dtype=torch.uint8, **pin)
     d2h = out_b
 
+    kv_dst = None if kv_new is None else KVu[(slice(None),) + kv_new]  # [2, B, H, rows, d]
+
     def e2e_step(i):
         din.copy_(hin[i % n_inputs], non_blocking=True)
-        if kv_new is not None:
-            Ku[kv_new].copy_(din[q_b:q_b + kv_b].view(Ku.dtype).view(Ku[kv_new].shape))
-            Vu[kv_new].copy_(din[q_b + kv_b:].view(Vu.dtype).view(Vu[kv_new].shape))
+        if kv_new is not None:  # the staged K rows then V rows, as [2, B, H, rows, d]
+            kv_dst.copy_(din[q_b:].view(KVu.dtype).view(kv_dst.shape))
         step_into(dQ, O_e, LSE_e)
         hout.copy_(dout, non_blocking=True)
 
